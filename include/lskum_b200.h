@@ -1,0 +1,115 @@
+/* lskum_b200.h — B200-specific extensions to the drop-in C ABI (lskum/lskum.h).
+ *
+ * The reference keeps part of its interface in C++ only (run_fixed_point,
+ * the per-phase operators, partition_cloud).  Those are exposed here as plain
+ * C so test harnesses, the bench and per-rank launchers can reach the same
+ * boundaries without C++ types.  Each entry cites the reference interface it
+ * mirrors.  All calls are synchronous; device memory never outlives the call
+ * (sessions own theirs until lskum_b200_session_destroy).
+ *
+ * Extra config keys accepted by lskum_config_set (reference config.cpp:98-131
+ * rejects unknown keys; these are additive):
+ *   device=N          CUDA device ordinal for single-GPU runs (default 0)
+ *   gpus=N            number of device domains (RCB parts on distinct devices
+ *                     when available; default 1)
+ *   fp_mode=fast|strict  strict = the reference's exact operation sequence in
+ *                     the flux kernel; fast = deduplicated x/y reconstruction
+ *                     (default fast).  Sweeps, time step, update and residue
+ *                     are bitwise-reference in both modes.
+ *   chunk=N           iterations per captured CUDA graph (default 16)
+ */
+#ifndef LSKUM_B200_H
+#define LSKUM_B200_H
+
+#include "lskum/lskum.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- backend / device info ---- */
+const char* lskum_b200_backend(void);
+int lskum_b200_device_count(int* out);
+
+/* ---- clouds on plain arrays (PointCloud(records), reference cloud.hpp:42-74) ---- */
+int lskum_b200_cloud_from_arrays(int32_t n, const double* x, const double* y,
+                                 const uint8_t* kind, const double* nx, const double* ny,
+                                 const int64_t* offsets, const int32_t* nbrs,
+                                 lskum_cloud** out);
+int lskum_b200_cloud_nnz(const lskum_cloud* cloud, int64_t* out);
+/* Any output pointer may be NULL. */
+int lskum_b200_cloud_geometry(const lskum_cloud* cloud, double* x, double* y, uint8_t* kind,
+                              double* nx, double* ny, int64_t* offsets, int32_t* nbrs);
+/* PointCloud::reset_store (reference cloud.cpp:90-92); layout 0 = aos, 1 = soa. */
+int lskum_b200_cloud_reset_store(lskum_cloud* cloud, int layout);
+/* Whole 21-slot store as point-major (AoS) n*21 doubles, whatever the layout. */
+int lskum_b200_cloud_get_fields(const lskum_cloud* cloud, double* aos);
+int lskum_b200_cloud_set_fields(lskum_cloud* cloud, const double* aos);
+
+/* ---- fixed-point driver (run_fixed_point, reference runtime.hpp:103) ----
+ * Iterates from the primitives already in the cloud's store (no free-stream
+ * reset) — the C++-host entry the reference tests call directly. */
+int lskum_b200_run_fixed_point(lskum_cloud* cloud, const lskum_config* cfg,
+                               lskum_result** out);
+/* 1-based iteration at which a failed run aborted (0 if none / not applicable). */
+int lskum_b200_result_abort_iteration(const lskum_result* result);
+int lskum_b200_result_wall_ms(const lskum_result* result, int iteration, double* out);
+
+/* ---- per-phase device operators (reference kernels.hpp:25-63) ----
+ * Each runs one phase over every point of `cloud` on the GPU, reading and
+ * writing the cloud's host field store (uploaded and downloaded around the
+ * kernel).  Same error codes and messages as the reference phase. */
+typedef struct {
+  double gamma;   /* GasModel::gamma */
+  double cfl;     /* KernelParams::cfl */
+  double det_tol; /* KernelParams::det_tol */
+  int fp_mode;    /* 0 = fast, 1 = strict (flux only) */
+} lskum_b200_params;
+
+int lskum_b200_op_q_variables(lskum_cloud* cloud, const lskum_b200_params* p);
+/* scratch: n*8 doubles (qx[4], qy[4] per point), as q_derivatives_kernel. */
+int lskum_b200_op_q_derivatives(lskum_cloud* cloud, const lskum_b200_params* p,
+                                double* scratch);
+int lskum_b200_op_publish(lskum_cloud* cloud, const double* scratch);
+int lskum_b200_op_flux_residual(lskum_cloud* cloud, const lskum_b200_params* p);
+/* axis 0/1 = x/y, sign 0/1 = plus/minus; first != 0 zeroes the accumulator. */
+int lskum_b200_op_flux_direction(lskum_cloud* cloud, const lskum_b200_params* p, int axis,
+                                 int sign, int first);
+int lskum_b200_op_timestep(lskum_cloud* cloud, const lskum_b200_params* p);
+int lskum_b200_op_state_update(lskum_cloud* cloud, const lskum_b200_params* p);
+/* deterministic_reduce (reference reduce.hpp:11-17) evaluated on the device. */
+int lskum_b200_reduce(const double* values, int64_t n, double* out);
+
+/* ---- partitioning (partition_cloud, reference partition.hpp:27) ----
+ * owner[i] = part of point i; ghosts of part p are ghosts[ghost_off[p]..ghost_off[p+1]). */
+int lskum_b200_partition(const lskum_cloud* cloud, int n_parts, int32_t* owner,
+                         int64_t* ghost_off, int32_t* ghosts, int64_t ghost_cap);
+
+/* ---- device-resident sessions (bench.py, per-rank launchers) ----
+ * create: validate, free-stream initialise (unless from_state != 0), upload,
+ *         build the CUDA graphs; capacity = max iterations over the session.
+ * iterate: run n more iterations; *device_ms = CUDA-event time on the
+ *          session's stream around exactly those iterations.
+ * download: copy the 21-slot store back into the cloud. */
+typedef struct lskum_b200_session lskum_b200_session;
+int lskum_b200_session_create(lskum_cloud* cloud, const lskum_config* cfg, int capacity,
+                              int from_state, lskum_b200_session** out);
+int lskum_b200_session_iterate(lskum_b200_session* s, int n, double* device_ms);
+int lskum_b200_session_residues(const lskum_b200_session* s, double* out, int cap,
+                                int* n_out);
+/* Per-kernel device seconds accumulated so far (globaltimer, per launch). */
+int lskum_b200_session_kernel_count(const lskum_b200_session* s);
+const char* lskum_b200_session_kernel_name(const lskum_b200_session* s, int index);
+int lskum_b200_session_kernel_stats(const lskum_b200_session* s, int index, double* seconds,
+                                    int64_t* launches);
+/* Kernel launches per iteration and the CUDA stream (cudaStream_t as integer). */
+int lskum_b200_session_info(const lskum_b200_session* s, int* launches_per_iter,
+                            uint64_t* stream);
+int lskum_b200_session_download(lskum_b200_session* s);
+void lskum_b200_session_destroy(lskum_b200_session* s);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* LSKUM_B200_H */

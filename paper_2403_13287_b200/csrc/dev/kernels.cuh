@@ -1,0 +1,640 @@
+// kernels.cuh — sm_100a kernels of one LSKUM fixed-point iteration.
+//
+// Device-side replacement for the reference's phase kernels
+// (/root/reference/proj/src/core/kernels.cpp:68-223) and residue reduction
+// (runtime.cpp:251-269, reduce.hpp:11-17).  Per iteration (order 2, n_inner s):
+//
+//   k_sweep   x s   q, dq[b] -> dq[1-b]      one thread per point, bitwise
+//   k_flux          q[a], dq -> res -> dt -> prim' -> q[1-a], mag
+//                   (flux residual + local time step + forward Euler + wall
+//                    slip + next q-variables + residue summand, fused)
+//   k_tree_partial, k_tree_final   midpoint-tree sum of mag, bitwise
+//
+// Data layout in HBM (structure of arrays of 32-byte records):
+//   xy  double2[n]        nrm double2[n]     kind u8[n]     part u8[n]
+//   off int32[n+1]        nbr int32[nnz]     mind double[n] (geometry, per run)
+//   prim D4[n]            q[2] D4[n]         dq[2] D4[2n]  ({qx}, {qy} per point)
+//   res D4[n], dt double[n] (written on the copy-back iteration only), mag double[n]
+// Every D4 gather is one 256-bit LDG (one 32-byte sector).
+#pragma once
+
+#include <cstdint>
+
+#include "dmath.cuh"
+
+namespace lskd {
+
+constexpr unsigned long long kNoErr = ~0ull;
+enum : unsigned { PH_QVAR = 0, PH_SWEEP = 1, PH_FLUX = 2, PH_UPDATE = 3, PH_RESIDUE = 4 };
+enum : unsigned { KIND_INTERIOR = 0, KIND_WALL = 1, KIND_OUTER = 2 };
+constexpr unsigned kSolveSlot = 0xFFFFFu;  // "after every neighbour" in the error key
+
+// Error key: min over failures reproduces the reference's first failure
+// (phase order, lowest partition, ascending point id, direction Gx+..Gy-,
+// neighbour position) — runtime.cpp:115-118, kernels.cpp:122, :37-64.
+__device__ __forceinline__ unsigned long long err_key(unsigned phase, unsigned part,
+                                                      unsigned point, unsigned dir,
+                                                      unsigned j) {
+  return (static_cast<unsigned long long>(phase & 7u) << 61) |
+         (static_cast<unsigned long long>(part & 0xFFu) << 53) |
+         (static_cast<unsigned long long>(point & 0x7FFFFFFFu) << 22) |
+         (static_cast<unsigned long long>(dir & 3u) << 20) | (j & 0xFFFFFu);
+}
+
+struct KTimer {
+  unsigned long long t0, t1;
+  unsigned int done, pad;
+  unsigned long long total_ns, launches;
+};
+
+enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_RESIDUE = 3, KT_COUNT = 4 };
+
+// Device control block (one per domain).
+struct Ctl {
+  unsigned long long err_key;
+  int err_iter;  // 0-based iteration of the failure
+  int iter;      // 0-based index of the iteration in flight
+  int diag_iter; // iteration whose res/dt are kept for copy-back
+  int pad;
+  KTimer kt[KT_COUNT];
+};
+
+struct Geo {
+  const double2* xy;
+  const double2* nrm;
+  const std::uint8_t* kind;
+  const std::uint8_t* part;
+  const int* off;
+  const int* nbr;
+  const double* mind;
+  int n;
+};
+
+struct Gas {
+  double gamma, gm1, inv_gm1, cfl, det_tol;
+};
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key) {
+  atomicMin(&ctl->err_key, key);
+  *reinterpret_cast<volatile int*>(&ctl->err_iter) = ctl->iter;
+}
+
+// ---- per-kernel device timing (globaltimer; one record per kernel class) ----
+__device__ __forceinline__ void ktimer_begin(Ctl* ctl, int k) {
+  if (threadIdx.x == 0) atomicMin(&ctl->kt[k].t0, globaltimer());
+}
+// Call after a __syncthreads() that every thread of the block reaches.
+__device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* iter_t0) {
+  if (threadIdx.x == 0) {
+    atomicMax(&ctl->kt[k].t1, globaltimer());
+    __threadfence();
+    const unsigned nblocks = gridDim.x * gridDim.y;
+    if (atomicAdd(&ctl->kt[k].done, 1u) == nblocks - 1) {
+      __threadfence();
+      const unsigned long long t0 = atomicExch(&ctl->kt[k].t0, ~0ull);
+      const unsigned long long t1 = atomicExch(&ctl->kt[k].t1, 0ull);
+      ctl->kt[k].done = 0;
+      ctl->kt[k].total_ns += t1 - t0;
+      ctl->kt[k].launches += 1;
+      if (iter_t0) iter_t0[ctl->iter] = t0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Geometry: nearest-neighbour distance per point (the min over the stencil in
+// local_timestep_kernel, kernels.cpp:170-175) — constant for a run.
+__global__ void k_min_dist(Geo g, double* mind) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const double2 pi = g.xy[i];
+  double best = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+  for (int e = g.off[i]; e < g.off[i + 1]; ++e) {
+    const double2 pn = g.xy[g.nbr[e]];
+    const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+    const double d = sqrt(X::add(X::mul(dx, dx), X::mul(dy, dy)));
+    best = d < best ? d : best;  // std::min(best, d)
+  }
+  mind[i] = best;
+}
+
+// q_variables over all points (kernels.cpp:68-80); used for the first
+// iteration and by the per-phase operator.  Afterwards q is produced by k_flux.
+__global__ void k_qvar(Geo g, const D4* prim, D4* q, Gas gas, Ctl* ctl) {
+  ktimer_begin(ctl, KT_QVAR);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < g.n) {
+    const D4 s = ld4_rw(prim + i);
+    if (!(s.a > 0.0) || !(s.d > 0.0)) {
+      raise_err(ctl, err_key(PH_QVAR, g.part[i], i, 0, 0));
+    } else {
+      st4(q + i, q_from_prim(s.a, s.b, s.c, s.d, gas.gm1));
+    }
+  }
+  __syncthreads();
+  ktimer_end(ctl, KT_QVAR, nullptr);
+}
+
+// One Jacobi sweep of the derivative system (kernels.cpp:82-106): bitwise
+// equal to the reference (exact operation sequence, ascending stencil order).
+__global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
+                                               const D4* __restrict__ dq_in,
+                                               D4* __restrict__ dq_out, Gas gas, Ctl* ctl,
+                                               unsigned long long* iter_t0) {
+  __shared__ int s_skip;
+  ktimer_begin(ctl, KT_SWEEP);
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (!s_skip && i < g.n) {
+    const double2 pi = g.xy[i];
+    const D4 qi = ld4(q + i), qxi = ld4(dq_in + 2 * i), qyi = ld4(dq_in + 2 * i + 1);
+    double sxx = 0.0, sxy = 0.0, syy = 0.0;
+    double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
+    const int e1 = g.off[i + 1];
+    for (int e = g.off[i]; e < e1; ++e) {
+      const int nb = g.nbr[e];
+      const double2 pn = g.xy[nb];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const D4 qn = ld4(q + nb), qxn = ld4(dq_in + 2 * nb), qyn = ld4(dq_in + 2 * nb + 1);
+      sxx = X::add(sxx, X::mul(dx, dx));
+      sxy = X::add(sxy, X::mul(dx, dy));
+      syy = X::add(syy, X::mul(dy, dy));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double df = X::sub(corrected<true>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy),
+                                 corrected<true>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy));
+        bx[c] = X::add(bx[c], X::mul(dx, df));
+        by[c] = X::add(by[c], X::mul(dy, df));
+      }
+    }
+    const double det = X::sub(X::mul(sxx, syy), X::mul(sxy, sxy));
+    if (!(det > gas.det_tol)) {
+      raise_err(ctl, err_key(PH_SWEEP, g.part[i], i, 0, 0));
+    } else {
+      D4 fx, fy;
+      fx.a = X::sub(X::mul(syy, bx[0]), X::mul(sxy, by[0])) / det;
+      fx.b = X::sub(X::mul(syy, bx[1]), X::mul(sxy, by[1])) / det;
+      fx.c = X::sub(X::mul(syy, bx[2]), X::mul(sxy, by[2])) / det;
+      fx.d = X::sub(X::mul(syy, bx[3]), X::mul(sxy, by[3])) / det;
+      fy.a = X::sub(X::mul(sxx, by[0]), X::mul(sxy, bx[0])) / det;
+      fy.b = X::sub(X::mul(sxx, by[1]), X::mul(sxy, bx[1])) / det;
+      fy.c = X::sub(X::mul(sxx, by[2]), X::mul(sxy, bx[2])) / det;
+      fy.d = X::sub(X::mul(sxx, by[3]), X::mul(sxy, bx[3])) / det;
+      st4(dq_out + 2 * i, fx);
+      st4(dq_out + 2 * i + 1, fy);
+    }
+  }
+  __syncthreads();
+  ktimer_end(ctl, KT_SWEEP, iter_t0);
+}
+
+// ---------------------------------------------------------------------------
+// Flux residual (+ fused update).  W lanes cooperate on one point, one lane
+// per stencil neighbour (pair): each pair's two reconstructions q~ -> prim and
+// split fluxes are computed once and shared by its x- and y-direction terms
+// (bitwise neutral: the reference recomputes identical values per direction).
+// Lanes then transpose through shared memory so each least-squares
+// accumulator is summed in ascending neighbour order, exactly as
+// directional_term does (kernels.cpp:37-64).
+struct PairRec {
+  double dx, dy;
+  double dg[4][4];  // Delta G for Gx+, Gx-, Gy+, Gy- (only member directions valid)
+};
+
+struct FluxArgs {
+  Geo g;
+  Gas gas;
+  const D4* q;      // q of this iteration (read)
+  const D4* dq;     // published derivatives (read)
+  D4* prim;         // FUSED: updated in place; OP: unused
+  D4* q_next;       // FUSED: q of the next iteration
+  D4* res;          // OP: accumulator in/out; FUSED: written on diag iteration
+  double* dt;       // FUSED: written on diag iteration
+  double* mag;      // FUSED: (dt*res0)^2 per point for the residue
+  Ctl* ctl;
+  unsigned long long* iter_t0;
+  int kcap;         // shared-memory stencil capacity per point
+  int mask;         // OP: directions to evaluate (bit d); FUSED: 0xF
+  int first;        // OP: zero the accumulator before adding
+};
+
+__host__ __device__ constexpr int flux_points_per_block(int W) { return W >= 32 ? 8 : (W >= 16 ? 16 : 32); }
+
+template <int W, bool S, bool FUSED>
+__global__ void __launch_bounds__(W * flux_points_per_block(W))
+    k_flux(FluxArgs a) {
+  constexpr int P = flux_points_per_block(W);
+  constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
+  constexpr int NC = 16 / NOWN;                 // components per owning lane
+  using A = Ar<S>;
+  extern __shared__ double smem[];
+  PairRec* recs = reinterpret_cast<PairRec*>(smem);               // [P][kcap]
+  double* terms = smem + static_cast<size_t>(P) * a.kcap * (sizeof(PairRec) / 8);  // [P][16]
+  __shared__ int s_skip;
+
+  ktimer_begin(a.ctl, KT_FLUX);
+  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->err_key) != kNoErr;
+  __syncthreads();
+  const int lane = threadIdx.x % W;
+  const int slot = threadIdx.x / W;
+  const int i = blockIdx.x * P + slot;
+  const Geo& g = a.g;
+  const bool live = !s_skip && i < g.n && g.kind[i] != KIND_OUTER;
+  int k = 0, e0 = 0;
+  if (live) {
+    e0 = g.off[i];
+    k = g.off[i + 1] - e0;
+  }
+  PairRec* my = recs + static_cast<size_t>(slot) * a.kcap;
+
+  // ---- phase A: one lane per (point, neighbour) pair ----
+  if (live) {
+    const double2 pi = g.xy[i];
+    const D4 qi = ld4(a.q + i), qxi = ld4(a.dq + 2 * i), qyi = ld4(a.dq + 2 * i + 1);
+    for (int j = lane; j < k; j += W) {
+      const int nb = g.nbr[e0 + j];
+      const double2 pn = g.xy[nb];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+      PairRec& r = my[j];
+      r.dx = dx;
+      r.dy = dy;
+      const unsigned dfirst = dx <= 0.0 ? 0u : 1u;
+      double ti[4], tn[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
+        tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
+      }
+      if (!(ti[3] < 0.0) || !(tn[3] < 0.0)) {
+        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+        continue;
+      }
+      double ri, u1i, u2i, pri, rn, u1n, u2n, prn;
+      prim_from_q<S>(ti[0], ti[1], ti[2], ti[3], a.gas.inv_gm1, a.gas.gm1, ri, u1i, u2i, pri);
+      prim_from_q<S>(tn[0], tn[1], tn[2], tn[3], a.gas.inv_gm1, a.gas.gm1, rn, u1n, u2n, prn);
+      if (!(ri > 0.0) || !(pri > 0.0) || !(rn > 0.0) || !(prn > 0.0)) {
+        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+        continue;
+      }
+      const FluxState fi = flux_state<S>(ri, u1i, u2i, pri, a.gas.inv_gm1, a.gas.gm1);
+      const FluxState fn = flux_state<S>(rn, u1n, u2n, prn, a.gas.inv_gm1, a.gas.gm1);
+      const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
+      const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
+      double gi[4], gn[4];
+      if (xp || xm) {
+        const AxisTerms ai = axis_terms<S>(fi, 0), an = axis_terms<S>(fn, 0);
+        if (xp) {
+          split_flux<S>(fi, ai, 0, false, gi);
+          split_flux<S>(fn, an, 0, false, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
+        }
+        if (xm) {
+          split_flux<S>(fi, ai, 0, true, gi);
+          split_flux<S>(fn, an, 0, true, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
+        }
+      }
+      if (yp || ym) {
+        const AxisTerms ai = axis_terms<S>(fi, 1), an = axis_terms<S>(fn, 1);
+        if (yp) {
+          split_flux<S>(fi, ai, 1, false, gi);
+          split_flux<S>(fn, an, 1, false, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
+        }
+        if (ym) {
+          split_flux<S>(fi, ai, 1, true, gi);
+          split_flux<S>(fn, an, 1, true, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[3][c] = X::sub(gn[c], gi[c]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase B: ordered least-squares sums + 2x2 solve per direction ----
+  if (live && lane < NOWN) {
+    const int d = lane / (4 / NC);                // direction owned
+    const int c0 = (lane % (4 / NC)) * NC;        // first component owned
+    if (a.mask & (1 << d)) {
+      double sxx = 0.0, sxy = 0.0, syy = 0.0, bx[NC], by[NC];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) bx[cc] = by[cc] = 0.0;
+      for (int j = 0; j < k; ++j) {
+        const double dx = my[j].dx, dy = my[j].dy;
+        const double dd = d < 2 ? dx : dy;
+        const bool member = (d & 1) ? dd >= 0.0 : dd <= 0.0;
+        if (!member) continue;
+        sxx = A::add(sxx, A::mul(dx, dx));
+        sxy = A::add(sxy, A::mul(dx, dy));
+        syy = A::add(syy, A::mul(dy, dy));
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const double df = my[j].dg[d][c0 + cc];
+          bx[cc] = A::add(bx[cc], A::mul(dx, df));
+          by[cc] = A::add(by[cc], A::mul(dy, df));
+        }
+      }
+      const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
+      if (!(det > a.gas.det_tol)) {
+        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, d, kSolveSlot));
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const double t = d < 2 ? A::sub(A::mul(syy, bx[cc]), A::mul(sxy, by[cc])) / det
+                                 : A::sub(A::mul(sxx, by[cc]), A::mul(sxy, bx[cc])) / det;
+          terms[slot * 16 + d * 4 + c0 + cc] = t;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase C: one thread per point ----
+  if (threadIdx.x < P && !s_skip) {
+    const int ip = blockIdx.x * P + threadIdx.x;
+    if (ip < g.n) {
+      const double* t = terms + threadIdx.x * 16;
+      const bool outer = g.kind[ip] == KIND_OUTER;
+      if constexpr (!FUSED) {
+        if (!outer) {
+          D4 acc = a.first ? D4{0.0, 0.0, 0.0, 0.0} : ld4_rw(a.res + ip);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            if (!(a.mask & (1 << d))) continue;
+            acc.a = X::add(acc.a, t[d * 4 + 0]);
+            acc.b = X::add(acc.b, t[d * 4 + 1]);
+            acc.c = X::add(acc.c, t[d * 4 + 2]);
+            acc.d = X::add(acc.d, t[d * 4 + 3]);
+          }
+          st4(a.res + ip, acc);
+        }
+      } else {
+        const int it = a.ctl->iter;
+        const bool diag = it == a.ctl->diag_iter;
+        if (outer) {
+          st4(a.q_next + ip, ld4(a.q + ip));
+          a.mag[ip] = 0.0;
+          if (diag) a.dt[ip] = 0.0;
+        } else {
+          // residual: zero, then Gx+, Gx-, Gy+, Gy- (kernels.cpp:124-138)
+          double r[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            r[c] = X::add(X::add(X::add(X::add(0.0, t[c]), t[4 + c]), t[8 + c]), t[12 + c]);
+          const D4 s = ld4_rw(a.prim + ip);
+          // local time step (kernels.cpp:160-182)
+          const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
+          const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
+          const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
+          // forward Euler on the conserved state (kernels.cpp:184-219)
+          double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
+          double en = X::add(s.d / a.gas.gm1,
+                             X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
+          m = X::sub(m, X::mul(dt, r[0]));
+          mx = X::sub(mx, X::mul(dt, r[1]));
+          my_ = X::sub(my_, X::mul(dt, r[2]));
+          en = X::sub(en, X::mul(dt, r[3]));
+          bool ok = m > 0.0;
+          double u1 = 0.0, u2 = 0.0, p = 0.0;
+          if (ok) {
+            u1 = mx / m;
+            u2 = my_ / m;
+            p = X::mul(a.gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
+            ok = p > 0.0;
+          }
+          if (!ok) {
+            // keep the failing conserved value for the diagnostic message
+            a.res[ip] = D4{m > 0.0 ? p : m, m > 0.0 ? 1.0 : 0.0, 0.0, 0.0};
+            raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], ip, 0, 0));
+          } else {
+            if (g.kind[ip] == KIND_WALL) {
+              const double2 nv = g.nrm[ip];
+              const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
+              u1 = X::sub(u1, X::mul(un, nv.x));
+              u2 = X::sub(u2, X::mul(un, nv.y));
+            }
+            st4(a.prim + ip, D4{m, u1, u2, p});
+            st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
+            const double dm = X::mul(dt, r[0]);
+            a.mag[ip] = X::mul(dm, dm);
+            if (diag) {
+              st4(a.res + ip, D4{r[0], r[1], r[2], r[3]});
+              a.dt[ip] = dt;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+}
+
+// ---------------------------------------------------------------------------
+// Per-phase operators for the reference operator API (kernels.hpp:52-59).
+__global__ void k_op_timestep(Geo g, const D4* prim, double* dt, Gas gas) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  if (g.kind[i] == KIND_OUTER) {
+    dt[i] = 0.0;
+    return;
+  }
+  const D4 s = ld4(prim + i);
+  const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
+  const double sound = sqrt(X::mul(gas.gamma, s.d) / s.a);
+  dt[i] = X::mul(gas.cfl, g.mind[i]) / X::add(speed, sound);
+}
+
+__global__ void k_op_update(Geo g, D4* prim, const D4* res, const double* dt, Gas gas,
+                            Ctl* ctl, double* diag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n || g.kind[i] == KIND_OUTER) return;
+  const D4 s = ld4_rw(prim + i);
+  if (!(s.a > 0.0) || !(s.d > 0.0)) {  // conserved_from_primitives require_valid
+    raise_err(ctl, err_key(PH_QVAR, g.part[i], i, 0, 0));
+    return;
+  }
+  const D4 r = ld4(res + i);
+  const double h = dt[i];
+  double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
+  double en = X::add(s.d / gas.gm1,
+                     X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
+  m = X::sub(m, X::mul(h, r.a));
+  mx = X::sub(mx, X::mul(h, r.b));
+  my_ = X::sub(my_, X::mul(h, r.c));
+  en = X::sub(en, X::mul(h, r.d));
+  if (!(m > 0.0)) {
+    diag[2 * i] = m;
+    diag[2 * i + 1] = 0.0;
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
+    return;
+  }
+  double u1 = mx / m, u2 = my_ / m;
+  const double p = X::mul(gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
+  if (!(p > 0.0)) {
+    diag[2 * i] = p;
+    diag[2 * i + 1] = 1.0;
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
+    return;
+  }
+  if (g.kind[i] == KIND_WALL) {
+    const double2 nv = g.nrm[i];
+    const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
+    u1 = X::sub(u1, X::mul(un, nv.x));
+    u2 = X::sub(u2, X::mul(un, nv.y));
+  }
+  st4(prim + i, D4{m, u1, u2, p});
+}
+
+// ---------------------------------------------------------------------------
+// Residue: the reference's recursive midpoint-tree sum over ids [0, n)
+// (reduce.hpp:11-17), evaluated exactly.  Node (d, k) of the tree is found by
+// replaying the midpoint splits along k's bits; a node of size <= 1 is a leaf.
+__device__ __forceinline__ void tree_node(long long lo0, long long hi0, int depth,
+                                          long long k, long long& lo, long long& hi) {
+  lo = lo0;
+  hi = hi0;
+  for (int l = depth - 1; l >= 0; --l) {
+    const long long mid = lo + (hi - lo) / 2;
+    if ((k >> l) & 1) lo = mid;
+    else hi = mid;
+  }
+}
+
+__device__ double tree_sum(const double* v, long long lo, long long hi) {
+  const long long len = hi - lo;
+  if (len <= 0) return 0.0;
+  if (len == 1) return v[lo];
+  if (len == 2) return X::add(v[lo], v[lo + 1]);
+  if (len == 3) return X::add(v[lo], X::add(v[lo + 1], v[lo + 2]));
+  const long long mid = lo + len / 2;
+  return X::add(tree_sum(v, lo, mid), tree_sum(v, mid, hi));
+}
+
+// Combines 2^levels children (val/sz in ping) up `levels` levels; T threads.
+template <int T>
+__device__ void tree_combine(double* val, long long* sz, double* val2, long long* sz2,
+                             int levels) {
+  double* cv = val;
+  long long* cs = sz;
+  double* nv = val2;
+  long long* ns = sz2;
+  for (int l = levels; l > 0; --l) {
+    const int half = 1 << (l - 1);
+    for (int t = threadIdx.x; t < half; t += T) {
+      const long long sl = cs[2 * t], sr = cs[2 * t + 1];
+      const long long ps = sl + sr;
+      double v;
+      if (ps <= 0) v = 0.0;
+      else if (ps == 1) v = sr == 1 ? cv[2 * t + 1] : cv[2 * t];
+      else v = X::add(cv[2 * t], cv[2 * t + 1]);
+      nv[t] = v;
+      ns[t] = ps;
+    }
+    __syncthreads();
+    double* tv = cv; cv = nv; nv = tv;
+    long long* ts = cs; cs = ns; ns = ts;
+  }
+  if (threadIdx.x == 0) {
+    val[0] = cv[0];
+    sz[0] = cs[0];
+  }
+  __syncthreads();
+}
+
+constexpr int kTreeThreads = 256;
+constexpr int kTreeThreadLevels = 8;
+
+// Stage 1: block b reduces node (d1, b); its 256 threads take the nodes 8
+// levels further down and sum them serially by the same recursion.
+__global__ void __launch_bounds__(kTreeThreads)
+    k_tree_partial(const double* v, long long n, int d1, double* part_val, long long* part_sz,
+                   Ctl* ctl) {
+  __shared__ double sv[2][kTreeThreads];
+  __shared__ long long ss[2][kTreeThreads];
+  __shared__ int s_skip;
+  ktimer_begin(ctl, KT_RESIDUE);
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  __syncthreads();
+  if (!s_skip) {
+    long long lo, hi, tlo, thi;
+    tree_node(0, n, d1, blockIdx.x, lo, hi);
+    tree_node(lo, hi, kTreeThreadLevels, threadIdx.x, tlo, thi);
+    sv[0][threadIdx.x] = tree_sum(v, tlo, thi);
+    ss[0][threadIdx.x] = thi - tlo;
+  }
+  __syncthreads();
+  if (!s_skip) {
+    tree_combine<kTreeThreads>(sv[0], ss[0], sv[1], ss[1], kTreeThreadLevels);
+    if (threadIdx.x == 0) {
+      part_val[blockIdx.x] = sv[0][0];
+      part_sz[blockIdx.x] = ss[0][0];
+    }
+  }
+  __syncthreads();
+  ktimer_end(ctl, KT_RESIDUE, nullptr);
+}
+
+// Stage 2: one block folds the 2^d1 partials, forms sqrt(sum)/n and records
+// the history entry (runtime.cpp:251-269); non-finite -> positivity error.
+__global__ void __launch_bounds__(1024)
+    k_tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
+                 double* history, unsigned long long* iter_t1, Ctl* ctl) {
+  __shared__ double sv[2][1024];
+  __shared__ long long ss[2][1024];
+  __shared__ int s_skip;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  __syncthreads();
+  if (s_skip) return;
+  const int m = 1 << d1;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    sv[0][t] = part_val[t];
+    ss[0][t] = part_sz[t];
+  }
+  __syncthreads();
+  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
+  if (threadIdx.x == 0) {
+    const double res = sqrt(sv[0][0]) / static_cast<double>(n);
+    const int it = ctl->iter;
+    if (!isfinite(res)) {
+      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0));
+    } else {
+      if (history) history[it] = res;
+      if (iter_t1) iter_t1[it] = globaltimer();
+      ctl->iter = it + 1;
+    }
+  }
+}
+
+// Plain tree sum of an arbitrary vector (lskum_b200_reduce): same two stages
+// without the history bookkeeping.
+__global__ void k_tree_result(const double* part_val, const long long* part_sz, int d1,
+                              double* out) {
+  __shared__ double sv[2][1024];
+  __shared__ long long ss[2][1024];
+  const int m = 1 << d1;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    sv[0][t] = part_val[t];
+    ss[0][t] = part_sz[t];
+  }
+  __syncthreads();
+  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
+  if (threadIdx.x == 0) *out = sv[0][0];
+}
+
+__global__ void k_copy_d4(const D4* src, D4* dst, long long count) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < count) st4(dst + i, ld4(src + i));
+}
+
+}  // namespace lskd

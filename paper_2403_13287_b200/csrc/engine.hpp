@@ -1,0 +1,58 @@
+// engine.hpp — the boundary between the C++ host layer and the CUDA engine.
+//
+// The host (host/*.cpp, g++) owns clouds, settings, validation and
+// partitioning; the engine (dev/engine.cu, nvcc, sm_100a) owns device memory,
+// streams, CUDA graphs and kernels.  Everything crossing this header is plain
+// host data; device pointers never leave engine.cu.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "host/core.hpp"
+
+namespace lskb {
+
+struct EngineSpec {
+  double gamma = 1.4, cfl = 0.5, det_tol = 0.0;
+  int iters = 0, inner = 3, order = 2;
+  int fp_mode = 0;  // 0 fast, 1 strict
+  int chunk = 16;   // iterations per captured graph
+  int device = 0;
+  // Partition of each point (reference error tie-break, runtime.cpp:115-118).
+  std::vector<std::uint8_t> part_of;
+};
+
+// Config check + stencil screening gate + bisection (host side of a run).
+EngineSpec prepare_run(const PointSet& ps, const Settings& s);
+
+// Fixed-point loop from the primitives in ps.fields; on return ps.fields holds
+// the reference's final 21-slot store.  Throws Fault like run_fixed_point.
+RunRecord engine_run(PointSet& ps, const EngineSpec& spec);
+
+// Device-resident session (bench, ranks).
+class Session;
+Session* session_open(PointSet& ps, const EngineSpec& spec, int capacity);
+double session_iterate(Session* s, int n);  // returns device ms; throws Fault
+std::vector<double> session_residues(const Session* s);
+std::vector<KernelTime> session_kernels(const Session* s);
+int session_launches_per_iter(const Session* s);
+std::uint64_t session_stream(const Session* s);
+void session_download(Session* s);
+void session_close(Session* s);
+
+// Per-phase operators on the whole cloud (reference kernels.hpp:25-63).
+enum class Op { q_variables, q_derivatives, publish, flux_fused, flux_direction, timestep,
+                state_update };
+struct OpSpec {
+  double gamma = 1.4, cfl = 0.5, det_tol = 0.0;
+  int fp_mode = 0;
+  int axis = 0, sign = 0, first = 1;
+  int device = 0;
+};
+void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch);
+double engine_reduce(const double* v, std::int64_t n, int device);
+int engine_device_count();
+
+}  // namespace lskb

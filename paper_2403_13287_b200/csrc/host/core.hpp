@@ -1,0 +1,209 @@
+// core.hpp — host-side model of the LSKUM problem (C++20).
+//
+// Native C++ counterpart of the reference's host layers L1/L4
+// (/root/reference/proj/src/core/{cloud,layout,config,bench,error}.hpp):
+// a columnar point set with CSR stencils, the 21-slot field block, the
+// solver settings and the error type that crosses the C ABI as a status.
+// The iteration itself lives on the GPU (../dev); this header is what the
+// host side of the boundary hands to it.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace lskb {
+
+// Status codes == LSKUM_ERR_* (reference error.hpp:9-17, lskum.h:18-27).
+enum class Status : int {
+  ok = 0,
+  argument = 1,
+  parse = 2,
+  io = 3,
+  validation = 4,
+  singular = 5,
+  positivity = 6,
+  config = 7,
+};
+
+class Fault : public std::runtime_error {
+ public:
+  Fault(Status s, const std::string& what) : std::runtime_error(what), status_(s) {}
+  Status status() const noexcept { return status_; }
+
+ private:
+  Status status_;
+};
+
+[[noreturn]] inline void raise(Status s, const std::string& what) { throw Fault(s, what); }
+
+// %f rendering, as std::to_string(double) produces in the reference messages.
+std::string fmt_f(double v);
+
+enum class Kind : std::uint8_t { interior = 0, wall = 1, outer = 2 };
+enum class Layout : std::uint8_t { aos = 0, soa = 1 };
+
+// Slot map of the 21-double field record (reference layout.hpp:11-19).
+namespace slot {
+inline constexpr int prim = 0, q = 4, qx = 8, qy = 12, res = 16, dt = 20, count = 21;
+}
+
+// Per-point solver fields in one buffer; AoS or SoA differ only in strides
+// (reference layout.hpp:24-48).  The GPU never sees this block directly: it
+// is the staging/copy-back format behind lskum_cloud_primitive/fields_equal.
+class FieldBlock {
+ public:
+  FieldBlock() = default;
+  FieldBlock(Layout layout, std::int32_t n);
+
+  Layout layout() const { return layout_; }
+  std::int32_t size() const { return n_; }
+  double& at(std::int32_t p, int s) { return data_[index(p, s)]; }
+  double at(std::int32_t p, int s) const { return data_[index(p, s)]; }
+  std::size_t point_stride() const { return layout_ == Layout::aos ? slot::count : 1; }
+  std::size_t slot_stride() const {
+    return layout_ == Layout::aos ? 1 : static_cast<std::size_t>(n_);
+  }
+  double* raw() { return data_.data(); }
+  const double* raw() const { return data_.data(); }
+
+  // Point-major (AoS) export/import regardless of the layout.
+  void export_aos(double* out) const;
+  void import_aos(const double* in);
+
+ private:
+  std::size_t index(std::int32_t p, int s) const {
+    return static_cast<std::size_t>(p) * point_stride() + static_cast<std::size_t>(s) * slot_stride();
+  }
+  Layout layout_ = Layout::aos;
+  std::int32_t n_ = 0;
+  std::vector<double> data_;
+};
+
+// Bitwise comparison over every (point, slot) (reference layout.cpp:29-45).
+bool fields_identical(const FieldBlock& a, const FieldBlock& b);
+
+// Columnar point set + CSR stencils (reference cloud.hpp:37-74).
+struct PointSet {
+  std::vector<double> x, y, nx, ny;
+  std::vector<Kind> kind;
+  std::vector<std::int64_t> off{0};  // n+1
+  std::vector<std::int32_t> nbr;     // ascending ids per point
+  FieldBlock fields;
+
+  std::int32_t n() const { return static_cast<std::int32_t>(x.size()); }
+  std::int64_t nnz() const { return off.empty() ? 0 : off.back(); }
+  std::int32_t degree(std::int32_t i) const {
+    return static_cast<std::int32_t>(off[i + 1] - off[i]);
+  }
+  bool has_wall() const;
+  int max_degree() const;
+  void reset_fields(Layout layout) { fields = FieldBlock(layout, n()); }
+};
+
+// One row of input, as produced by the readers and generators.
+struct PointRow {
+  double x = 0, y = 0, nx = 0, ny = 0;
+  Kind kind = Kind::interior;
+};
+
+// Checks ids/stencils (reference cloud.cpp:42-83 semantics) and assembles.
+PointSet assemble(std::vector<PointRow> rows, std::vector<std::int64_t> off,
+                  std::vector<std::int32_t> nbr);
+
+// ---- grid files (reference cloud.cpp:427-545 format) ----
+PointSet read_grid_file(const std::string& path);
+PointSet parse_grid_text(const char* text, std::size_t len);
+void write_grid_file(const PointSet& ps, const std::string& path);
+
+// ---- generators + kNN (reference cloud.cpp:137-237, 323-425) ----
+struct Box {
+  double xmin = 0.0, xmax = 1.0, ymin = 0.0, ymax = 1.0;
+};
+PointSet make_rect(int nx, int ny, const Box& box, double jitter, std::uint64_t seed, int k);
+PointSet make_annulus(int n_theta, int n_rings, double r_outer, double jitter,
+                      std::uint64_t seed, int k);
+void attach_knn(PointSet& ps, int k);
+
+// ---- stencil screening (reference cloud.cpp:252-321) ----
+struct Screening {
+  double h_ref = 0.0, det_tol = 0.0;
+  std::int32_t n_defective = 0, n_wall_isolated = 0, min_stencil = 0;
+  std::vector<std::int32_t> defective;
+};
+Screening screen_stencils(const PointSet& ps);
+
+// ---- recursive coordinate bisection (reference partition.cpp:12-80) ----
+struct Piece {
+  std::vector<std::int32_t> owned;   // ascending
+  std::vector<std::int32_t> halo;    // ascending; stencil closure minus owned
+};
+std::vector<Piece> bisect_cloud(const PointSet& ps, int n_parts);
+
+// ---- settings (reference config.hpp:12-57, config.cpp) ----
+struct Settings {
+  // solver
+  double mach = 0.63, aoa = 2.0, gamma = 1.4, cfl = 0.5;
+  int iters = 1000, inner = 3, order = 2;
+  Layout layout = Layout::aos;
+  int residual_split4 = 0;  // 0 fused, 1 split4
+  int parts = 1, workers = 1;
+  std::string out_prefix;
+  // grid source
+  std::string grid, generate;
+  double jitter = 0.0;
+  std::uint64_t seed = 0;
+  int knn = 8;
+  Box bounds;
+  double outer_radius = 10.0;
+  // B200 additions
+  int device = 0, gpus = 1, fp_mode = 0, chunk = 16;
+
+  void check() const;  // ErrorCode::config on bad values (reference config.cpp:47-56)
+  void set(const std::string& key, const std::string& value);
+  std::string get(const std::string& key) const;
+  void load(const std::string& path);
+};
+PointSet acquire_points(const Settings& s);
+
+// ---- run results / reports (reference runtime.hpp:29-47, bench.cpp) ----
+struct KernelTime {
+  std::string name;
+  double seconds = 0.0;
+  std::int64_t launches = 0;
+};
+
+struct RunRecord {
+  int iterations = 0;
+  std::vector<double> residue, log10_rel, wall_ms;
+  std::vector<KernelTime> kernels;
+  double total_seconds = 0.0;
+  int abort_iteration = 0;
+};
+
+void freestream(PointSet& ps, double mach, double aoa_deg, double gamma);
+double rate_of_data_processing(double seconds, std::int64_t iters, std::int64_t n);
+double relative_rate(double rdp_test, double rdp_ref);
+double pressure_coeff(double p, double mach, double gamma);
+
+struct KernelRow {
+  std::string name;
+  double seconds = 0.0, rdp = 0.0;
+};
+struct Report {
+  int iterations = 0;
+  std::int32_t n = 0;
+  double total_seconds = 0.0, total_rdp = 0.0;
+  std::vector<KernelRow> rows;
+};
+Report summarize(const RunRecord& run, std::int32_t n);
+void write_run_outputs(const std::string& prefix, const PointSet& ps, const RunRecord& run,
+                       const Report& rep, const Settings& s);
+
+// Runs the fixed-point loop on the GPU from the primitives in ps.fields
+// (reference run_fixed_point, runtime.cpp:195-275).  Throws Fault on failure
+// with the reference's code and "iteration N: ..." message.
+RunRecord solve_on_device(PointSet& ps, const Settings& s);
+
+}  // namespace lskb

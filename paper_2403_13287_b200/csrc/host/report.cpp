@@ -1,0 +1,146 @@
+// report.cpp — initial state, metrics and output files.
+//
+// Free-stream initialisation (reference bench.cpp:43-56), RDP and relative
+// performance (:58-70), the per-kernel report with the split4 aggregate row
+// (:72-99), Cp (:101-105) and the four output files with the reference's
+// exact formats (:107-183): .residue.csv, .solution.dat, .bench.csv,
+// .surface.csv.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <filesystem>
+
+#include "core.hpp"
+
+namespace lskb {
+
+namespace {
+
+class OutFile {
+ public:
+  explicit OutFile(const std::string& path) : path_(path) {
+    const std::filesystem::path parent = std::filesystem::path(path).parent_path();
+    if (!parent.empty()) {
+      std::error_code ec;
+      std::filesystem::create_directories(parent, ec);
+    }
+    f_ = std::fopen(path.c_str(), "wb");
+    if (!f_) raise(Status::io, "cannot open output file: " + path);
+  }
+  ~OutFile() {
+    if (f_) std::fclose(f_);
+  }
+  void put(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+    va_list ap;
+    va_start(ap, fmt);
+    if (std::vfprintf(f_, fmt, ap) < 0) ok_ = false;
+    va_end(ap);
+  }
+  void close() {
+    const bool closed = std::fclose(f_) == 0;
+    f_ = nullptr;
+    if (!closed || !ok_) raise(Status::io, "failed writing output file: " + path_);
+  }
+
+ private:
+  std::string path_;
+  std::FILE* f_ = nullptr;
+  bool ok_ = true;
+};
+
+}  // namespace
+
+void freestream(PointSet& ps, double mach, double aoa_deg, double gamma) {
+  const double a = aoa_deg * M_PI / 180.0;
+  const double u1 = mach * std::cos(a), u2 = mach * std::sin(a), p = 1.0 / gamma;
+  for (std::int32_t i = 0; i < ps.n(); ++i) {
+    ps.fields.at(i, slot::prim) = 1.0;
+    ps.fields.at(i, slot::prim + 1) = u1;
+    ps.fields.at(i, slot::prim + 2) = u2;
+    ps.fields.at(i, slot::prim + 3) = p;
+  }
+}
+
+double rate_of_data_processing(double seconds, std::int64_t iters, std::int64_t n) {
+  if (iters <= 0 || n <= 0) raise(Status::argument, "rdp needs positive iteration and point counts");
+  return seconds / static_cast<double>(iters) / static_cast<double>(n);
+}
+
+double relative_rate(double rdp_test, double rdp_ref) {
+  if (rdp_ref == 0.0) raise(Status::argument, "relative performance needs a nonzero reference");
+  return rdp_test / rdp_ref;
+}
+
+double pressure_coeff(double p, double mach, double gamma) {
+  if (mach == 0.0) return 0.0;
+  return (p - 1.0 / gamma) / (0.5 * mach * mach);
+}
+
+Report summarize(const RunRecord& run, std::int32_t n) {
+  Report rep;
+  rep.iterations = run.iterations;
+  rep.n = n;
+  rep.total_seconds = run.total_seconds;
+  const bool rate = run.iterations > 0 && n > 0;
+  rep.total_rdp = rate ? rate_of_data_processing(run.total_seconds, run.iterations, n) : 0.0;
+  double split_s = 0.0, split_r = 0.0;
+  bool split = false;
+  for (const KernelTime& k : run.kernels) {
+    KernelRow row{k.name, k.seconds, rate ? rate_of_data_processing(k.seconds, run.iterations, n) : 0.0};
+    if (k.name.rfind("flux_residual_", 0) == 0) {
+      split = true;
+      split_s += row.seconds;
+      split_r += row.rdp;
+    }
+    rep.rows.push_back(row);
+  }
+  if (split) rep.rows.push_back({"flux_residual", split_s, split_r});
+  return rep;
+}
+
+void write_run_outputs(const std::string& prefix, const PointSet& ps, const RunRecord& run,
+                       const Report& rep, const Settings& s) {
+  {
+    OutFile f(prefix + ".residue.csv");
+    f.put("iter,residue,log10rel,wall_ms\n");
+    for (std::size_t i = 0; i < run.residue.size(); ++i)
+      f.put("%zu,%.17g,%.17g,%.3f\n", i + 1, run.residue[i], run.log10_rel[i],
+            i < run.wall_ms.size() ? run.wall_ms[i] : 0.0);
+    f.close();
+  }
+  {
+    OutFile f(prefix + ".solution.dat");
+    f.put("# id x y rho u1 u2 p\n");
+    for (std::int32_t i = 0; i < ps.n(); ++i)
+      f.put("%d %.17g %.17g %.17g %.17g %.17g %.17g\n", i, ps.x[i], ps.y[i], ps.fields.at(i, slot::prim),
+            ps.fields.at(i, slot::prim + 1), ps.fields.at(i, slot::prim + 2), ps.fields.at(i, slot::prim + 3));
+    f.close();
+  }
+  {
+    OutFile f(prefix + ".bench.csv");
+    f.put("kernel,seconds,rdp\n");
+    for (const KernelRow& k : rep.rows) f.put("%s,%.9g,%.9g\n", k.name.c_str(), k.seconds, k.rdp);
+    f.put("total,%.9g,%.9g\n", rep.total_seconds, rep.total_rdp);
+    f.close();
+  }
+  if (ps.has_wall()) {
+    OutFile f(prefix + ".surface.csv");
+    f.put("arc_position,cp\n");
+    double arc = 0.0, px = 0.0, py = 0.0;
+    bool have = false;
+    for (std::int32_t i = 0; i < ps.n(); ++i) {
+      if (ps.kind[i] != Kind::wall) continue;
+      if (have) {
+        const double dx = ps.x[i] - px, dy = ps.y[i] - py;
+        arc += std::sqrt(dx * dx + dy * dy);
+      }
+      px = ps.x[i];
+      py = ps.y[i];
+      have = true;
+      f.put("%.17g,%.17g\n", arc, pressure_coeff(ps.fields.at(i, slot::prim + 3), s.mach, s.gamma));
+    }
+    f.close();
+  }
+}
+
+}  // namespace lskb

@@ -1,0 +1,52 @@
+// solve.cpp — host driver of one run (reference run_fixed_point,
+// runtime.cpp:195-275): config check, stencil screening gate, bisection into
+// `parts` pieces (the pieces fix the error tie-break order and, with gpus > 1,
+// the device domains), then the device loop.
+#include <algorithm>
+
+#include "../engine.hpp"
+#include "core.hpp"
+
+namespace lskb {
+
+namespace {
+
+EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
+  EngineSpec spec;
+  spec.gamma = s.gamma;
+  spec.cfl = s.cfl;
+  spec.det_tol = det_tol;
+  spec.iters = s.iters;
+  spec.inner = s.inner;
+  spec.order = s.order;
+  spec.fp_mode = s.fp_mode;
+  spec.chunk = s.chunk;
+  spec.device = s.device;
+  const std::vector<Piece> pieces = bisect_cloud(ps, s.parts);
+  if (pieces.size() > 1) {
+    spec.part_of.assign(static_cast<std::size_t>(ps.n()), 0);
+    for (std::size_t p = 0; p < pieces.size(); ++p)
+      for (std::int32_t i : pieces[p].owned)
+        spec.part_of[i] = static_cast<std::uint8_t>(std::min<std::size_t>(p, 255));
+  }
+  return spec;
+}
+
+}  // namespace
+
+EngineSpec prepare_run(const PointSet& ps, const Settings& s) {
+  s.check();
+  const Screening scr = screen_stencils(ps);
+  if (scr.n_defective > 0)
+    raise(Status::validation, "cloud has " + std::to_string(scr.n_defective) +
+                                  " defective stencils (first at point " +
+                                  std::to_string(scr.defective.front()) + ")");
+  return spec_from(ps, s, scr.det_tol);
+}
+
+RunRecord solve_on_device(PointSet& ps, const Settings& s) {
+  const EngineSpec spec = prepare_run(ps, s);
+  return engine_run(ps, spec);
+}
+
+}  // namespace lskb
