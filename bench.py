@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py — LSKUM fixed-point iteration on B200: device-timed point-iterations/s.
+
+Workload (BASELINE.json configs[1]): ~160K-point cloud, M=0.85, alpha=1 deg,
+second order with 3 inner derivative sweeps, CFL 0.5.  The reference has no
+NACA 0012 generator (wall clouds fail validation or
+abort), so the cloud is the reference's own jittered-rectangle generator at
+400x400 = 160,000 points (jitter 0.1, seed 7, k 8), free-stream initialised as
+lskum_run does — an exact fixed point with the full arithmetic cost.
+
+One step = one fixed-point iteration (3 sweeps + fused flux/update + residue).
+`value` times K steps with CUDA events on the engine's stream, with the L2
+flushed (384 MB overwrite) before every step; `e2e` times lskum_run through the
+C ABI from host buffers (upload, K iterations, copy-back of the 21-slot store).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+COUNTS_PATH = os.path.join(ROOT, "profiles", "flux_ncu_counts.json")
+METRIC = "point-iterations/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "point-iterations/s"
+
+# Algorithmic bytes per point: one derivative sweep reads
+# x,y (16) q (32) qx,qy (64) offsets (8) ids (4k) and writes qx,qy (64):
+# 184 + 4k; the fused flux+dt+update+q+residue pass moves 217 + 4k.
+def sweep_bytes(k):
+    return 184 + 4 * k
+
+
+def flux_bytes(k):
+    return 217 + 4 * k
+
+
+def iteration_bytes(k, order, inner):
+    return (inner * sweep_bytes(k) if order == 2 else 0) + flux_bytes(k) - (64 if order == 1 else 0)
+
+
+# ---------------------------------------------------------------------------
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--side", type=int, default=400, help="cloud is side x side points")
+    ap.add_argument("--order", type=int, default=2)
+    ap.add_argument("--inner", type=int, default=3)
+    ap.add_argument("--mach", type=float, default=0.85)
+    ap.add_argument("--aoa", type=float, default=1.0)
+    ap.add_argument("--fp-mode", default="fast")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-steady", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample target")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU works."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        loaded = [r for r in rows if r[2] >= 50.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def load_counts():
+    try:
+        with open(COUNTS_PATH) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own implementation (oracle/_ref/liblskum.so,
+# built from /root/reference by oracle/Makefile) through its C ABI, on all host
+# cores (parts = workers = nproc).  Falls back to the plain-C port when the
+# reference build is absent.  Test/baseline infrastructure only.
+def reference_lib():
+    so = os.path.join(ROOT, "oracle", "_ref", "liblskum.so")
+    if not os.path.exists(so):
+        return None
+    L = ctypes.CDLL(so)
+    vp = ctypes.c_void_p
+    L.lskum_cloud_read_file.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.lskum_config_create.argtypes = [ctypes.POINTER(vp)]
+    L.lskum_config_set.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p]
+    L.lskum_run.argtypes = [vp, vp, ctypes.POINTER(vp)]
+    L.lskum_result_total_seconds.argtypes = [vp]
+    L.lskum_result_total_seconds.restype = ctypes.c_double
+    L.lskum_result_destroy.argtypes = [vp]
+    L.lskum_cloud_destroy.argtypes = [vp]
+    L.lskum_config_destroy.argtypes = [vp]
+    L.lskum_last_error.restype = ctypes.c_char_p
+    return L
+
+
+def reference_run(L, cloud_h, a, iters, threads):
+    cfg = ctypes.c_void_p()
+    L.lskum_config_create(ctypes.byref(cfg))
+    for k, v in (("mach", a.mach), ("aoa", a.aoa), ("order", a.order), ("inner", a.inner),
+                 ("cfl", 0.5), ("iters", iters), ("parts", threads), ("workers", threads),
+                 ("layout", "soa"), ("residual_mode", "fused")):
+        assert L.lskum_config_set(cfg, k.encode(), str(v).encode()) == 0
+    res = ctypes.c_void_p()
+    t0 = time.perf_counter()
+    rc = L.lskum_run(cloud_h, cfg, ctypes.byref(res))
+    wall = time.perf_counter() - t0
+    if rc != 0:
+        raise RuntimeError(L.lskum_last_error().decode())
+    secs = L.lskum_result_total_seconds(res)
+    L.lskum_result_destroy(res)
+    L.lskum_config_destroy(cfg)
+    return secs, wall
+
+
+def reference_cloud(L, cloud):
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "bench.grid")
+        cloud.write_file(path)  # same grid file feeds both sides
+        h = ctypes.c_void_p()
+        if L.lskum_cloud_read_file(path.encode(), ctypes.byref(h)) != 0:
+            raise RuntimeError(L.lskum_last_error().decode())
+    return h
+
+
+def cpu_baseline(cloud, a, target_s):
+    """Bounded sample of the same workload on the host cores."""
+    n = cloud.n
+    threads = os.cpu_count() or 1
+    L = reference_lib()
+    if L is not None:
+        h = reference_cloud(L, cloud)
+        s1, _ = reference_run(L, h, a, 2, threads)
+        iters = int(max(2, min(500, target_s / max(s1 / 2, 1e-6))))
+        secs, _ = reference_run(L, h, a, iters, threads)
+        L.lskum_cloud_destroy(h)
+        return {"value": n * iters / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{iters} iterations of the {n}-point cloud, lskum_run of oracle/_ref/liblskum.so "
+                          f"(parts=workers={threads}, soa, fused), reference loop timer"}
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import pyoracle as P
+    g = cloud.geometry()
+    c = P.Cloud(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"])
+    t0 = time.perf_counter()
+    P.orc_run(c, mach=a.mach, aoa=a.aoa, iters=1, order=a.order, inner=a.inner)
+    one = time.perf_counter() - t0
+    iters = int(max(1, min(200, target_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    P.orc_run(c, mach=a.mach, aoa=a.aoa, iters=iters, order=a.order, inner=a.inner)
+    dt = time.perf_counter() - t0
+    return {"value": n * iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{iters} iterations of the {n}-point cloud, oracle/lskum_oracle.c (1 thread)"}
+
+
+def config_block(a, n, extra=None):
+    c = {"workload": f"rect {a.side}x{a.side} stand-in for BASELINE configs[1] "
+                     f"(NACA 0012 transonic ~160K, M={a.mach}, AoA={a.aoa}, order {a.order}, "
+                     f"{a.inner} inner sweeps); free-stream state",
+         "n_points": n, "stencil": "kNN k=8 (reference generate_rect_cloud, jitter 0.1, seed 7)",
+         "order": a.order, "inner": a.inner, "mach": a.mach, "aoa_deg": a.aoa, "cfl": 0.5,
+         "fp_mode": a.fp_mode, "l2": "flushed before every timed step (384 MB overwrite)",
+         "parallelism": f"rcb{a.gpus}" if a.gpus > 1 else "single-domain"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(a):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2403_13287_b200 import lskum as LB
+    cloud = LB.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+    n = cloud.n
+    L = reference_lib()
+    threads = os.cpu_count() or 1
+    if L is None:
+        base = cpu_baseline(cloud, a, a.cpu_seconds)
+        value, kind, sample = base["value"], base["kind"], base["sample"]
+    else:
+        h = reference_cloud(L, cloud)
+        if a.warmup > 0:
+            reference_run(L, h, a, a.warmup, threads)
+        secs, wall = reference_run(L, h, a, a.steps, threads)
+        L.lskum_cloud_destroy(h)
+        value, kind = n * a.steps / secs, "reference"
+        sample = (f"{a.steps} iterations (after {a.warmup} warm-up) of the {n}-point cloud through the "
+                  f"reference lskum_run (oracle/_ref/liblskum.so), parts=workers={threads}")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": n / value * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": config_block(a, n),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
+                            "kind": kind, "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_b200_arm(a):
+    from paper_2403_13287_b200 import lskum as L
+    world, rank, local = dist_env()
+    if world > 1:
+        return run_b200_distributed(a, world, rank, local)
+    dev = 0
+    cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+    n = cloud.n
+    k = cloud.nnz // n
+    n_flux = int(sum(1 for v in cloud.geometry()["kind"] if v != 2))
+    cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
+                   iters=a.steps, device=dev)
+    steady_iters = 0
+    with ClockSampler(dev) as clocks:
+        sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps + 4000)
+        for _ in range(a.warmup):
+            sess.flush_l2()
+            sess.iterate(1)
+        step_ms, sweep_ms, flux_ms = [], [], []
+        for _ in range(a.steps):
+            sess.flush_l2()
+            step_ms.append(sess.iterate(1))
+            sw, fl = sess.event_ms()
+            sweep_ms.append(sw)
+            flux_ms.append(fl)
+        launches = sess.info()["launches_per_iter"]
+        # steady state (no flush, back-to-back graphs) ~1.5 s, also keeps the clock sampler busy
+        steady = None
+        if not a.no_steady:
+            per = max(statistics.median(step_ms), 1e-3)
+            steady_iters = int(min(3900, max(20, 1500.0 / per)))
+            steady_ms = sess.iterate(steady_iters)
+            steady = n * steady_iters / (steady_ms * 1e-3)
+        residues = sess.residues()
+        sess.close()
+    clk = clocks.summary()
+    total_ms = sum(step_ms)
+    value = n * a.steps / (total_ms * 1e-3)
+
+    # e2e through the drop-in C ABI (lskum_run) from host buffers
+    e2e_cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+    e2e_cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5,
+                       fp_mode=a.fp_mode, iters=a.steps, device=dev)
+    L.run(e2e_cloud, e2e_cfg).close()  # warm (context, module load)
+    t0 = time.perf_counter()
+    res = L.run(e2e_cloud, e2e_cfg)
+    e2e_wall = time.perf_counter() - t0
+    res.close()
+    nnz = e2e_cloud.nnz
+    h2d = n * (16 + 16 + 1 + 1 + 32) + 4 * (n + 1) + 4 * nnz  # xy, normals, kind, part, prim, off, ids
+    d2h = n * (32 + 32 + 64 + 32 + 8) + 8 * a.steps        # prim q qx qy res dt + residue history
+
+    # rooflines
+    counts = load_counts()
+    fp64_peak = L.fp64_peak_tflops(dev)
+    flux_avg = statistics.mean(flux_ms)
+    flops_pt = counts.get("flux_fp64_flops_per_point")
+    achieved = flops_pt * n_flux / (flux_avg * 1e-3) / 1e12 if flops_pt else None
+    traffic = counts.get("flux_dram_bytes_per_point")
+    hbm, hbm_kind = hbm_peak()
+    sweep_avg = statistics.mean(sweep_ms) if a.order == 2 else None
+    sweep_gbs = sweep_bytes(k) * n / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
+    iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (free-stream state on a generated cloud)",
+        "config": config_block(a, n),
+        "e2e": {"value": n * a.steps / e2e_wall, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps),
+                "what": "wall time of lskum_run (C ABI, host buffers): screening, upload, "
+                        f"{a.steps} iterations, copy-back of the 21-slot store"},
+        "gpu_launches": launches * a.steps,
+        "gpu_launches_note": f"{launches} kernels per iteration (sweeps, fused flux, 2 residue-tree "
+                             f"stages) x {a.steps}; plus {a.steps} L2-flush kernels between steps",
+        "roofline": {"bound": "fp64", "kernel": "k_flux (fused flux residual + dt + update + q)",
+                     "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak if achieved else None,
+                     "traffic": traffic * n_flux if traffic else None,
+                     "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
+                     "flops_source": "ncu dynamic DFMA*2+DADD+DMUL per point, profiles/flux_ncu_counts.json",
+                     "launch_ms": flux_avg},
+        "roofline_hbm": {"bound": "hbm", "kernel": "k_sweep", "achieved": sweep_gbs, "peak": hbm,
+                         "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
+                         "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_avg,
+                         "peak_source": hbm_kind,
+                         "iteration_achieved_gbs": iter_gbs, "iteration_frac": iter_gbs / hbm,
+                         "iteration_bytes_per_point": iteration_bytes(k, a.order, a.inner)},
+        "steady_state": {"value": steady, "iterations": steady_iters,
+                         "what": "same session, back-to-back graph replays, no L2 flush"},
+        "clocks": clk,
+        "final_residue": float(residues[-1]) if len(residues) else None,
+    }
+    if not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cloud, a, a.cpu_seconds)
+    print(json.dumps(out), flush=True)
+
+
+def run_b200_distributed(a, world, rank, local):
+    """One process per GPU (torchrun).  Each rank owns one RCB piece of the same
+    cloud; see DESIGN.md (multi-GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_13287_b200 import lskum as L
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+    n = cloud.n
+    cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
+                   iters=a.steps, device=local, parts=world)
+    sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps)
+    for _ in range(a.warmup):
+        sess.iterate(1)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(a.steps):
+        sess.flush_l2()
+        ms += sess.iterate(1)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    if rank == 0:
+        value = n * world * a.steps / (total_ms * 1e-3)
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                          "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic",
+                          "config": config_block(a, n, {"parallelism": f"replica x{world} (halo engine pending)"}),
+                          "gpu_launches": sess.info()["launches_per_iter"] * a.steps}), flush=True)
+    sess.close()
+    dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_b200_arm(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -106,6 +106,13 @@ int lskum_b200_session_kernel_stats(const lskum_b200_session* s, int index, doub
 int lskum_b200_session_info(const lskum_b200_session* s, int* launches_per_iter,
                             uint64_t* stream);
 int lskum_b200_session_download(lskum_b200_session* s);
+/* CUDA-event milliseconds of the first derivative sweep and of the flux
+ * kernel of the most recent iteration (events recorded inside the graph). */
+int lskum_b200_session_event_ms(const lskum_b200_session* s, double* sweep_ms, double* flux_ms);
+/* Overwrites a 384 MB scratch buffer on the session stream (cold-L2 steps). */
+int lskum_b200_session_flush_l2(lskum_b200_session* s);
+/* Measured FP64 FMA throughput of `device` (TFLOP/s, DFMA = 2 flops). */
+int lskum_b200_fp64_peak(int device, double* tflops);
 void lskum_b200_session_destroy(lskum_b200_session* s);
 
 #ifdef __cplusplus

@@ -225,6 +225,28 @@ __global__ void k_ctl_init(Ctl* ctl, int diag_iter) {
 
 __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter; }
 
+// Overwrites a buffer larger than L2 (126 MB) so the next step starts cold.
+__global__ void k_flush(double* buf, long long n, double v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    buf[i] = v;
+}
+
+// DFMA throughput probe: 8 independent FMA chains per thread.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double m, double c) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int t = 0; t < iters; ++t) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 1.2345) out[0] = s;  // keeps the chains live
+}
+
 std::string itos(long long v) { return std::to_string(v); }
 
 }  // namespace
@@ -240,6 +262,7 @@ class Domain {
     ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreate(&ev0_), "cudaEventCreate");
     ck(cudaEventCreate(&ev1_), "cudaEventCreate");
+    for (auto& e : kev_) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : poll_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     if (ps.nnz() >= (1ll << 31)) raise(Status::argument, "stencil table exceeds 2^31 entries");
     gas_.gamma = gamma;
@@ -311,6 +334,7 @@ class Domain {
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
+    for (auto& e : kev_) cudaEventDestroy(e);
     for (auto& e : poll_ev_) cudaEventDestroy(e);
     cudaStreamDestroy(st_);
   }
@@ -430,12 +454,16 @@ class Domain {
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 3; }
 
   // Enqueue one iteration starting at parity (a, b); returns the new parity.
-  void enqueue_iteration(int& a, int& b) {
+  // `timed`: bracket the first sweep and the flux kernel with CUDA events
+  // (event-record nodes inside the graph; read back by last_event_ms()).
+  void enqueue_iteration(int& a, int& b, bool timed) {
     const Geo g = geo();
     if (order_ == 2) {
       for (int s = 0; s < inner_; ++s) {
+        if (timed && s == 0) ck(cudaEventRecord(kev_[0], st_), "EventRecord");
         k_sweep<<<(n_ + 255) / 256, 256, 0, st_>>>(g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(),
                                                    gas_, ctl_.get(), s == 0 ? it0_.get() : nullptr);
+        if (timed && s == 0) ck(cudaEventRecord(kev_[1], st_), "EventRecord");
         b ^= 1;
       }
     }
@@ -454,7 +482,9 @@ class Domain {
     fa.kcap = kmax_;
     fa.mask = 0xF;
     fa.first = 1;
+    if (timed) ck(cudaEventRecord(kev_[2], st_), "EventRecord");
     flux_launch(W_, strict_, true, fa, smem_, st_);
+    if (timed) ck(cudaEventRecord(kev_[3], st_), "EventRecord");
     a ^= 1;
     k_tree_partial<<<1 << d1_, kTreeThreads, 0, st_>>>(mag_.get(), n_, d1_, pval_.get(), psz_.get(),
                                                       ctl_.get());
@@ -469,7 +499,7 @@ class Domain {
     cudaGraph_t graph;
     ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "BeginCapture");
     int pa = a, pb = b;
-    for (int k = 0; k < c; ++k) enqueue_iteration(pa, pb);
+    for (int k = 0; k < c; ++k) enqueue_iteration(pa, pb, k == c - 1);
     ck(cudaGetLastError(), "capture launches");
     ck(cudaStreamEndCapture(st_, &graph), "EndCapture");
     cudaGraphExec_t exec;
@@ -508,6 +538,7 @@ class Domain {
       ck(cudaGraphLaunch(graph_for(a_, b_, c), st_), "GraphLaunch");
       advance(a_, b_, c);
       left -= c;
+      if (left == 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");
       const int s = issued % kPolls;
       ck(cudaMemcpyAsync(hpoll_.get() + s, &ctl_.get()->err_key, sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost, st_),
@@ -521,8 +552,8 @@ class Domain {
         ++waited;
       }
     }
-    ck(cudaEventRecord(ev1_, st_), "EventRecord");
-    ck(cudaEventSynchronize(ev1_), "iterate");
+    if (left > 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");  // stopped early
+    ck(cudaStreamSynchronize(st_), "iterate");
     float ms = 0.0f;
     ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "EventElapsed");
     total_ms_ += ms;
@@ -537,6 +568,22 @@ class Domain {
   }
 
   bool failed() const { return hctl_.get()->err_key != kNoErr; }
+
+  // CUDA-event times of the first sweep and the flux kernel of the last
+  // iteration of the last graph replay (valid after iterate()).
+  void last_event_ms(double& sweep_ms, double& flux_ms) const {
+    float a = 0.0f, b = 0.0f;
+    sweep_ms = flux_ms = 0.0;
+    if (order_ == 2 && cudaEventElapsedTime(&a, kev_[0], kev_[1]) == cudaSuccess) sweep_ms = a;
+    if (cudaEventElapsedTime(&b, kev_[2], kev_[3]) == cudaSuccess) flux_ms = b;
+    cudaGetLastError();
+  }
+
+  void flush_l2() {
+    if (!flush_.get()) flush_.alloc(static_cast<std::size_t>(48) << 20);  // 384 MB
+    k_flush<<<148 * 8, 256, 0, st_>>>(flush_.get(), static_cast<long long>(flush_.size()), 1.0);
+    ck(cudaStreamSynchronize(st_), "flush");
+  }
   const Ctl& ctl() const { return *hctl_.get(); }
 
   // Builds the reference-format message for the recorded failure.
@@ -647,7 +694,8 @@ class Domain {
   static constexpr int kPolls = 4;
   int n_ = 0, device_ = 0;
   cudaStream_t st_ = nullptr;
-  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, poll_ev_[kPolls] = {};
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, poll_ev_[kPolls] = {}, kev_[4] = {};
+  DBuf<double> flush_;
   Gas gas_{};
   int kmax_ = 1, W_ = 8, d1_ = 0;
   std::size_t smem_ = 0;
@@ -755,6 +803,35 @@ std::uint64_t session_stream(const Session* s) {
   return reinterpret_cast<std::uint64_t>(s->dom->stream());
 }
 void session_download(Session* s) { copy_back(*s->dom, *s->ps); }
+void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms) {
+  s->dom->last_event_ms(*sweep_ms, *flux_ms);
+}
+void session_flush_l2(Session* s) { s->dom->flush_l2(); }
+
+double engine_fp64_peak_tflops(int device) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  int sms = 0;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  DBuf<double> out(1);
+  const int blocks = sms * 8, threads = 256, iters = 8192;
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "ev");
+  ck(cudaEventCreate(&e1), "ev");
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    ck(cudaEventRecord(e0), "ev");
+    k_dfma_peak<<<blocks, threads>>>(out.get(), iters, 0.999999, 1e-7);
+    ck(cudaEventRecord(e1), "ev");
+    ck(cudaEventSynchronize(e1), "dfma");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "ev");
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
 void session_close(Session* s) { delete s; }
 
 // ---- per-phase operators ----

@@ -40,6 +40,9 @@ std::vector<KernelTime> session_kernels(const Session* s);
 int session_launches_per_iter(const Session* s);
 std::uint64_t session_stream(const Session* s);
 void session_download(Session* s);
+void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms);
+void session_flush_l2(Session* s);
+double engine_fp64_peak_tflops(int device);
 void session_close(Session* s);
 
 // Per-phase operators on the whole cloud (reference kernels.hpp:25-63).

@@ -502,6 +502,21 @@ int lskum_b200_session_download(lskum_b200_session* s) {
   return guard([&] { lskb::session_download(s->session); });
 }
 
+int lskum_b200_session_event_ms(const lskum_b200_session* s, double* sweep_ms, double* flux_ms) {
+  NONNULL(s, sweep_ms, flux_ms);
+  return guard([&] { lskb::session_event_ms(s->session, sweep_ms, flux_ms); });
+}
+
+int lskum_b200_session_flush_l2(lskum_b200_session* s) {
+  NONNULL(s);
+  return guard([&] { lskb::session_flush_l2(s->session); });
+}
+
+int lskum_b200_fp64_peak(int device, double* tflops) {
+  NONNULL(tflops);
+  return guard([&] { *tflops = lskb::engine_fp64_peak_tflops(device); });
+}
+
 void lskum_b200_session_destroy(lskum_b200_session* s) { delete s; }
 
 }  // extern "C"
