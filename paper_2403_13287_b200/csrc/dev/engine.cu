@@ -83,56 +83,50 @@ int flux_width(int kmax) { return kmax <= 8 ? 8 : (kmax <= 16 ? 16 : 32); }
 
 std::size_t flux_smem_bytes(int W, int kcap) {
   const int P = flux_points_per_block(W);
-  return static_cast<std::size_t>(P) * kcap * sizeof(PairRec) + static_cast<std::size_t>(P) * 16 * sizeof(double);
+  return (static_cast<std::size_t>(P) * flux_stride(kcap) + static_cast<std::size_t>(P) * 16) * sizeof(double);
 }
 
-template <int W, bool S, bool F>
+template <int W, bool S>
 void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   static std::size_t configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > configured[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux<W, S, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_flux<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux)");
     configured[dev & 63] = smem;
   }
   const int P = flux_points_per_block(W);
   const int blocks = (a.g.n + P - 1) / P;
-  k_flux<W, S, F><<<blocks, W * P, smem, st>>>(a);
+  k_flux<W, S><<<blocks, W * P, smem, st>>>(a);
 }
 
-template <bool S, bool F>
-void flux_launch_w(int W, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
-  if (W == 8) flux_launch_t<8, S, F>(a, smem, st);
-  else if (W == 16) flux_launch_t<16, S, F>(a, smem, st);
-  else flux_launch_t<32, S, F>(a, smem, st);
-}
-
-void flux_launch(int W, bool strict, bool fused, const FluxArgs& a, std::size_t smem,
-                 cudaStream_t st) {
+void flux_launch(int W, bool strict, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   if (strict) {
-    if (fused) flux_launch_w<true, true>(W, a, smem, st);
-    else flux_launch_w<true, false>(W, a, smem, st);
+    if (W == 8) flux_launch_t<8, true>(a, smem, st);
+    else if (W == 16) flux_launch_t<16, true>(a, smem, st);
+    else flux_launch_t<32, true>(a, smem, st);
   } else {
-    if (fused) flux_launch_w<false, true>(W, a, smem, st);
-    else flux_launch_w<false, false>(W, a, smem, st);
+    if (W == 8) flux_launch_t<8, false>(a, smem, st);
+    else if (W == 16) flux_launch_t<16, false>(a, smem, st);
+    else flux_launch_t<32, false>(a, smem, st);
   }
 }
 
-// Depth of the per-block nodes of the residue tree: ~2048+ values per block,
-// at most 1024 blocks (one block folds the partials).
+// Depth of the per-block nodes of the residue tree: at most ~8 values per
+// thread (256 threads per block), at most 1024 blocks (one block folds the
+// partials).
 int tree_depth(long long n) {
   int d = 0;
-  while (d < 10 && (1ll << (d + 1)) * 2048 <= n) ++d;
+  while (d < 10 && (n >> (d + 8)) > 8) ++d;
   return d;
 }
 
 // ---- diagnostics: re-evaluates the failing item named by the error key ----
 template <bool S>
-__global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, const D4* res,
-                           const double* op_diag, Gas gas, unsigned long long key,
-                           double* out) {
+__global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, const double* uval,
+                           const double* uwhich, Gas gas, unsigned long long key, double* out) {
   const unsigned phase = static_cast<unsigned>(key >> 61);
   const int i = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
   const unsigned dir = static_cast<unsigned>((key >> 20) & 3ull);
@@ -145,13 +139,8 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
     return;
   }
   if (phase == PH_UPDATE) {
-    if (op_diag) {
-      out[1] = op_diag[2 * i];
-      out[0] = op_diag[2 * i + 1];
-    } else {
-      out[1] = res[i].a;
-      out[0] = res[i].b;
-    }
+    out[1] = uval[i];
+    out[0] = uwhich[i];
     return;
   }
   const double2 pi = g.xy[i];
@@ -270,9 +259,15 @@ class Domain {
     gas_.inv_gm1 = 1.0 / (gamma - 1.0);
     gas_.cfl = cfl;
     gas_.det_tol = det_tol;
+    {
+      const double m = 2.0 / (gamma - 1.0);
+      const double mr = std::nearbyint(m);
+      gas_.half_pow = (std::fabs(m - mr) < 1e-9 && mr >= 1.0 && mr <= 40.0) ? static_cast<int>(mr) : -1;
+    }
     kmax_ = std::max(1, ps.max_degree());
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
+    stride_ = flux_stride(kmax_);
     d1_ = tree_depth(n_);
 
     const std::size_t n = static_cast<std::size_t>(n_);
@@ -451,19 +446,30 @@ class Domain {
     refresh_ctl();
   }
 
-  int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 3; }
+  int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
 
   // Enqueue one iteration starting at parity (a, b); returns the new parity.
+  // Event record that also fires when captured into a graph (an external
+  // event-record node); a plain captured cudaEventRecord only orders work.
+  void record_ext(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(st_, &cs), "StreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusActive)
+      ck(cudaEventRecordWithFlags(e, st_, cudaEventRecordExternal), "EventRecordExternal");
+    else
+      ck(cudaEventRecord(e, st_), "EventRecord");
+  }
+
   // `timed`: bracket the first sweep and the flux kernel with CUDA events
   // (event-record nodes inside the graph; read back by last_event_ms()).
   void enqueue_iteration(int& a, int& b, bool timed) {
     const Geo g = geo();
     if (order_ == 2) {
       for (int s = 0; s < inner_; ++s) {
-        if (timed && s == 0) ck(cudaEventRecord(kev_[0], st_), "EventRecord");
+        if (timed && s == 0) record_ext(kev_[0]);
         k_sweep<<<(n_ + 255) / 256, 256, 0, st_>>>(g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(),
                                                    gas_, ctl_.get(), s == 0 ? it0_.get() : nullptr);
-        if (timed && s == 0) ck(cudaEventRecord(kev_[1], st_), "EventRecord");
+        if (timed && s == 0) record_ext(kev_[1]);
         b ^= 1;
       }
     }
@@ -472,19 +478,27 @@ class Domain {
     fa.gas = gas_;
     fa.q = q_[a].get();
     fa.dq = dq_[b].get();
-    fa.prim = prim_.get();
-    fa.q_next = q_[a ^ 1].get();
     fa.res = res_.get();
-    fa.dt = dt_.get();
-    fa.mag = mag_.get();
     fa.ctl = ctl_.get();
     fa.iter_t0 = order_ == 2 ? nullptr : it0_.get();
     fa.kcap = kmax_;
+    fa.stride = stride_;
     fa.mask = 0xF;
     fa.first = 1;
-    if (timed) ck(cudaEventRecord(kev_[2], st_), "EventRecord");
-    flux_launch(W_, strict_, true, fa, smem_, st_);
-    if (timed) ck(cudaEventRecord(kev_[3], st_), "EventRecord");
+    if (timed) record_ext(kev_[2]);
+    flux_launch(W_, strict_, fa, smem_, st_);
+    if (timed) record_ext(kev_[3]);
+    UpdateArgs ua;
+    ua.g = g;
+    ua.gas = gas_;
+    ua.q = q_[a].get();
+    ua.res = res_.get();
+    ua.prim = prim_.get();
+    ua.q_next = q_[a ^ 1].get();
+    ua.dt = dt_.get();
+    ua.mag = mag_.get();
+    ua.ctl = ctl_.get();
+    k_update<<<(n_ + 255) / 256, 256, 0, st_>>>(ua);
     a ^= 1;
     k_tree_partial<<<1 << d1_, kTreeThreads, 0, st_>>>(mag_.get(), n_, d1_, pval_.get(), psz_.get(),
                                                       ctl_.get());
@@ -594,10 +608,10 @@ class Domain {
   }
   Fault fault_in_run() {
     const int t = std::max(0, hctl_.get()->err_iter);
-    return fault(true, q_of_iter(t), dq_of_flux(t), nullptr);
+    return fault(true, q_of_iter(t), dq_of_flux(t));
   }
 
-  Fault fault(bool with_iteration, const D4* qsrc, const D4* dqsrc, const double* op_diag) {
+  Fault fault(bool with_iteration, const D4* qsrc, const D4* dqsrc) {
     const unsigned long long key = hctl_.get()->err_key;
     const unsigned phase = static_cast<unsigned>(key >> 61);
     const long long point = static_cast<long long>((key >> 22) & 0x7FFFFFFFull);
@@ -606,10 +620,10 @@ class Domain {
       return Fault(Status::positivity,
                    "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
     if (strict_)
-      k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), res_.get(), op_diag, gas_,
+      k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), mag_.get(), gas_,
                                          key, diag_.get());
     else
-      k_diagnose<false><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), res_.get(), op_diag, gas_,
+      k_diagnose<false><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), mag_.get(), gas_,
                                           key, diag_.get());
     double d[6];
     ck(cudaMemcpyAsync(d, diag_.get(), sizeof d, cudaMemcpyDeviceToHost, st_), "D2H diag");
@@ -656,6 +670,7 @@ class Domain {
   D4* res() { return res_.get(); }
   double* dt() { return dt_.get(); }
   double* mind() { return mind_.get(); }
+  double* mag() { return mag_.get(); }
   Ctl* dctl() { return ctl_.get(); }
   const Gas& gas() const { return gas_; }
   int width() const { return W_; }
@@ -680,7 +695,8 @@ class Domain {
     return out;
   }
   std::vector<KernelTime> kernel_times() const {
-    static const char* names[KT_COUNT] = {"q_variables", "q_derivatives", "flux_residual", "residue"};
+    static const char* names[KT_COUNT] = {"q_variables", "q_derivatives", "flux_residual", "state_update",
+                                          "residue"};
     std::vector<KernelTime> out;
     for (int k = 0; k < KT_COUNT; ++k) {
       const KTimer& t = hctl_.get()->kt[k];
@@ -699,6 +715,7 @@ class Domain {
   Gas gas_{};
   int kmax_ = 1, W_ = 8, d1_ = 0;
   std::size_t smem_ = 0;
+  int stride_ = 0;
   DBuf<double2> xy_, nrm_;
   DBuf<std::uint8_t> kind_, part_;
   DBuf<int> off_, nbr_;
@@ -845,7 +862,6 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
   const int blocks = (n + 255) / 256;
   const std::size_t nn = static_cast<std::size_t>(n);
   cudaStream_t st = d.stream();
-  DBuf<double> op_diag(2 * nn);
   // dq_[1] doubles as the scratch buffer of q_derivatives / publish.
   switch (op) {
     case Op::q_variables:
@@ -869,22 +885,23 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
       fa.res = d.res();
       fa.ctl = d.dctl();
       fa.kcap = d.kmax();
+      fa.stride = flux_stride(d.kmax());
       fa.mask = op == Op::flux_fused ? 0xF : (1 << (spec.axis * 2 + spec.sign));
       fa.first = op == Op::flux_fused ? 1 : spec.first;
-      flux_launch(d.width(), spec.fp_mode == 1, false, fa, d.smem(), st);
+      flux_launch(d.width(), spec.fp_mode == 1, fa, d.smem(), st);
       break;
     }
     case Op::timestep:
       k_op_timestep<<<blocks, 256, 0, st>>>(g, d.prim(), d.dt(), d.gas());
       break;
     case Op::state_update:
-      k_op_update<<<blocks, 256, 0, st>>>(g, d.prim(), d.res(), d.dt(), d.gas(), d.dctl(), op_diag.get());
+      k_op_update<<<blocks, 256, 0, st>>>(g, d.prim(), d.res(), d.dt(), d.gas(), d.dctl(), d.mag());
       break;
   }
   ck(cudaGetLastError(), "operator launch");
   ck(cudaStreamSynchronize(st), "operator");
   d.refresh_ctl();
-  if (d.failed()) throw d.fault(false, d.q_buf(0), d.dq_buf(0), op_diag.get());
+  if (d.failed()) throw d.fault(false, d.q_buf(0), d.dq_buf(0));
   if (op == Op::q_derivatives) {
     ck(cudaMemcpy(scratch, d.dq_buf(1), nn * 8 * sizeof(double), cudaMemcpyDeviceToHost), "D2H scratch");
     return;  // the store itself is untouched (reference kernels.hpp:30-35)

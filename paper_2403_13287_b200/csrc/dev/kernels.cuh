@@ -5,16 +5,17 @@
 // (runtime.cpp:251-269, reduce.hpp:11-17).  Per iteration (order 2, n_inner s):
 //
 //   k_sweep   x s   q, dq[b] -> dq[1-b]      one thread per point, bitwise
-//   k_flux          q[a], dq -> res -> dt -> prim' -> q[1-a], mag
-//                   (flux residual + local time step + forward Euler + wall
-//                    slip + next q-variables + residue summand, fused)
+//   k_flux          q[a], dq -> res                 (W lanes per point)
+//   k_update        res, prim -> dt -> prim' -> q[1-a], mag
+//                   (local time step + forward Euler + wall slip + next
+//                    q-variables + residue summand, one thread per point)
 //   k_tree_partial, k_tree_final   midpoint-tree sum of mag, bitwise
 //
 // Data layout in HBM (structure of arrays of 32-byte records):
 //   xy  double2[n]        nrm double2[n]     kind u8[n]     part u8[n]
 //   off int32[n+1]        nbr int32[nnz]     mind double[n] (geometry, per run)
 //   prim D4[n]            q[2] D4[n]         dq[2] D4[2n]  ({qx}, {qy} per point)
-//   res D4[n], dt double[n] (written on the copy-back iteration only), mag double[n]
+//   res D4[n] (every iteration), dt double[n] (copy-back iteration only), mag double[n]
 // Every D4 gather is one 256-bit LDG (one 32-byte sector).
 #pragma once
 
@@ -47,7 +48,7 @@ struct KTimer {
   unsigned long long total_ns, launches;
 };
 
-enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_RESIDUE = 3, KT_COUNT = 4 };
+enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_UPDATE = 3, KT_RESIDUE = 4, KT_COUNT = 5 };
 
 // Device control block (one per domain).
 struct Ctl {
@@ -68,10 +69,6 @@ struct Geo {
   const int* nbr;
   const double* mind;
   int n;
-};
-
-struct Gas {
-  double gamma, gm1, inv_gm1, cfl, det_tol;
 };
 
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
@@ -194,13 +191,14 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
 }
 
 // ---------------------------------------------------------------------------
-// Flux residual (+ fused update).  W lanes cooperate on one point, one lane
-// per stencil neighbour (pair): each pair's two reconstructions q~ -> prim and
-// split fluxes are computed once and shared by its x- and y-direction terms
+// Flux residual.  W lanes cooperate on one point, one lane per stencil
+// neighbour (pair): each pair's two reconstructions q~ -> prim and split
+// fluxes are computed once and shared by its x- and y-direction terms
 // (bitwise neutral: the reference recomputes identical values per direction).
 // Lanes then transpose through shared memory so each least-squares
 // accumulator is summed in ascending neighbour order, exactly as
-// directional_term does (kernels.cpp:37-64).
+// directional_term does (kernels.cpp:37-64).  The residual is written to
+// `res`; the per-point update runs in k_update (one thread per point).
 struct PairRec {
   double dx, dy;
   double dg[4][4];  // Delta G for Gx+, Gx-, Gy+, Gy- (only member directions valid)
@@ -209,32 +207,37 @@ struct PairRec {
 struct FluxArgs {
   Geo g;
   Gas gas;
-  const D4* q;      // q of this iteration (read)
-  const D4* dq;     // published derivatives (read)
-  D4* prim;         // FUSED: updated in place; OP: unused
-  D4* q_next;       // FUSED: q of the next iteration
-  D4* res;          // OP: accumulator in/out; FUSED: written on diag iteration
-  double* dt;       // FUSED: written on diag iteration
-  double* mag;      // FUSED: (dt*res0)^2 per point for the residue
+  const D4* q;    // q of this iteration
+  const D4* dq;   // published derivatives
+  D4* res;        // residual out (accumulated into when first == 0)
   Ctl* ctl;
-  unsigned long long* iter_t0;
-  int kcap;         // shared-memory stencil capacity per point
-  int mask;         // OP: directions to evaluate (bit d); FUSED: 0xF
-  int first;        // OP: zero the accumulator before adding
+  unsigned long long* iter_t0;  // per-iteration start stamps (first kernel only)
+  int kcap;       // shared-memory stencil capacity per point
+  int stride;     // doubles per point in shared memory (bank-conflict padding)
+  int mask;       // directions to evaluate (bit d: Gx+, Gx-, Gy+, Gy-)
+  int first;      // zero the accumulator before adding
 };
 
 __host__ __device__ constexpr int flux_points_per_block(int W) { return W >= 32 ? 8 : (W >= 16 ? 16 : 32); }
+__host__ __device__ constexpr int flux_min_blocks(int W) { return W >= 32 ? 1 : 3; }
 
-template <int W, bool S, bool FUSED>
-__global__ void __launch_bounds__(W * flux_points_per_block(W))
+// Pair-record stride per point, padded so consecutive points start 16 banks
+// apart (two sub-warps per 32-bank wavefront in phase B).
+__host__ __device__ inline int flux_stride(int kcap) {
+  int s = kcap * static_cast<int>(sizeof(PairRec) / 8);
+  while (s % 16 != 8) ++s;
+  return s;
+}
+
+template <int W, bool S>
+__global__ void __launch_bounds__(W * flux_points_per_block(W), flux_min_blocks(W))
     k_flux(FluxArgs a) {
   constexpr int P = flux_points_per_block(W);
   constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
   constexpr int NC = 16 / NOWN;                 // components per owning lane
   using A = Ar<S>;
   extern __shared__ double smem[];
-  PairRec* recs = reinterpret_cast<PairRec*>(smem);               // [P][kcap]
-  double* terms = smem + static_cast<size_t>(P) * a.kcap * (sizeof(PairRec) / 8);  // [P][16]
+  double* terms = smem + static_cast<size_t>(P) * a.stride;  // [P][16]
   __shared__ int s_skip;
 
   ktimer_begin(a.ctl, KT_FLUX);
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W))
     e0 = g.off[i];
     k = g.off[i + 1] - e0;
   }
-  PairRec* my = recs + static_cast<size_t>(slot) * a.kcap;
+  PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
 
   // ---- phase A: one lane per (point, neighbour) pair ----
   if (live) {
@@ -275,15 +278,11 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W))
         raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
         continue;
       }
-      double ri, u1i, u2i, pri, rn, u1n, u2n, prn;
-      prim_from_q<S>(ti[0], ti[1], ti[2], ti[3], a.gas.inv_gm1, a.gas.gm1, ri, u1i, u2i, pri);
-      prim_from_q<S>(tn[0], tn[1], tn[2], tn[3], a.gas.inv_gm1, a.gas.gm1, rn, u1n, u2n, prn);
-      if (!(ri > 0.0) || !(pri > 0.0) || !(rn > 0.0) || !(prn > 0.0)) {
+      FluxState fi, fn;
+      if (!reconstruct<S>(ti, a.gas, fi) || !reconstruct<S>(tn, a.gas, fn)) {
         raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
         continue;
       }
-      const FluxState fi = flux_state<S>(ri, u1i, u2i, pri, a.gas.inv_gm1, a.gas.gm1);
-      const FluxState fn = flux_state<S>(rn, u1n, u2n, prn, a.gas.inv_gm1, a.gas.gm1);
       const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
       const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
       double gi[4], gn[4];
@@ -359,85 +358,94 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W))
   }
   __syncthreads();
 
-  // ---- phase C: one thread per point ----
-  if (threadIdx.x < P && !s_skip) {
-    const int ip = blockIdx.x * P + threadIdx.x;
-    if (ip < g.n) {
-      const double* t = terms + threadIdx.x * 16;
-      const bool outer = g.kind[ip] == KIND_OUTER;
-      if constexpr (!FUSED) {
-        if (!outer) {
-          D4 acc = a.first ? D4{0.0, 0.0, 0.0, 0.0} : ld4_rw(a.res + ip);
+  // ---- residual: zero (or accumulator), then Gx+, Gx-, Gy+, Gy- in order
+  //      (kernels.cpp:124-138); one lane per (point, component) ----
+  if (threadIdx.x < 4 * P && !s_skip) {
+    const int sl = threadIdx.x >> 2, c = threadIdx.x & 3;
+    const int ip = blockIdx.x * P + sl;
+    if (ip < g.n && g.kind[ip] != KIND_OUTER) {
+      double* rp = reinterpret_cast<double*>(a.res + ip) + c;
+      double acc = a.first ? 0.0 : *rp;
 #pragma unroll
-          for (int d = 0; d < 4; ++d) {
-            if (!(a.mask & (1 << d))) continue;
-            acc.a = X::add(acc.a, t[d * 4 + 0]);
-            acc.b = X::add(acc.b, t[d * 4 + 1]);
-            acc.c = X::add(acc.c, t[d * 4 + 2]);
-            acc.d = X::add(acc.d, t[d * 4 + 3]);
-          }
-          st4(a.res + ip, acc);
-        }
-      } else {
-        const int it = a.ctl->iter;
-        const bool diag = it == a.ctl->diag_iter;
-        if (outer) {
-          st4(a.q_next + ip, ld4(a.q + ip));
-          a.mag[ip] = 0.0;
-          if (diag) a.dt[ip] = 0.0;
-        } else {
-          // residual: zero, then Gx+, Gx-, Gy+, Gy- (kernels.cpp:124-138)
-          double r[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            r[c] = X::add(X::add(X::add(X::add(0.0, t[c]), t[4 + c]), t[8 + c]), t[12 + c]);
-          const D4 s = ld4_rw(a.prim + ip);
-          // local time step (kernels.cpp:160-182)
-          const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
-          const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
-          const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
-          // forward Euler on the conserved state (kernels.cpp:184-219)
-          double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
-          double en = X::add(s.d / a.gas.gm1,
-                             X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
-          m = X::sub(m, X::mul(dt, r[0]));
-          mx = X::sub(mx, X::mul(dt, r[1]));
-          my_ = X::sub(my_, X::mul(dt, r[2]));
-          en = X::sub(en, X::mul(dt, r[3]));
-          bool ok = m > 0.0;
-          double u1 = 0.0, u2 = 0.0, p = 0.0;
-          if (ok) {
-            u1 = mx / m;
-            u2 = my_ / m;
-            p = X::mul(a.gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
-            ok = p > 0.0;
-          }
-          if (!ok) {
-            // keep the failing conserved value for the diagnostic message
-            a.res[ip] = D4{m > 0.0 ? p : m, m > 0.0 ? 1.0 : 0.0, 0.0, 0.0};
-            raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], ip, 0, 0));
-          } else {
-            if (g.kind[ip] == KIND_WALL) {
-              const double2 nv = g.nrm[ip];
-              const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
-              u1 = X::sub(u1, X::mul(un, nv.x));
-              u2 = X::sub(u2, X::mul(un, nv.y));
-            }
-            st4(a.prim + ip, D4{m, u1, u2, p});
-            st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
-            const double dm = X::mul(dt, r[0]);
-            a.mag[ip] = X::mul(dm, dm);
-            if (diag) {
-              st4(a.res + ip, D4{r[0], r[1], r[2], r[3]});
-              a.dt[ip] = dt;
-            }
-          }
-        }
-      }
+      for (int d = 0; d < 4; ++d)
+        if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
+      *rp = acc;
     }
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+}
+
+// Local time step + forward-Euler update + wall slip + next q-variables +
+// residue summand, one thread per point (kernels.cpp:68-80, 160-223).
+struct UpdateArgs {
+  Geo g;
+  Gas gas;
+  const D4* q;   // q of this iteration (copied forward for outer points)
+  const D4* res; // residual of this iteration
+  D4* prim;      // updated in place
+  D4* q_next;
+  double* dt;    // written on the diag (copy-back) iteration
+  double* mag;   // (dt * res0)^2
+  Ctl* ctl;
+};
+
+__global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
+  __shared__ int s_skip;
+  ktimer_begin(a.ctl, KT_UPDATE);
+  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->err_key) != kNoErr;
+  __syncthreads();
+  const int ip = blockIdx.x * blockDim.x + threadIdx.x;
+  const Geo& g = a.g;
+  if (!s_skip && ip < g.n) {
+    const bool diag = a.ctl->iter == a.ctl->diag_iter;
+    if (g.kind[ip] == KIND_OUTER) {
+      st4(a.q_next + ip, ld4(a.q + ip));
+      a.mag[ip] = 0.0;
+      if (diag) a.dt[ip] = 0.0;
+    } else {
+      const D4 r = ld4(a.res + ip);
+      const D4 s = ld4_rw(a.prim + ip);
+      const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
+      const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
+      const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
+      double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
+      double en = X::add(s.d / a.gas.gm1,
+                         X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
+      m = X::sub(m, X::mul(dt, r.a));
+      mx = X::sub(mx, X::mul(dt, r.b));
+      my_ = X::sub(my_, X::mul(dt, r.c));
+      en = X::sub(en, X::mul(dt, r.d));
+      bool ok = m > 0.0;
+      double u1 = 0.0, u2 = 0.0, p = 0.0;
+      if (ok) {
+        u1 = mx / m;
+        u2 = my_ / m;
+        p = X::mul(a.gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
+        ok = p > 0.0;
+      }
+      if (!ok) {
+        // keep the failing conserved value for the diagnostic message
+        a.dt[ip] = m > 0.0 ? p : m;
+        a.mag[ip] = m > 0.0 ? 1.0 : 0.0;
+        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], ip, 0, 0));
+      } else {
+        if (g.kind[ip] == KIND_WALL) {
+          const double2 nv = g.nrm[ip];
+          const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
+          u1 = X::sub(u1, X::mul(un, nv.x));
+          u2 = X::sub(u2, X::mul(un, nv.y));
+        }
+        st4(a.prim + ip, D4{m, u1, u2, p});
+        st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
+        const double dm = X::mul(dt, r.a);
+        a.mag[ip] = X::mul(dm, dm);
+        if (diag) a.dt[ip] = dt;
+      }
+    }
+  }
+  __syncthreads();
+  ktimer_end(a.ctl, KT_UPDATE, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -455,8 +463,8 @@ __global__ void k_op_timestep(Geo g, const D4* prim, double* dt, Gas gas) {
   dt[i] = X::mul(gas.cfl, g.mind[i]) / X::add(speed, sound);
 }
 
-__global__ void k_op_update(Geo g, D4* prim, const D4* res, const double* dt, Gas gas,
-                            Ctl* ctl, double* diag) {
+__global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas, Ctl* ctl,
+                            double* which) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n || g.kind[i] == KIND_OUTER) return;
   const D4 s = ld4_rw(prim + i);
@@ -474,16 +482,16 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, const double* dt, Ga
   my_ = X::sub(my_, X::mul(h, r.c));
   en = X::sub(en, X::mul(h, r.d));
   if (!(m > 0.0)) {
-    diag[2 * i] = m;
-    diag[2 * i + 1] = 0.0;
+    dt[i] = m;
+    which[i] = 0.0;
     raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
     return;
   }
   double u1 = mx / m, u2 = my_ / m;
   const double p = X::mul(gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
   if (!(p > 0.0)) {
-    diag[2 * i] = p;
-    diag[2 * i + 1] = 1.0;
+    dt[i] = p;
+    which[i] = 1.0;
     raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
     return;
   }
