@@ -115,6 +115,11 @@ int lskum_b200_session_flush_l2(lskum_b200_session* s);
 int lskum_b200_fp64_peak(int device, double* tflops);
 void lskum_b200_session_destroy(lskum_b200_session* s);
 
+/* ---- verification hook ----
+ * Evaluates CUDA libdevice erf (fn 0) / exp (fn 1) into ref[] and the engine's
+ * constant-table replicas used by the flux kernel into ours[] (must be bitwise equal). */
+int lskum_b200_math_selftest(int fn, const double* in, int64_t n, double* ref, double* ours);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -86,32 +87,70 @@ std::size_t flux_smem_bytes(int W, int kcap) {
   return (static_cast<std::size_t>(P) * flux_stride(kcap) + static_cast<std::size_t>(P) * 16) * sizeof(double);
 }
 
-template <int W, bool S>
+template <int W, bool S, int MB>
 void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   static std::size_t configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > configured[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_flux<W, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux)");
     configured[dev & 63] = smem;
   }
   const int P = flux_points_per_block(W);
-  const int blocks = (a.g.n + P - 1) / P;
-  k_flux<W, S><<<blocks, W * P, smem, st>>>(a);
+  static int resident[64] = {};
+  if (!resident[dev & 63]) {
+    int per_sm = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux<W, S, MB>, W * P, smem), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    resident[dev & 63] = std::max(1, per_sm) * sms;
+  }
+  const int groups = (a.g.n + P - 1) / P;
+  k_flux<W, S, MB><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
+}
+
+int sweep_grid(int n) {
+  static int resident[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!resident[dev & 63]) {
+    int per_sm = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep, 256, 0), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    resident[dev & 63] = std::max(1, per_sm) * sms;
+  }
+  return std::max(1, std::min((n + 255) / 256, resident[dev & 63]));
+}
+
+// Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per
+// SM (LSKUM_FLUX_MINB = 2 | 3 | 4, default 3).
+int flux_min_blocks() {
+  static int mb = [] {
+    const char* e = std::getenv("LSKUM_FLUX_MINB");
+    const int v = e ? std::atoi(e) : 3;
+    return (v >= 2 && v <= 4) ? v : 3;
+  }();
+  return mb;
+}
+
+template <bool S>
+void flux_launch_s(int W, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
+  if (W == 8) {
+    const int mb = flux_min_blocks();
+    if (mb == 2) flux_launch_t<8, S, 2>(a, smem, st);
+    else if (mb == 4) flux_launch_t<8, S, 4>(a, smem, st);
+    else flux_launch_t<8, S, 3>(a, smem, st);
+  } else if (W == 16) {
+    flux_launch_t<16, S, 2>(a, smem, st);
+  } else {
+    flux_launch_t<32, S, 1>(a, smem, st);
+  }
 }
 
 void flux_launch(int W, bool strict, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
-  if (strict) {
-    if (W == 8) flux_launch_t<8, true>(a, smem, st);
-    else if (W == 16) flux_launch_t<16, true>(a, smem, st);
-    else flux_launch_t<32, true>(a, smem, st);
-  } else {
-    if (W == 8) flux_launch_t<8, false>(a, smem, st);
-    else if (W == 16) flux_launch_t<16, false>(a, smem, st);
-    else flux_launch_t<32, false>(a, smem, st);
-  }
+  if (strict) flux_launch_s<true>(W, a, smem, st);
+  else flux_launch_s<false>(W, a, smem, st);
 }
 
 // Depth of the per-block nodes of the residue tree: at most ~8 values per
@@ -265,6 +304,9 @@ class Domain {
       gas_.half_pow = (std::fabs(m - mr) < 1e-9 && mr >= 1.0 && mr <= 40.0) ? static_cast<int>(mr) : -1;
     }
     kmax_ = std::max(1, ps.max_degree());
+    kfix_ = kmax_;
+    for (std::int32_t i = 0; i < ps.n() && kfix_ > 0; ++i)
+      if (ps.off[i + 1] - ps.off[i] != kmax_ || ps.off[i] != static_cast<std::int64_t>(i) * kmax_) kfix_ = 0;
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
     stride_ = flux_stride(kmax_);
@@ -344,6 +386,7 @@ class Domain {
     g.nbr = nbr_.get();
     g.mind = mind_.get();
     g.n = n_;
+    g.kfix = kfix_;
     return g;
   }
 
@@ -467,7 +510,7 @@ class Domain {
     if (order_ == 2) {
       for (int s = 0; s < inner_; ++s) {
         if (timed && s == 0) record_ext(kev_[0]);
-        k_sweep<<<(n_ + 255) / 256, 256, 0, st_>>>(g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(),
+        k_sweep<<<sweep_grid(n_), 256, 0, st_>>>(g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(),
                                                    gas_, ctl_.get(), s == 0 ? it0_.get() : nullptr);
         if (timed && s == 0) record_ext(kev_[1]);
         b ^= 1;
@@ -713,7 +756,7 @@ class Domain {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, poll_ev_[kPolls] = {}, kev_[4] = {};
   DBuf<double> flush_;
   Gas gas_{};
-  int kmax_ = 1, W_ = 8, d1_ = 0;
+  int kmax_ = 1, kfix_ = 0, W_ = 8, d1_ = 0;
   std::size_t smem_ = 0;
   int stride_ = 0;
   DBuf<double2> xy_, nrm_;
@@ -825,6 +868,31 @@ void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms) {
 }
 void session_flush_l2(Session* s) { s->dom->flush_l2(); }
 
+__global__ void k_math_selftest(int fn, const double* in, long long n, double* ref, double* ours) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double x = in[i];
+    if (fn == 0) {
+      ref[i] = erf(x);
+      ours[i] = lk_erf(x);
+    } else {
+      ref[i] = exp(x);
+      ours[i] = lk_exp(x);
+    }
+  }
+}
+
+void engine_math_selftest(int fn, const double* in, std::int64_t n, double* ref, double* ours) {
+  if (n <= 0) return;
+  DBuf<double> d_in(static_cast<std::size_t>(n)), d_ref(static_cast<std::size_t>(n)),
+      d_ours(static_cast<std::size_t>(n));
+  ck(cudaMemcpy(d_in.get(), in, n * sizeof(double), cudaMemcpyHostToDevice), "H2D selftest");
+  k_math_selftest<<<1184, 256>>>(fn, d_in.get(), n, d_ref.get(), d_ours.get());
+  ck(cudaGetLastError(), "selftest launch");
+  ck(cudaMemcpy(ref, d_ref.get(), n * sizeof(double), cudaMemcpyDeviceToHost), "D2H selftest");
+  ck(cudaMemcpy(ours, d_ours.get(), n * sizeof(double), cudaMemcpyDeviceToHost), "D2H selftest");
+}
+
 double engine_fp64_peak_tflops(int device) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   int sms = 0;
@@ -868,7 +936,8 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
       k_qvar<<<blocks, 256, 0, st>>>(g, d.prim(), d.q_buf(0), d.gas(), d.dctl());
       break;
     case Op::q_derivatives:
-      k_sweep<<<blocks, 256, 0, st>>>(g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(), nullptr);
+      k_sweep<<<sweep_grid(n), 256, 0, st>>>(g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(),
+                                             nullptr);
       break;
     case Op::publish:
       ck(cudaMemcpyAsync(d.dq_buf(1), scratch, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D scratch");

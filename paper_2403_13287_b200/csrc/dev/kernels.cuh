@@ -69,7 +69,18 @@ struct Geo {
   const int* nbr;
   const double* mind;
   int n;
+  int kfix;  // uniform stencil size (offsets are then i*kfix), 0 = use CSR offsets
 };
+
+__device__ __forceinline__ void stencil_of(const Geo& g, int i, int& e0, int& k) {
+  if (g.kfix > 0) {
+    e0 = i * g.kfix;
+    k = g.kfix;
+  } else {
+    e0 = g.off[i];
+    k = g.off[i + 1] - e0;
+  }
+}
 
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
@@ -146,14 +157,15 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
   ktimer_begin(ctl, KT_SWEEP);
   if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (!s_skip && i < g.n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n;
+       i += gridDim.x * blockDim.x) {
     const double2 pi = g.xy[i];
     const D4 qi = ld4(q + i), qxi = ld4(dq_in + 2 * i), qyi = ld4(dq_in + 2 * i + 1);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
-    const int e1 = g.off[i + 1];
-    for (int e = g.off[i]; e < e1; ++e) {
+    int e0, k;
+    stencil_of(g, i, e0, k);
+    for (int e = e0; e < e0 + k; ++e) {
       const int nb = g.nbr[e];
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
@@ -219,7 +231,6 @@ struct FluxArgs {
 };
 
 __host__ __device__ constexpr int flux_points_per_block(int W) { return W >= 32 ? 8 : (W >= 16 ? 16 : 32); }
-__host__ __device__ constexpr int flux_min_blocks(int W) { return W >= 32 ? 1 : 3; }
 
 // Pair-record stride per point, padded so consecutive points start 16 banks
 // apart (two sub-warps per 32-bank wavefront in phase B).
@@ -229,9 +240,8 @@ __host__ __device__ inline int flux_stride(int kcap) {
   return s;
 }
 
-template <int W, bool S>
-__global__ void __launch_bounds__(W * flux_points_per_block(W), flux_min_blocks(W))
-    k_flux(FluxArgs a) {
+template <int W, bool S, int MB>
+__global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxArgs a) {
   constexpr int P = flux_points_per_block(W);
   constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
   constexpr int NC = 16 / NOWN;                 // components per owning lane
@@ -245,132 +255,135 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), flux_min_blocks(
   __syncthreads();
   const int lane = threadIdx.x % W;
   const int slot = threadIdx.x / W;
-  const int i = blockIdx.x * P + slot;
   const Geo& g = a.g;
-  const bool live = !s_skip && i < g.n && g.kind[i] != KIND_OUTER;
-  int k = 0, e0 = 0;
-  if (live) {
-    e0 = g.off[i];
-    k = g.off[i + 1] - e0;
-  }
   PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
+  const int groups = (g.n + P - 1) / P;
+  // Persistent blocks: one resident block per slot walks groups of P points,
+  // amortising the start-up latency and the timer atomics.
+  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x) {
+    const int i = grp * P + slot;
+    const bool live = i < g.n && g.kind[i] != KIND_OUTER;
+    int k = 0, e0 = 0;
+    if (live) stencil_of(g, i, e0, k);
 
-  // ---- phase A: one lane per (point, neighbour) pair ----
-  if (live) {
-    const double2 pi = g.xy[i];
-    const D4 qi = ld4(a.q + i), qxi = ld4(a.dq + 2 * i), qyi = ld4(a.dq + 2 * i + 1);
-    for (int j = lane; j < k; j += W) {
-      const int nb = g.nbr[e0 + j];
-      const double2 pn = g.xy[nb];
-      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
-      PairRec& r = my[j];
-      r.dx = dx;
-      r.dy = dy;
-      const unsigned dfirst = dx <= 0.0 ? 0u : 1u;
-      double ti[4], tn[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
-        tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
-      }
-      if (!(ti[3] < 0.0) || !(tn[3] < 0.0)) {
-        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
-        continue;
-      }
-      FluxState fi, fn;
-      if (!reconstruct<S>(ti, a.gas, fi) || !reconstruct<S>(tn, a.gas, fn)) {
-        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
-        continue;
-      }
-      const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
-      const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
-      double gi[4], gn[4];
-      if (xp || xm) {
-        const AxisTerms ai = axis_terms<S>(fi, 0), an = axis_terms<S>(fn, 0);
-        if (xp) {
-          split_flux<S>(fi, ai, 0, false, gi);
-          split_flux<S>(fn, an, 0, false, gn);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
+    // ---- phase A: one lane per (point, neighbour) pair ----
+    if (live) {
+      const double2 pi = g.xy[i];
+      const D4 qi = ld4(a.q + i), qxi = ld4(a.dq + 2 * i), qyi = ld4(a.dq + 2 * i + 1);
+      for (int j = lane; j < k; j += W) {
+        const int nb = g.nbr[e0 + j];
+        const double2 pn = g.xy[nb];
+        const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+        const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+        PairRec& r = my[j];
+        r.dx = dx;
+        r.dy = dy;
+        const unsigned dfirst = dx <= 0.0 ? 0u : 1u;
+        double ti[4], tn[4];
+  #pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
+          tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
         }
-        if (xm) {
-          split_flux<S>(fi, ai, 0, true, gi);
-          split_flux<S>(fn, an, 0, true, gn);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
+        if (!(ti[3] < 0.0) || !(tn[3] < 0.0)) {
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+          continue;
         }
-      }
-      if (yp || ym) {
-        const AxisTerms ai = axis_terms<S>(fi, 1), an = axis_terms<S>(fn, 1);
-        if (yp) {
-          split_flux<S>(fi, ai, 1, false, gi);
-          split_flux<S>(fn, an, 1, false, gn);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
+        FluxState fi, fn;
+        if (!reconstruct<S>(ti, a.gas, fi) || !reconstruct<S>(tn, a.gas, fn)) {
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+          continue;
         }
-        if (ym) {
-          split_flux<S>(fi, ai, 1, true, gi);
-          split_flux<S>(fn, an, 1, true, gn);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[3][c] = X::sub(gn[c], gi[c]);
+        const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
+        const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
+        double gi[4], gn[4];
+        if (xp || xm) {
+          const AxisTerms ai = axis_terms<S>(fi, 0), an = axis_terms<S>(fn, 0);
+          if (xp) {
+            split_flux<S>(fi, ai, 0, false, gi);
+            split_flux<S>(fn, an, 0, false, gn);
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
+          }
+          if (xm) {
+            split_flux<S>(fi, ai, 0, true, gi);
+            split_flux<S>(fn, an, 0, true, gn);
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
+          }
+        }
+        if (yp || ym) {
+          const AxisTerms ai = axis_terms<S>(fi, 1), an = axis_terms<S>(fn, 1);
+          if (yp) {
+            split_flux<S>(fi, ai, 1, false, gi);
+            split_flux<S>(fn, an, 1, false, gn);
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
+          }
+          if (ym) {
+            split_flux<S>(fi, ai, 1, true, gi);
+            split_flux<S>(fn, an, 1, true, gn);
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) r.dg[3][c] = X::sub(gn[c], gi[c]);
+          }
         }
       }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // ---- phase B: ordered least-squares sums + 2x2 solve per direction ----
-  if (live && lane < NOWN) {
-    const int d = lane / (4 / NC);                // direction owned
-    const int c0 = (lane % (4 / NC)) * NC;        // first component owned
-    if (a.mask & (1 << d)) {
-      double sxx = 0.0, sxy = 0.0, syy = 0.0, bx[NC], by[NC];
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) bx[cc] = by[cc] = 0.0;
-      for (int j = 0; j < k; ++j) {
-        const double dx = my[j].dx, dy = my[j].dy;
-        const double dd = d < 2 ? dx : dy;
-        const bool member = (d & 1) ? dd >= 0.0 : dd <= 0.0;
-        if (!member) continue;
-        sxx = A::add(sxx, A::mul(dx, dx));
-        sxy = A::add(sxy, A::mul(dx, dy));
-        syy = A::add(syy, A::mul(dy, dy));
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-          const double df = my[j].dg[d][c0 + cc];
-          bx[cc] = A::add(bx[cc], A::mul(dx, df));
-          by[cc] = A::add(by[cc], A::mul(dy, df));
+    // ---- phase B: ordered least-squares sums + 2x2 solve per direction ----
+    if (live && lane < NOWN) {
+      const int d = lane / (4 / NC);                // direction owned
+      const int c0 = (lane % (4 / NC)) * NC;        // first component owned
+      if (a.mask & (1 << d)) {
+        double sxx = 0.0, sxy = 0.0, syy = 0.0, bx[NC], by[NC];
+  #pragma unroll
+        for (int cc = 0; cc < NC; ++cc) bx[cc] = by[cc] = 0.0;
+        for (int j = 0; j < k; ++j) {
+          const double dx = my[j].dx, dy = my[j].dy;
+          const double dd = d < 2 ? dx : dy;
+          const bool member = (d & 1) ? dd >= 0.0 : dd <= 0.0;
+          if (!member) continue;
+          sxx = A::add(sxx, A::mul(dx, dx));
+          sxy = A::add(sxy, A::mul(dx, dy));
+          syy = A::add(syy, A::mul(dy, dy));
+  #pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            const double df = my[j].dg[d][c0 + cc];
+            bx[cc] = A::add(bx[cc], A::mul(dx, df));
+            by[cc] = A::add(by[cc], A::mul(dy, df));
+          }
         }
-      }
-      const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
-      if (!(det > a.gas.det_tol)) {
-        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, d, kSolveSlot));
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-          const double t = d < 2 ? A::sub(A::mul(syy, bx[cc]), A::mul(sxy, by[cc])) / det
-                                 : A::sub(A::mul(sxx, by[cc]), A::mul(sxy, bx[cc])) / det;
-          terms[slot * 16 + d * 4 + c0 + cc] = t;
+        const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
+        if (!(det > a.gas.det_tol)) {
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, d, kSolveSlot));
+        } else {
+  #pragma unroll
+          for (int cc = 0; cc < NC; ++cc) {
+            const double t = d < 2 ? A::sub(A::mul(syy, bx[cc]), A::mul(sxy, by[cc])) / det
+                                   : A::sub(A::mul(sxx, by[cc]), A::mul(sxy, bx[cc])) / det;
+            terms[slot * 16 + d * 4 + c0 + cc] = t;
+          }
         }
       }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // ---- residual: zero (or accumulator), then Gx+, Gx-, Gy+, Gy- in order
-  //      (kernels.cpp:124-138); one lane per (point, component) ----
-  if (threadIdx.x < 4 * P && !s_skip) {
-    const int sl = threadIdx.x >> 2, c = threadIdx.x & 3;
-    const int ip = blockIdx.x * P + sl;
-    if (ip < g.n && g.kind[ip] != KIND_OUTER) {
-      double* rp = reinterpret_cast<double*>(a.res + ip) + c;
-      double acc = a.first ? 0.0 : *rp;
-#pragma unroll
-      for (int d = 0; d < 4; ++d)
-        if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
-      *rp = acc;
+    // ---- residual: zero (or accumulator), then Gx+, Gx-, Gy+, Gy- in order
+    //      (kernels.cpp:124-138); one lane per (point, component) ----
+    if (threadIdx.x < 4 * P) {
+      const int sl = threadIdx.x >> 2, c = threadIdx.x & 3;
+      const int ip = grp * P + sl;
+      if (ip < g.n && g.kind[ip] != KIND_OUTER) {
+        double* rp = reinterpret_cast<double*>(a.res + ip) + c;
+        double acc = a.first ? 0.0 : *rp;
+  #pragma unroll
+        for (int d = 0; d < 4; ++d)
+          if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
+        *rp = acc;
+      }
     }
+    __syncthreads();  // terms/records are reused by the next group
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);

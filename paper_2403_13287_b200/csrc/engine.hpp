@@ -43,6 +43,8 @@ void session_download(Session* s);
 void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms);
 void session_flush_l2(Session* s);
 double engine_fp64_peak_tflops(int device);
+// Evaluates libdevice erf/exp (fn 0/1) and the engine's constant-table replicas.
+void engine_math_selftest(int fn, const double* in, std::int64_t n, double* ref, double* ours);
 void session_close(Session* s);
 
 // Per-phase operators on the whole cloud (reference kernels.hpp:25-63).

@@ -517,6 +517,12 @@ int lskum_b200_fp64_peak(int device, double* tflops) {
   return guard([&] { *tflops = lskb::engine_fp64_peak_tflops(device); });
 }
 
+int lskum_b200_math_selftest(int fn, const double* in, int64_t n, double* ref, double* ours) {
+  if (n > 0 && (!in || !ref || !ours)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
+  if (fn != 0 && fn != 1) return fail(LSKUM_ERR_ARGUMENT, "fn must be 0 (erf) or 1 (exp)");
+  return guard([&] { lskb::engine_math_selftest(fn, in, n, ref, ours); });
+}
+
 void lskum_b200_session_destroy(lskum_b200_session* s) { delete s; }
 
 }  // extern "C"
