@@ -290,42 +290,38 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
           continue;
         }
         FluxState fi, fn;
-        if (!reconstruct<S>(ti, a.gas, fi) || !reconstruct<S>(tn, a.gas, fn)) {
+        if (!reconstruct2<S>(ti, tn, a.gas, fi, fn)) {
           raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
           continue;
         }
         const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
         const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
+        AxisTerms at[4];
+        axis_terms4<S>(fi, fn, at);
         double gi[4], gn[4];
-        if (xp || xm) {
-          const AxisTerms ai = axis_terms<S>(fi, 0), an = axis_terms<S>(fn, 0);
-          if (xp) {
-            split_flux<S>(fi, ai, 0, false, gi);
-            split_flux<S>(fn, an, 0, false, gn);
-  #pragma unroll
-            for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
-          }
-          if (xm) {
-            split_flux<S>(fi, ai, 0, true, gi);
-            split_flux<S>(fn, an, 0, true, gn);
-  #pragma unroll
-            for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
-          }
+        if (xp) {
+          split_flux<S>(fi, at[0], 0, false, gi);
+          split_flux<S>(fn, at[1], 0, false, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
         }
-        if (yp || ym) {
-          const AxisTerms ai = axis_terms<S>(fi, 1), an = axis_terms<S>(fn, 1);
-          if (yp) {
-            split_flux<S>(fi, ai, 1, false, gi);
-            split_flux<S>(fn, an, 1, false, gn);
-  #pragma unroll
-            for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
-          }
-          if (ym) {
-            split_flux<S>(fi, ai, 1, true, gi);
-            split_flux<S>(fn, an, 1, true, gn);
-  #pragma unroll
-            for (int c = 0; c < 4; ++c) r.dg[3][c] = X::sub(gn[c], gi[c]);
-          }
+        if (xm) {
+          split_flux<S>(fi, at[0], 0, true, gi);
+          split_flux<S>(fn, at[1], 0, true, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
+        }
+        if (yp) {
+          split_flux<S>(fi, at[2], 1, false, gi);
+          split_flux<S>(fn, at[3], 1, false, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
+        }
+        if (ym) {
+          split_flux<S>(fi, at[2], 1, true, gi);
+          split_flux<S>(fn, at[3], 1, true, gn);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r.dg[3][c] = X::sub(gn[c], gi[c]);
         }
       }
     }
