@@ -87,13 +87,14 @@ std::size_t flux_smem_bytes(int W, int kcap) {
   return (static_cast<std::size_t>(P) * flux_stride(kcap) + static_cast<std::size_t>(P) * 16) * sizeof(double);
 }
 
-template <int W, bool S, int MB>
+template <int W, bool S, int MB, bool ST>
 void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
+  if (ST) smem += flux_stage_bytes(W, flux_points_per_block(W));
   static std::size_t configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > configured[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux<W, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_flux<W, S, MB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux)");
     configured[dev & 63] = smem;
@@ -102,12 +103,12 @@ void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   static int resident[64] = {};
   if (!resident[dev & 63]) {
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux<W, S, MB>, W * P, smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux<W, S, MB, ST>, W * P, smem), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int groups = (a.g.n + P - 1) / P;
-  k_flux<W, S, MB><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
+  k_flux<W, S, MB, ST><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
 }
 
 int sweep_grid(int n) {
@@ -123,8 +124,8 @@ int sweep_grid(int n) {
   return std::max(1, std::min((n + 255) / 256, resident[dev & 63]));
 }
 
-// Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per
-// SM (LSKUM_FLUX_MINB = 2 | 3 | 4, default 3).
+// Register/occupancy trade-off of the unstaged W=8 kernel: minimum resident
+// blocks per SM (LSKUM_FLUX_MINB = 2 | 3, default 3).
 int flux_min_blocks() {
   static int mb = [] {
     const char* e = std::getenv("LSKUM_FLUX_MINB");
@@ -134,17 +135,29 @@ int flux_min_blocks() {
   return mb;
 }
 
+// Gather staging (cp.async) for uniform stencils, LSKUM_FLUX_STAGE=0 disables.
+bool flux_staging() {
+  static bool on = [] {
+    const char* e = std::getenv("LSKUM_FLUX_STAGE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <bool S>
 void flux_launch_s(int W, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   if (W == 8) {
+    if (flux_staging() && a.g.kfix > 0 && a.g.kfix <= 8) {
+      flux_launch_t<8, S, 2, true>(a, smem, st);
+      return;
+    }
     const int mb = flux_min_blocks();
-    if (mb == 2) flux_launch_t<8, S, 2>(a, smem, st);
-    else if (mb == 4) flux_launch_t<8, S, 4>(a, smem, st);
-    else flux_launch_t<8, S, 3>(a, smem, st);
+    if (mb == 2) flux_launch_t<8, S, 2, false>(a, smem, st);
+    else flux_launch_t<8, S, 3, false>(a, smem, st);
   } else if (W == 16) {
-    flux_launch_t<16, S, 2>(a, smem, st);
+    flux_launch_t<16, S, 2, false>(a, smem, st);
   } else {
-    flux_launch_t<32, S, 1>(a, smem, st);
+    flux_launch_t<32, S, 1, false>(a, smem, st);
   }
 }
 

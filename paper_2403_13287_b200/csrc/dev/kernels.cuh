@@ -216,6 +216,30 @@ struct PairRec {
   double dg[4][4];  // Delta G for Gx+, Gx-, Gy+, Gy- (only member directions valid)
 };
 
+// Staged neighbour data for one lane (cp.async, 7 x 16 B).
+struct alignas(16) Gathered {
+  double2 xy;
+  D4 q, qx, qy;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void stage_point(Gathered* dst, const double2* xy, const D4* q, const D4* dq, int p) {
+  cp_async16(&dst->xy, xy + p);
+  cp_async16(&dst->q, q + p);
+  cp_async16(reinterpret_cast<char*>(&dst->q) + 16, reinterpret_cast<const char*>(q + p) + 16);
+  const char* d = reinterpret_cast<const char*>(dq + 2 * p);
+  char* o = reinterpret_cast<char*>(&dst->qx);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) cp_async16(o + 16 * k, d + 16 * k);
+}
+
 struct FluxArgs {
   Geo g;
   Gas gas;
@@ -230,6 +254,12 @@ struct FluxArgs {
   int first;      // zero the accumulator before adding
 };
 
+// Shared-memory bytes of the gather staging area (two buffers of P points x
+// (W neighbours + the point itself)).
+__host__ __device__ constexpr int flux_stage_bytes(int W, int P) {
+  return 2 * P * (W + 1) * static_cast<int>(sizeof(Gathered));
+}
+
 __host__ __device__ constexpr int flux_points_per_block(int W) { return W >= 32 ? 8 : (W >= 16 ? 16 : 32); }
 
 // Pair-record stride per point, padded so consecutive points start 16 banks
@@ -240,7 +270,10 @@ __host__ __device__ inline int flux_stride(int kcap) {
   return s;
 }
 
-template <int W, bool S, int MB>
+// STAGED (uniform stencils with k <= W): the neighbour and own-point records
+// of the next group are copied into shared memory with cp.async while the
+// current group computes, hiding the dependent index -> gather latency.
+template <int W, bool S, int MB, bool STAGED>
 __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxArgs a) {
   constexpr int P = flux_points_per_block(W);
   constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
@@ -258,23 +291,76 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
   const Geo& g = a.g;
   PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
   const int groups = (g.n + P - 1) / P;
+  Gathered* stage = reinterpret_cast<Gathered*>(terms + P * 16);  // [2][P * (W + 1)]
+  // index of this lane's neighbour in group G (-1 if none)
+  auto next_index = [&](int G) {
+    const int ip = G * P + slot;
+    return (G < groups && ip < g.n && lane < g.kfix) ? g.nbr[ip * g.kfix + lane] : -1;
+  };
+  auto stage_group = [&](int G, int buf, int nb) {
+    Gathered* base = stage + buf * P * (W + 1);
+    const int ip = G * P + slot;
+    if (G < groups && ip < g.n) {
+      if (nb >= 0) stage_point(base + threadIdx.x, g.xy, a.q, a.dq, nb);
+      if (lane == 0) stage_point(base + P * W + slot, g.xy, a.q, a.dq, ip);
+    }
+    cp_async_commit();
+  };
+  int nb_next = -1;
+  if constexpr (STAGED) {
+    if (!s_skip) {
+      stage_group(blockIdx.x, 0, next_index(blockIdx.x));
+      nb_next = next_index(blockIdx.x + gridDim.x);
+    }
+  }
   // Persistent blocks: one resident block per slot walks groups of P points,
   // amortising the start-up latency and the timer atomics.
-  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x) {
+  int t = 0;
+  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x, ++t) {
     const int i = grp * P + slot;
+    if constexpr (STAGED) {
+      stage_group(grp + gridDim.x, (t + 1) & 1, nb_next);
+      nb_next = next_index(grp + 2 * gridDim.x);
+      cp_async_wait<1>();
+      __syncthreads();
+    }
     const bool live = i < g.n && g.kind[i] != KIND_OUTER;
     int k = 0, e0 = 0;
     if (live) stencil_of(g, i, e0, k);
 
     // ---- phase A: one lane per (point, neighbour) pair ----
     if (live) {
-      const double2 pi = g.xy[i];
-      const D4 qi = ld4(a.q + i), qxi = ld4(a.dq + 2 * i), qyi = ld4(a.dq + 2 * i + 1);
+      double2 pi;
+      D4 qi, qxi, qyi;
+      if constexpr (STAGED) {
+        const Gathered& o = stage[(t & 1) * P * (W + 1) + P * W + slot];
+        pi = o.xy;
+        qi = o.q;
+        qxi = o.qx;
+        qyi = o.qy;
+      } else {
+        pi = g.xy[i];
+        qi = ld4(a.q + i);
+        qxi = ld4(a.dq + 2 * i);
+        qyi = ld4(a.dq + 2 * i + 1);
+      }
       for (int j = lane; j < k; j += W) {
         const int nb = g.nbr[e0 + j];
-        const double2 pn = g.xy[nb];
+        double2 pn;
+        D4 qn, qxn, qyn;
+        if constexpr (STAGED) {
+          const Gathered& o = stage[(t & 1) * P * (W + 1) + threadIdx.x];
+          pn = o.xy;
+          qn = o.q;
+          qxn = o.qx;
+          qyn = o.qy;
+        } else {
+          pn = g.xy[nb];
+          qn = ld4(a.q + nb);
+          qxn = ld4(a.dq + 2 * nb);
+          qyn = ld4(a.dq + 2 * nb + 1);
+        }
         const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-        const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
         PairRec& r = my[j];
         r.dx = dx;
         r.dy = dy;
@@ -379,8 +465,9 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
         *rp = acc;
       }
     }
-    __syncthreads();  // terms/records are reused by the next group
+    __syncthreads();  // terms/records/staging are reused by later groups
   }
+  if constexpr (STAGED) cp_async_wait<0>();
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
 }
