@@ -135,11 +135,12 @@ int flux_min_blocks() {
   return mb;
 }
 
-// Gather staging (cp.async) for uniform stencils, LSKUM_FLUX_STAGE=0 disables.
+// Gather staging (cp.async) for uniform stencils: opt-in (LSKUM_FLUX_STAGE=1);
+// measured slower so far (shared-memory footprint limits residency).
 bool flux_staging() {
   static bool on = [] {
     const char* e = std::getenv("LSKUM_FLUX_STAGE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -796,7 +797,9 @@ namespace {
 std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
   auto d = std::make_unique<Domain>(ps, spec.device, spec.part_of, spec.gamma, spec.cfl,
                                     spec.det_tol, capacity);
+  trace("engine: geometry uploaded");
   d->upload(ps.fields, false);
+  trace("engine: state uploaded");
   d->begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
   return d;
 }
@@ -825,11 +828,13 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
     return rec;
   }
   auto d = open_domain(ps, spec, spec.iters);
+  trace("engine: domain open");
   if (d->failed()) {  // first q_variables
     copy_back(*d, ps);
     throw d->fault_in_run();
   }
   d->iterate(spec.iters);
+  trace("engine: iterated");
   if (d->failed()) {
     Fault f = d->fault_in_run();
     copy_back(*d, ps);
@@ -837,6 +842,7 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
     throw f;
   }
   copy_back(*d, ps);
+  trace("engine: copied back");
   rec.iterations = d->done();
   rec.residue = d->residues();
   rec.wall_ms = d->wall_ms();

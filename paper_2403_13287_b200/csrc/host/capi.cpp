@@ -181,13 +181,16 @@ void lskum_config_destroy(lskum_config* cfg) { delete cfg; }
 static int run_impl(lskum_cloud* cloud, const lskum_config* cfg, lskum_result** out, bool reinit) {
   NONNULL(cloud, cfg, out);
   return guard([&] {
+    lskb::trace("run: enter");
     if (reinit) {
       cfg->s.check();
       cloud->ps.reset_fields(cfg->s.layout);
       lskb::freestream(cloud->ps, cfg->s.mach, cfg->s.aoa, cfg->s.gamma);
     }
+    lskb::trace("run: store initialised");
     lskb::RunRecord run = lskb::solve_on_device(cloud->ps, cfg->s);
     lskb::Report rep = lskb::summarize(run, cloud->ps.n());
+    lskb::trace("run: done");
     *out = new lskum_result{std::move(run), std::move(rep), cfg->s};
   });
 }

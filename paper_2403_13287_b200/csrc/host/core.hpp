@@ -38,6 +38,9 @@ class Fault : public std::runtime_error {
 
 [[noreturn]] inline void raise(Status s, const std::string& what) { throw Fault(s, what); }
 
+// Host-phase tracing to stderr when LSKUM_TRACE is set (setup cost analysis).
+void trace(const char* what);
+
 // %f rendering, as std::to_string(double) produces in the reference messages.
 std::string fmt_f(double v);
 

@@ -8,6 +8,8 @@
 // seconds; error messages name the offending line as the reference does.
 #include <algorithm>
 #include <charconv>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +20,14 @@
 #include "par.hpp"
 
 namespace lskb {
+
+void trace(const char* what) {
+  static const bool on = std::getenv("LSKUM_TRACE") != nullptr;
+  if (!on) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, "[lskum %10.3f ms] %s\n", ms, what);
+}
 
 std::string fmt_f(double v) {
   char buf[512];

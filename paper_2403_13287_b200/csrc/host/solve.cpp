@@ -37,11 +37,14 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
 EngineSpec prepare_run(const PointSet& ps, const Settings& s) {
   s.check();
   const Screening scr = screen_stencils(ps);
+  trace("prepare: screened");
   if (scr.n_defective > 0)
     raise(Status::validation, "cloud has " + std::to_string(scr.n_defective) +
                                   " defective stencils (first at point " +
                                   std::to_string(scr.defective.front()) + ")");
-  return spec_from(ps, s, scr.det_tol);
+  EngineSpec spec = spec_from(ps, s, scr.det_tol);
+  trace("prepare: partitioned");
+  return spec;
 }
 
 RunRecord solve_on_device(PointSet& ps, const Settings& s) {
