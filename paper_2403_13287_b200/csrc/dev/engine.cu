@@ -36,28 +36,50 @@ void ck(cudaError_t e, const char* what) {
   }
 }
 
+// Device buffers come from the device's stream-ordered memory pool
+// (cudaMallocAsync), whose release threshold is raised once per device so
+// memory freed by one run is reused by the next without driver round trips.
+void ensure_pool(int device) {
+  static bool done[64] = {};
+  if (done[device & 63]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[device & 63] = true;
+}
+
 template <class T>
 class DBuf {
  public:
   DBuf() = default;
-  explicit DBuf(std::size_t count) { alloc(count); }
+  explicit DBuf(std::size_t count, cudaStream_t st = nullptr) { alloc(count, st); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p_) cudaFree(p_);
-  }
-  void alloc(std::size_t count) {
-    if (p_) cudaFree(p_);
-    p_ = nullptr;
+  ~DBuf() { release(); }
+  void alloc(std::size_t count, cudaStream_t st = nullptr) {
+    release();
+    st_ = st;
     n_ = count;
-    if (count) ck(cudaMalloc(reinterpret_cast<void**>(&p_), count * sizeof(T)), "cudaMalloc");
+    if (!count) return;
+    if (st) ck(cudaMallocAsync(reinterpret_cast<void**>(&p_), count * sizeof(T), st), "cudaMallocAsync");
+    else ck(cudaMalloc(reinterpret_cast<void**>(&p_), count * sizeof(T)), "cudaMalloc");
   }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
 
  private:
+  void release() {
+    if (!p_) return;
+    if (st_) cudaFreeAsync(p_, st_);
+    else cudaFree(p_);
+    p_ = nullptr;
+  }
   T* p_ = nullptr;
   std::size_t n_ = 0;
+  cudaStream_t st_ = nullptr;
 };
 
 template <class T>
@@ -79,6 +101,30 @@ class HBuf {  // pinned host staging
  private:
   T* p_ = nullptr;
 };
+
+// Grow-only pinned host staging, one per host thread (runs on different
+// clouds may proceed concurrently from different threads).
+class Staging {
+ public:
+  ~Staging() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void* get(std::size_t bytes) {
+    if (bytes > cap_) {
+      if (p_) cudaFreeHost(p_);
+      p_ = nullptr;
+      cap_ = 0;
+      ck(cudaHostAlloc(&p_, bytes, 0), "cudaHostAlloc(staging)");
+      cap_ = bytes;
+    }
+    return p_;
+  }
+
+ private:
+  void* p_ = nullptr;
+  std::size_t cap_ = 0;
+};
+thread_local Staging t_staging;
 
 int flux_width(int kmax) { return kmax <= 8 ? 8 : (kmax <= 16 ? 16 : 32); }
 
@@ -267,6 +313,43 @@ __global__ void k_ctl_init(Ctl* ctl, int diag_iter) {
 
 __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter; }
 
+// Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
+// major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
+__global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, const D4* res,
+                              const double* dt, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const D4 v[5] = {prim[i], q[i], dq[2 * i], dq[2 * i + 1], res[i]};
+    double r[21];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      r[4 * k] = v[k].a;
+      r[4 * k + 1] = v[k].b;
+      r[4 * k + 2] = v[k].c;
+      r[4 * k + 3] = v[k].d;
+    }
+    r[20] = dt[i];
+    if (soa) {
+#pragma unroll
+      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(k) * n + i] = r[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(i) * 21 + k] = r[k];
+    }
+  }
+}
+
+// Scatters the primitives (slots 0-3 of a FieldBlock in either layout) into D4 records.
+__global__ void k_unpack_prim(int n, int soa, const double* in, D4* prim) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (soa)
+      prim[i] = D4{in[i], in[static_cast<size_t>(n) + i], in[2 * static_cast<size_t>(n) + i],
+                   in[3 * static_cast<size_t>(n) + i]};
+    else
+      prim[i] = D4{in[4 * static_cast<size_t>(i)], in[4 * static_cast<size_t>(i) + 1],
+                   in[4 * static_cast<size_t>(i) + 2], in[4 * static_cast<size_t>(i) + 3]};
+  }
+}
+
 // Overwrites a buffer larger than L2 (126 MB) so the next step starts cold.
 __global__ void k_flush(double* buf, long long n, double v) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -299,9 +382,8 @@ class Domain {
  public:
   Domain(const PointSet& ps, int device, const std::vector<std::uint8_t>& part, double gamma,
          double cfl, double det_tol, int capacity)
-      : n_(ps.n()), device_(device) {
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "cudaStreamCreate");
+      : n_(ps.n()), device_(device), stream_holder_(device) {
+    st_ = stream_holder_.st;
     ck(cudaEventCreate(&ev0_), "cudaEventCreate");
     ck(cudaEventCreate(&ev1_), "cudaEventCreate");
     for (auto& e : kev_) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -327,51 +409,56 @@ class Domain {
     d1_ = tree_depth(n_);
 
     const std::size_t n = static_cast<std::size_t>(n_);
-    // geometry (interleaved on the host side into pinned staging)
-    HBuf<double2> hxy, hnrm;
-    hxy.alloc(n);
-    hnrm.alloc(n);
+    const std::size_t nnz = static_cast<std::size_t>(ps.nnz());
+    ensure_pool(device);
+    // geometry, packed on the host into pinned staging, then async copies
+    const std::size_t b_xy = n * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
+    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 2 * n + b_off + b_nbr + 64));
+    double2* hxy = reinterpret_cast<double2*>(hs);
+    double2* hnrm = hxy + n;
+    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hnrm + n);
+    std::uint8_t* hpart = hkind + n;
+    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * n + 15) & ~std::size_t{15}));
+    int* hnbr = hoff + n + 1;
     for (std::size_t i = 0; i < n; ++i) {
-      hxy.get()[i] = make_double2(ps.x[i], ps.y[i]);
-      hnrm.get()[i] = make_double2(ps.nx[i], ps.ny[i]);
+      hxy[i] = make_double2(ps.x[i], ps.y[i]);
+      hnrm[i] = make_double2(ps.nx[i], ps.ny[i]);
+      hkind[i] = static_cast<std::uint8_t>(ps.kind[i]);
+      hpart[i] = part.size() == n ? part[i] : 0;
+      hoff[i] = static_cast<int>(ps.off[i]);
     }
-    std::vector<int> hoff(n + 1);
-    for (std::size_t i = 0; i <= n; ++i) hoff[i] = static_cast<int>(ps.off[i]);
-    xy_.alloc(n);
-    nrm_.alloc(n);
-    kind_.alloc(n);
-    part_.alloc(n);
-    off_.alloc(n + 1);
-    nbr_.alloc(std::max<std::size_t>(1, static_cast<std::size_t>(ps.nnz())));
-    mind_.alloc(n);
-    ck(cudaMemcpyAsync(xy_.get(), hxy.get(), n * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D xy");
-    ck(cudaMemcpyAsync(nrm_.get(), hnrm.get(), n * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D nrm");
-    ck(cudaMemcpyAsync(kind_.get(), ps.kind.data(), n, cudaMemcpyHostToDevice, st_), "H2D kind");
-    if (part.size() == n)
-      ck(cudaMemcpyAsync(part_.get(), part.data(), n, cudaMemcpyHostToDevice, st_), "H2D part");
-    else
-      ck(cudaMemsetAsync(part_.get(), 0, n, st_), "memset part");
-    ck(cudaMemcpyAsync(off_.get(), hoff.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st_), "H2D off");
-    if (ps.nnz() > 0)
-      ck(cudaMemcpyAsync(nbr_.get(), ps.nbr.data(), ps.nnz() * sizeof(int), cudaMemcpyHostToDevice, st_),
-         "H2D nbr");
+    hoff[n] = static_cast<int>(ps.off[n]);
+    if (nnz) std::memcpy(hnbr, ps.nbr.data(), b_nbr);
+    xy_.alloc(n, st_);
+    nrm_.alloc(n, st_);
+    kind_.alloc(n, st_);
+    part_.alloc(n, st_);
+    off_.alloc(n + 1, st_);
+    nbr_.alloc(std::max<std::size_t>(1, nnz), st_);
+    mind_.alloc(n, st_);
+    ck(cudaMemcpyAsync(xy_.get(), hxy, b_xy, cudaMemcpyHostToDevice, st_), "H2D xy");
+    ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
+    ck(cudaMemcpyAsync(kind_.get(), hkind, n, cudaMemcpyHostToDevice, st_), "H2D kind");
+    ck(cudaMemcpyAsync(part_.get(), hpart, n, cudaMemcpyHostToDevice, st_), "H2D part");
+    ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
+    if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
     // state
-    prim_.alloc(n);
-    q_[0].alloc(n);
-    q_[1].alloc(n);
-    dq_[0].alloc(2 * n);
-    dq_[1].alloc(2 * n);
-    res_.alloc(n);
-    dt_.alloc(n);
-    mag_.alloc(n);
-    pval_.alloc(1024);
-    psz_.alloc(1024);
-    ctl_.alloc(1);
-    diag_.alloc(8);
+    prim_.alloc(n, st_);
+    q_[0].alloc(n, st_);
+    q_[1].alloc(n, st_);
+    dq_[0].alloc(2 * n, st_);
+    dq_[1].alloc(2 * n, st_);
+    res_.alloc(n, st_);
+    dt_.alloc(n, st_);
+    mag_.alloc(n, st_);
+    pval_.alloc(1024, st_);
+    psz_.alloc(1024, st_);
+    ctl_.alloc(1, st_);
+    diag_.alloc(8, st_);
     capacity_ = std::max(capacity, 1);
-    hist_.alloc(capacity_);
-    it0_.alloc(capacity_);
-    it1_.alloc(capacity_);
+    hist_.alloc(capacity_, st_);
+    it0_.alloc(capacity_, st_);
+    it1_.alloc(capacity_, st_);
     hpoll_.alloc(kPolls);
     hctl_.alloc(1);
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
@@ -382,12 +469,13 @@ class Domain {
 
   ~Domain() {
     cudaSetDevice(device_);
+    cudaStreamSynchronize(st_);  // nothing in flight before the buffers go back to the pool
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     for (auto& e : kev_) cudaEventDestroy(e);
     for (auto& e : poll_ev_) cudaEventDestroy(e);
-    cudaStreamDestroy(st_);
+    // the stream itself is released by stream_holder_ after every DBuf member
   }
 
   Geo geo() const {
@@ -407,7 +495,28 @@ class Domain {
   // ---- state transfer (FieldBlock <-> device records) ----
   void upload(const FieldBlock& f, bool full) {
     const std::size_t n = static_cast<std::size_t>(n_);
-    std::vector<D4> h(full ? 6 * n : n);
+    if (!full) {
+      // primitives only: 4 doubles per point through pinned staging (SoA: the
+      // first 4n doubles of the block; AoS: gathered 4 of every 21)
+      const bool soa = f.layout() == Layout::soa;
+      double* h = static_cast<double*>(t_staging.get(4 * n * sizeof(double)));
+      if (soa) {
+        std::memcpy(h, f.raw(), 4 * n * sizeof(double));
+      } else {
+        const double* src = f.raw();
+        for (std::size_t i = 0; i < n; ++i) std::memcpy(h + 4 * i, src + 21 * i, 4 * sizeof(double));
+      }
+      DBuf<double> tmp(4 * n, st_);
+      ck(cudaMemcpyAsync(tmp.get(), h, 4 * n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D prim");
+      k_unpack_prim<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(n_, soa ? 1 : 0, tmp.get(),
+                                                                            prim_.get());
+      ck(cudaGetLastError(), "k_unpack_prim");
+      ck(cudaStreamSynchronize(st_), "upload");
+      a_ = 0;
+      b_ = 0;
+      return;
+    }
+    std::vector<D4> h(6 * n);
     D4* hp = h.data();
     for (std::size_t i = 0; i < n; ++i) {
       const int p = static_cast<int>(i);
@@ -444,6 +553,18 @@ class Domain {
 
   void download(FieldBlock& f, bool with_q, const D4* qsrc, const D4* dqsrc) {
     const std::size_t n = static_cast<std::size_t>(n_);
+    if (with_q) {
+      // pack on the device in the host layout, one D2H into the FieldBlock
+      DBuf<double> packed(21 * n, st_);
+      k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
+          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(),
+          packed.get());
+      ck(cudaGetLastError(), "k_pack_fields");
+      ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
+         "D2H fields");
+      ck(cudaStreamSynchronize(st_), "download");
+      return;
+    }
     std::vector<D4> h(6 * n);
     D4* hp = h.data();
     ck(cudaMemcpyAsync(hp, prim_.get(), n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H prim");
@@ -765,7 +886,23 @@ class Domain {
 
  private:
   static constexpr int kPolls = 4;
+  // Owns the stream; declared before the buffers so it is destroyed after them
+  // (their stream-ordered frees are enqueued on it).
+  struct StreamHolder {
+    cudaStream_t st = nullptr;
+    explicit StreamHolder(int device) {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    ~StreamHolder() {
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
+    }
+  };
   int n_ = 0, device_ = 0;
+  StreamHolder stream_holder_;
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, poll_ev_[kPolls] = {}, kev_[4] = {};
   DBuf<double> flush_;

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -88,6 +89,8 @@ class FieldBlock {
 bool fields_identical(const FieldBlock& a, const FieldBlock& b);
 
 // Columnar point set + CSR stencils (reference cloud.hpp:37-74).
+struct Screening;
+
 struct PointSet {
   std::vector<double> x, y, nx, ny;
   std::vector<Kind> kind;
@@ -100,9 +103,12 @@ struct PointSet {
   std::int32_t degree(std::int32_t i) const {
     return static_cast<std::int32_t>(off[i + 1] - off[i]);
   }
+  // Screening report of this (immutable) geometry, computed on first use.
+  mutable std::shared_ptr<const Screening> screening;
+
   bool has_wall() const;
   int max_degree() const;
-  void reset_fields(Layout layout) { fields = FieldBlock(layout, n()); }
+  void reset_fields(Layout layout);
 };
 
 // One row of input, as produced by the readers and generators.

@@ -70,6 +70,14 @@ bool fields_identical(const FieldBlock& a, const FieldBlock& b) {
   return true;
 }
 
+void PointSet::reset_fields(Layout layout) {
+  if (fields.size() == n() && fields.layout() == layout) {
+    std::fill(fields.raw(), fields.raw() + static_cast<std::size_t>(n()) * slot::count, 0.0);
+  } else {
+    fields = FieldBlock(layout, n());
+  }
+}
+
 bool PointSet::has_wall() const {
   return std::find(kind.begin(), kind.end(), Kind::wall) != kind.end();
 }

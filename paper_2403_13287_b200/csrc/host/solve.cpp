@@ -22,8 +22,12 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
   spec.fp_mode = s.fp_mode;
   spec.chunk = s.chunk;
   spec.device = s.device;
+  if (s.parts > ps.n())
+    raise(Status::argument, "more partitions than points (" + std::to_string(s.parts) + " > " +
+                                std::to_string(ps.n()) + ")");
+  if (s.parts <= 1) return spec;  // one piece: every point is in partition 0
   const std::vector<Piece> pieces = bisect_cloud(ps, s.parts);
-  if (pieces.size() > 1) {
+  {
     spec.part_of.assign(static_cast<std::size_t>(ps.n()), 0);
     for (std::size_t p = 0; p < pieces.size(); ++p)
       for (std::int32_t i : pieces[p].owned)
@@ -36,7 +40,8 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
 
 EngineSpec prepare_run(const PointSet& ps, const Settings& s) {
   s.check();
-  const Screening scr = screen_stencils(ps);
+  if (!ps.screening) ps.screening = std::make_shared<const Screening>(screen_stencils(ps));
+  const Screening& scr = *ps.screening;
   trace("prepare: screened");
   if (scr.n_defective > 0)
     raise(Status::validation, "cloud has " + std::to_string(scr.n_defective) +
