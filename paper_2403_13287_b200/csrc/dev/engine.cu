@@ -225,9 +225,8 @@ int tree_depth(long long n) {
 // ---- diagnostics: re-evaluates the failing item named by the error key ----
 template <bool S>
 __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, const double* uval,
-                           const double* uwhich, Gas gas, unsigned long long key, double* out) {
+                           const double* uwhich, Gas gas, unsigned long long key, int i, double* out) {
   const unsigned phase = static_cast<unsigned>(key >> 61);
-  const int i = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
   const unsigned dir = static_cast<unsigned>((key >> 20) & 3ull);
   const unsigned j = static_cast<unsigned>(key & 0xFFFFFull);
   for (int t = 0; t < 6; ++t) out[t] = 0.0;
@@ -273,7 +272,7 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
     ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
     tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
   }
-  out[3] = nb;
+  out[3] = gidx(g, nb);
   if (!(ti[3] < 0.0)) {
     out[0] = 0.0;
     out[1] = ti[3];
@@ -297,11 +296,16 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
   out[2] = p;
 }
 
-__global__ void k_ctl_init(Ctl* ctl, int diag_iter) {
-  ctl->err_key = kNoErr;
-  ctl->err_iter = -1;
-  ctl->iter = 0;
-  ctl->diag_iter = diag_iter;
+// Resets this domain's timers, points it at the run's shared word and (for
+// the domain that owns it) resets that word.
+__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter) {
+  ctl->sh = sh;
+  if (own_shared) {
+    sh->err_key = kNoErr;
+    sh->err_iter = 0x7FFFFFFF;
+    sh->iter = 0;
+    sh->diag_iter = diag_iter;
+  }
   for (int k = 0; k < KT_COUNT; ++k) {
     ctl->kt[k].t0 = ~0ull;
     ctl->kt[k].t1 = 0;
@@ -311,7 +315,7 @@ __global__ void k_ctl_init(Ctl* ctl, int diag_iter) {
   }
 }
 
-__global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter; }
+__global__ void k_set_diag(Shared* sh, int diag_iter) { sh->diag_iter = diag_iter; }
 
 // Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
 // major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
@@ -377,18 +381,46 @@ std::string itos(long long v) { return std::to_string(v); }
 }  // namespace
 
 // ===========================================================================
-// Domain: one device's copy of the cloud and the solver state.
+// Domain: one device's share of the cloud and its solver state.  A domain owns
+// points [0, n_own) in local numbering and keeps read-only halo copies of the
+// points its stencils reach in [n_own, n_loc); with one domain n_own = n_loc = n
+// and local ids are global ids.
+struct GeomView {
+  int n_own = 0, n_loc = 0;
+  const double *x = nullptr, *y = nullptr, *nx = nullptr, *ny = nullptr;  // n_loc
+  const Kind* kind = nullptr;                                             // n_loc
+  const std::int64_t* off = nullptr;                                      // n_own + 1
+  const std::int32_t* nbr = nullptr;                                      // local ids
+  const std::uint8_t* part = nullptr;                                     // n_loc or null
+  const std::int32_t* gid = nullptr;                                      // n_loc or null
+  std::int64_t nnz = 0;
+};
+
+GeomView view_of(const PointSet& ps, const std::vector<std::uint8_t>& part) {
+  GeomView v;
+  v.n_own = v.n_loc = ps.n();
+  v.x = ps.x.data();
+  v.y = ps.y.data();
+  v.nx = ps.nx.data();
+  v.ny = ps.ny.data();
+  v.kind = ps.kind.data();
+  v.off = ps.off.data();
+  v.nbr = ps.nbr.data();
+  v.part = part.size() == static_cast<std::size_t>(ps.n()) ? part.data() : nullptr;
+  v.nnz = ps.nnz();
+  return v;
+}
+
 class Domain {
  public:
-  Domain(const PointSet& ps, int device, const std::vector<std::uint8_t>& part, double gamma,
-         double cfl, double det_tol, int capacity)
-      : n_(ps.n()), device_(device), stream_holder_(device) {
+  Domain(const GeomView& gv, int device, double gamma, double cfl, double det_tol, int capacity)
+      : n_(gv.n_own), n_loc_(gv.n_loc), device_(device), stream_holder_(device) {
     st_ = stream_holder_.st;
     ck(cudaEventCreate(&ev0_), "cudaEventCreate");
     ck(cudaEventCreate(&ev1_), "cudaEventCreate");
     for (auto& e : kev_) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : poll_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-    if (ps.nnz() >= (1ll << 31)) raise(Status::argument, "stencil table exceeds 2^31 entries");
+    if (gv.nnz >= (1ll << 31)) raise(Status::argument, "stencil table exceeds 2^31 entries");
     gas_.gamma = gamma;
     gas_.gm1 = gamma - 1.0;
     gas_.inv_gm1 = 1.0 / (gamma - 1.0);
@@ -399,61 +431,77 @@ class Domain {
       const double mr = std::nearbyint(m);
       gas_.half_pow = (std::fabs(m - mr) < 1e-9 && mr >= 1.0 && mr <= 40.0) ? static_cast<int>(mr) : -1;
     }
-    kmax_ = std::max(1, ps.max_degree());
+    std::int64_t km = 1;
+    for (int i = 0; i < n_; ++i) km = std::max(km, gv.off[i + 1] - gv.off[i]);
+    kmax_ = static_cast<int>(km);
     kfix_ = kmax_;
-    for (std::int32_t i = 0; i < ps.n() && kfix_ > 0; ++i)
-      if (ps.off[i + 1] - ps.off[i] != kmax_ || ps.off[i] != static_cast<std::int64_t>(i) * kmax_) kfix_ = 0;
+    for (int i = 0; i < n_ && kfix_ > 0; ++i)
+      if (gv.off[i + 1] - gv.off[i] != kmax_ || gv.off[i] != static_cast<std::int64_t>(i) * kmax_) kfix_ = 0;
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
     stride_ = flux_stride(kmax_);
     d1_ = tree_depth(n_);
+    n_res_ = n_;
 
-    const std::size_t n = static_cast<std::size_t>(n_);
-    const std::size_t nnz = static_cast<std::size_t>(ps.nnz());
+    const std::size_t n = static_cast<std::size_t>(n_), nl = static_cast<std::size_t>(n_loc_);
+    const std::size_t nnz = static_cast<std::size_t>(gv.nnz);
     ensure_pool(device);
     // geometry, packed on the host into pinned staging, then async copies
-    const std::size_t b_xy = n * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
-    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 2 * n + b_off + b_nbr + 64));
+    const std::size_t b_xy = nl * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
+    const std::size_t b_gid = gv.gid ? nl * sizeof(int) : 0;
+    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 2 * nl + b_off + b_nbr + b_gid + 64));
     double2* hxy = reinterpret_cast<double2*>(hs);
-    double2* hnrm = hxy + n;
-    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hnrm + n);
-    std::uint8_t* hpart = hkind + n;
-    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * n + 15) & ~std::size_t{15}));
+    double2* hnrm = hxy + nl;
+    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hnrm + nl);
+    std::uint8_t* hpart = hkind + nl;
+    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * nl + 15) & ~std::size_t{15}));
     int* hnbr = hoff + n + 1;
-    for (std::size_t i = 0; i < n; ++i) {
-      hxy[i] = make_double2(ps.x[i], ps.y[i]);
-      hnrm[i] = make_double2(ps.nx[i], ps.ny[i]);
-      hkind[i] = static_cast<std::uint8_t>(ps.kind[i]);
-      hpart[i] = part.size() == n ? part[i] : 0;
-      hoff[i] = static_cast<int>(ps.off[i]);
+    int* hgid = hnbr + nnz;
+    for (std::size_t i = 0; i < nl; ++i) {
+      hxy[i] = make_double2(gv.x[i], gv.y[i]);
+      hnrm[i] = make_double2(gv.nx[i], gv.ny[i]);
+      hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
+      hpart[i] = gv.part ? gv.part[i] : 0;
     }
-    hoff[n] = static_cast<int>(ps.off[n]);
-    if (nnz) std::memcpy(hnbr, ps.nbr.data(), b_nbr);
-    xy_.alloc(n, st_);
-    nrm_.alloc(n, st_);
-    kind_.alloc(n, st_);
-    part_.alloc(n, st_);
+    for (std::size_t i = 0; i <= n; ++i) hoff[i] = static_cast<int>(gv.off[i]);
+    if (nnz) std::memcpy(hnbr, gv.nbr, b_nbr);
+    if (gv.gid) {
+      std::memcpy(hgid, gv.gid, b_gid);
+      gid_host_.assign(gv.gid, gv.gid + nl);
+    }
+    xy_.alloc(nl, st_);
+    nrm_.alloc(nl, st_);
+    kind_.alloc(nl, st_);
+    part_.alloc(nl, st_);
     off_.alloc(n + 1, st_);
     nbr_.alloc(std::max<std::size_t>(1, nnz), st_);
     mind_.alloc(n, st_);
     ck(cudaMemcpyAsync(xy_.get(), hxy, b_xy, cudaMemcpyHostToDevice, st_), "H2D xy");
     ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
-    ck(cudaMemcpyAsync(kind_.get(), hkind, n, cudaMemcpyHostToDevice, st_), "H2D kind");
-    ck(cudaMemcpyAsync(part_.get(), hpart, n, cudaMemcpyHostToDevice, st_), "H2D part");
+    ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
+    ck(cudaMemcpyAsync(part_.get(), hpart, nl, cudaMemcpyHostToDevice, st_), "H2D part");
     ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
     if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
-    // state
-    prim_.alloc(n, st_);
-    q_[0].alloc(n, st_);
-    q_[1].alloc(n, st_);
-    dq_[0].alloc(2 * n, st_);
-    dq_[1].alloc(2 * n, st_);
+    if (gv.gid) {
+      gid_.alloc(nl, st_);
+      ck(cudaMemcpyAsync(gid_.get(), hgid, b_gid, cudaMemcpyHostToDevice, st_), "H2D gid");
+    }
+    // state: q / dq carry halo slots; prim covers them for the first q_variables
+    prim_.alloc(nl, st_);
+    q_[0].alloc(nl, st_);
+    q_[1].alloc(nl, st_);
+    dq_[0].alloc(2 * nl, st_);
+    dq_[1].alloc(2 * nl, st_);
     res_.alloc(n, st_);
     dt_.alloc(n, st_);
+    which_.alloc(n, st_);
     mag_.alloc(n, st_);
+    mag_out_ = mag_.get();
     pval_.alloc(1024, st_);
     psz_.alloc(1024, st_);
     ctl_.alloc(1, st_);
+    sh_.alloc(1, st_);
+    shared_ = sh_.get();
     diag_.alloc(8, st_);
     capacity_ = std::max(capacity, 1);
     hist_.alloc(capacity_, st_);
@@ -461,9 +509,10 @@ class Domain {
     it1_.alloc(capacity_, st_);
     hpoll_.alloc(kPolls);
     hctl_.alloc(1);
+    hsh_.alloc(1);
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
     ck(cudaGetLastError(), "k_min_dist");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), -1);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1);
     ck(cudaStreamSynchronize(st_), "geometry upload");
   }
 
@@ -487,15 +536,36 @@ class Domain {
     g.off = off_.get();
     g.nbr = nbr_.get();
     g.mind = mind_.get();
+    g.gid = gid_.get();
     g.n = n_;
     g.kfix = kfix_;
     return g;
   }
 
+  // ---- multi-domain wiring ----
+  // Use another domain's shared control word (error word, iteration counter).
+  void use_shared(Shared* sh) { shared_ = sh; }
+  Shared* shared() const { return shared_; }
+  // Residue summands are written (by global id) into `mag` (the root's array).
+  void use_mag(double* mag) { mag_out_ = mag; }
+  // Root only: residue tree over n_total global ids.
+  void set_residue_size(long long n_total) {
+    n_res_ = n_total;
+    d1_ = tree_depth(n_total);
+    if (n_total != n_) {
+      mag_.alloc(static_cast<std::size_t>(n_total), st_);
+      mag_out_ = mag_.get();
+    }
+  }
+  double* mag_buf() { return mag_.get(); }
+  int n_loc() const { return n_loc_; }
+  int device() const { return device_; }
+  int global_of(int local) const { return gid_host_.empty() ? local : gid_host_[local]; }
+
   // ---- state transfer (FieldBlock <-> device records) ----
   void upload(const FieldBlock& f, bool full) {
     const std::size_t n = static_cast<std::size_t>(n_);
-    if (!full) {
+    if (!full && gid_host_.empty()) {
       // primitives only: 4 doubles per point through pinned staging (SoA: the
       // first 4n doubles of the block; AoS: gathered 4 of every 21)
       const bool soa = f.layout() == Layout::soa;
@@ -512,53 +582,48 @@ class Domain {
                                                                             prim_.get());
       ck(cudaGetLastError(), "k_unpack_prim");
       ck(cudaStreamSynchronize(st_), "upload");
-      a_ = 0;
-      b_ = 0;
+      return;
+    }
+    if (!full) {
+      // owned + halo primitives gathered by global id
+      const std::size_t nl = static_cast<std::size_t>(n_loc_);
+      D4* h = static_cast<D4*>(t_staging.get(nl * sizeof(D4)));
+      for (std::size_t i = 0; i < nl; ++i) {
+        const int p = gid_host_[i];
+        h[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2), f.at(p, slot::prim + 3)};
+      }
+      ck(cudaMemcpyAsync(prim_.get(), h, nl * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D prim");
+      ck(cudaStreamSynchronize(st_), "upload");
       return;
     }
     std::vector<D4> h(6 * n);
     D4* hp = h.data();
     for (std::size_t i = 0; i < n; ++i) {
       const int p = static_cast<int>(i);
-      hp[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2),
-                 f.at(p, slot::prim + 3)};
-      if (full) {
-        hp[n + i] = D4{f.at(p, slot::q), f.at(p, slot::q + 1), f.at(p, slot::q + 2), f.at(p, slot::q + 3)};
-        hp[2 * n + 2 * i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qx + 2),
-                               f.at(p, slot::qx + 3)};
-        hp[2 * n + 2 * i + 1] = D4{f.at(p, slot::qy), f.at(p, slot::qy + 1), f.at(p, slot::qy + 2),
-                                   f.at(p, slot::qy + 3)};
-        hp[4 * n + i] = D4{f.at(p, slot::res), f.at(p, slot::res + 1), f.at(p, slot::res + 2),
-                           f.at(p, slot::res + 3)};
-        reinterpret_cast<double*>(hp + 5 * n)[i] = f.at(p, slot::dt);
-      }
+      hp[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2), f.at(p, slot::prim + 3)};
+      hp[n + i] = D4{f.at(p, slot::q), f.at(p, slot::q + 1), f.at(p, slot::q + 2), f.at(p, slot::q + 3)};
+      hp[2 * n + 2 * i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qx + 2), f.at(p, slot::qx + 3)};
+      hp[2 * n + 2 * i + 1] =
+          D4{f.at(p, slot::qy), f.at(p, slot::qy + 1), f.at(p, slot::qy + 2), f.at(p, slot::qy + 3)};
+      hp[4 * n + i] =
+          D4{f.at(p, slot::res), f.at(p, slot::res + 1), f.at(p, slot::res + 2), f.at(p, slot::res + 3)};
+      reinterpret_cast<double*>(hp + 5 * n)[i] = f.at(p, slot::dt);
     }
     ck(cudaMemcpyAsync(prim_.get(), hp, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D prim");
-    if (full) {
-      ck(cudaMemcpyAsync(q_[0].get(), hp + n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D q");
-      ck(cudaMemcpyAsync(dq_[0].get(), hp + 2 * n, 2 * n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D dq");
-      ck(cudaMemcpyAsync(res_.get(), hp + 4 * n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D res");
-      ck(cudaMemcpyAsync(dt_.get(), hp + 5 * n, n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D dt");
-    }
+    ck(cudaMemcpyAsync(q_[0].get(), hp + n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D q");
+    ck(cudaMemcpyAsync(dq_[0].get(), hp + 2 * n, 2 * n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D dq");
+    ck(cudaMemcpyAsync(res_.get(), hp + 4 * n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D res");
+    ck(cudaMemcpyAsync(dt_.get(), hp + 5 * n, n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D dt");
     ck(cudaStreamSynchronize(st_), "upload");
-    a_ = 0;
-    b_ = 0;
   }
-
-  // Which buffers hold each slot group for copy-back.
-  struct Sources {
-    const D4* q;
-    const D4* dq;
-  };
 
   void download(FieldBlock& f, bool with_q, const D4* qsrc, const D4* dqsrc) {
     const std::size_t n = static_cast<std::size_t>(n_);
-    if (with_q) {
+    if (with_q && gid_host_.empty()) {
       // pack on the device in the host layout, one D2H into the FieldBlock
       DBuf<double> packed(21 * n, st_);
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
-          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(),
-          packed.get());
+          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
       ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
          "D2H fields");
@@ -575,7 +640,7 @@ class Domain {
     ck(cudaStreamSynchronize(st_), "download");
     const double* dtp = reinterpret_cast<const double*>(hp + 5 * n);
     for (std::size_t i = 0; i < n; ++i) {
-      const int p = static_cast<int>(i);
+      const int p = global_of(static_cast<int>(i));
       const D4& s = hp[i];
       f.at(p, slot::prim) = s.a;
       f.at(p, slot::prim + 1) = s.b;
@@ -601,32 +666,41 @@ class Domain {
   }
 
   // ---- solver mode ----
-  void begin_run(int order, int inner, int fp_mode, int chunk) {
+  // Zeroes the once-per-run fields (runtime.cpp:216-224) and the control
+  // block; with `own_shared` this domain also resets the run's shared word.
+  void reset_run(int order, int inner, int fp_mode, int chunk, bool own_shared) {
     order_ = order;
     inner_ = inner;
     strict_ = fp_mode == 1;
     chunk_ = std::max(1, chunk);
-    const std::size_t n = static_cast<std::size_t>(n_);
-    // runtime.cpp:216-224 zeroes qx, qy, flux_res, delta_t once per run
-    ck(cudaMemsetAsync(dq_[0].get(), 0, 2 * n * sizeof(D4), st_), "zero dq");
-    ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * n * sizeof(D4), st_), "zero dq");
+    const std::size_t n = static_cast<std::size_t>(n_), nl = static_cast<std::size_t>(n_loc_);
+    ck(cudaMemsetAsync(dq_[0].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
+    ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(res_.get(), 0, n * sizeof(D4), st_), "zero res");
     ck(cudaMemsetAsync(dt_.get(), 0, n * sizeof(double), st_), "zero dt");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), -1);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1);
     a_ = 0;
     b_ = 0;
     done_ = 0;
     total_ms_ = 0.0;
-    // the first iteration's q_variables; later ones are fused into k_flux
-    k_qvar<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), prim_.get(), q_[0].get(), gas_, ctl_.get());
+  }
+  // The first iteration's q_variables over owned and halo points; later q
+  // comes out of k_update.
+  void first_q() {
+    Geo g = geo();
+    g.n = n_loc_;
+    k_qvar<<<(n_loc_ + 255) / 256, 256, 0, st_>>>(g, prim_.get(), q_[0].get(), gas_, ctl_.get());
     ck(cudaGetLastError(), "k_qvar");
+  }
+  void begin_run(int order, int inner, int fp_mode, int chunk) {
+    reset_run(order, inner, fp_mode, chunk, true);
+    first_q();
     ck(cudaStreamSynchronize(st_), "begin_run");
     refresh_ctl();
   }
 
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
 
-  // Enqueue one iteration starting at parity (a, b); returns the new parity.
   // Event record that also fires when captured into a graph (an external
   // event-record node); a plain captured cudaEventRecord only orders work.
   void record_ext(cudaEvent_t e) {
@@ -638,50 +712,70 @@ class Domain {
       ck(cudaEventRecord(e, st_), "EventRecord");
   }
 
-  // `timed`: bracket the first sweep and the flux kernel with CUDA events
-  // (event-record nodes inside the graph; read back by last_event_ms()).
-  void enqueue_iteration(int& a, int& b, bool timed) {
-    const Geo g = geo();
-    if (order_ == 2) {
-      for (int s = 0; s < inner_; ++s) {
-        if (timed && s == 0) record_ext(kev_[0]);
-        k_sweep<<<sweep_grid(n_), 256, 0, st_>>>(g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(),
-                                                   gas_, ctl_.get(), s == 0 ? it0_.get() : nullptr);
-        if (timed && s == 0) record_ext(kev_[1]);
-        b ^= 1;
-      }
-    }
+  // ---- building blocks of one iteration (also used by the multi-domain driver) ----
+  void launch_sweep(int a, int b, bool first) {
+    k_sweep<<<sweep_grid(n_), 256, 0, st_>>>(geo(), q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_,
+                                             ctl_.get(), first ? it0_.get() : nullptr);
+  }
+  void launch_flux(int a, int b, bool stamp) {
     FluxArgs fa;
-    fa.g = g;
+    fa.g = geo();
     fa.gas = gas_;
     fa.q = q_[a].get();
     fa.dq = dq_[b].get();
     fa.res = res_.get();
     fa.ctl = ctl_.get();
-    fa.iter_t0 = order_ == 2 ? nullptr : it0_.get();
+    fa.iter_t0 = stamp ? it0_.get() : nullptr;
     fa.kcap = kmax_;
     fa.stride = stride_;
     fa.mask = 0xF;
     fa.first = 1;
-    if (timed) record_ext(kev_[2]);
     flux_launch(W_, strict_, fa, smem_, st_);
-    if (timed) record_ext(kev_[3]);
+  }
+  void launch_update(int a) {
     UpdateArgs ua;
-    ua.g = g;
+    ua.g = geo();
     ua.gas = gas_;
     ua.q = q_[a].get();
     ua.res = res_.get();
     ua.prim = prim_.get();
     ua.q_next = q_[a ^ 1].get();
     ua.dt = dt_.get();
-    ua.mag = mag_.get();
+    ua.mag = mag_out_;
+    ua.which = which_.get();
     ua.ctl = ctl_.get();
     k_update<<<(n_ + 255) / 256, 256, 0, st_>>>(ua);
-    a ^= 1;
-    k_tree_partial<<<1 << d1_, kTreeThreads, 0, st_>>>(mag_.get(), n_, d1_, pval_.get(), psz_.get(),
+  }
+  void launch_residue() {
+    k_tree_partial<<<1 << d1_, kTreeThreads, 0, st_>>>(mag_.get(), n_res_, d1_, pval_.get(), psz_.get(),
                                                       ctl_.get());
-    k_tree_final<<<1, 1024, 0, st_>>>(pval_.get(), psz_.get(), d1_, n_, hist_.get(), it1_.get(),
-                                      ctl_.get());
+    k_tree_final<<<1, 1024, 0, st_>>>(pval_.get(), psz_.get(), d1_, n_res_, hist_.get(), it1_.get(), ctl_.get());
+  }
+  // Halo gather of `recs` records per point from the owners' buffers.
+  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src) {
+    const int nh = n_loc_ - n_;
+    if (nh <= 0) return;
+    k_halo<<<std::min((nh * recs + 255) / 256, 4096), 256, 0, st_>>>(dst, recs, n_, nh, hdom, hidx, src,
+                                                                       shared_);
+  }
+
+  // One iteration starting at parity (a, b); `timed` brackets the first sweep
+  // and the flux kernel with CUDA events (read back by last_event_ms()).
+  void enqueue_iteration(int& a, int& b, bool timed) {
+    if (order_ == 2) {
+      for (int s = 0; s < inner_; ++s) {
+        if (timed && s == 0) record_ext(kev_[0]);
+        launch_sweep(a, b, s == 0);
+        if (timed && s == 0) record_ext(kev_[1]);
+        b ^= 1;
+      }
+    }
+    if (timed) record_ext(kev_[2]);
+    launch_flux(a, b, order_ != 2);
+    if (timed) record_ext(kev_[3]);
+    launch_update(a);
+    a ^= 1;
+    launch_residue();
   }
 
   cudaGraphExec_t graph_for(int a, int b, int c) {
@@ -706,12 +800,14 @@ class Domain {
     if (order_ == 2 && ((c * inner_) & 1)) b ^= 1;
   }
 
+  void set_diag(int it) { k_set_diag<<<1, 1, 0, st_>>>(shared_, it); }
+
   // Runs up to n iterations; stops early on a device error.  Returns the
   // CUDA-event milliseconds around the enqueued work.
   double iterate(int n) {
     if (done_ + n > capacity_) raise(Status::argument, "session capacity exceeded");
     ck(cudaSetDevice(device_), "cudaSetDevice");
-    k_set_diag<<<1, 1, 0, st_>>>(ctl_.get(), done_ + n - 1);
+    set_diag(done_ + n - 1);
     // capture graphs before timing
     {
       int a = a_, b = b_, left = n;
@@ -731,18 +827,7 @@ class Domain {
       advance(a_, b_, c);
       left -= c;
       if (left == 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");
-      const int s = issued % kPolls;
-      ck(cudaMemcpyAsync(hpoll_.get() + s, &ctl_.get()->err_key, sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, st_),
-         "poll copy");
-      ck(cudaEventRecord(poll_ev_[s], st_), "poll event");
-      ++issued;
-      if (issued - waited >= kPolls - 1) {
-        const int w = waited % kPolls;
-        ck(cudaEventSynchronize(poll_ev_[w]), "poll sync");
-        failed = hpoll_.get()[w] != kNoErr;
-        ++waited;
-      }
+      failed = poll(issued, waited);
     }
     if (left > 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");  // stopped early
     ck(cudaStreamSynchronize(st_), "iterate");
@@ -750,16 +835,36 @@ class Domain {
     ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "EventElapsed");
     total_ms_ += ms;
     refresh_ctl();
-    done_ = hctl_.get()->iter;
+    done_ = hsh_.get()->iter;
     return ms;
+  }
+
+  // Enqueues an async copy of the error word; waits on the oldest copy once
+  // kPolls-1 are in flight.  True once an error has been observed.
+  bool poll(int& issued, int& waited) {
+    const int s = issued % kPolls;
+    ck(cudaMemcpyAsync(hpoll_.get() + s, &shared_->err_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st_),
+       "poll copy");
+    ck(cudaEventRecord(poll_ev_[s], st_), "poll event");
+    ++issued;
+    if (issued - waited >= kPolls - 1) {
+      const int w = waited % kPolls;
+      ck(cudaEventSynchronize(poll_ev_[w]), "poll sync");
+      ++waited;
+      return hpoll_.get()[w] != kNoErr;
+    }
+    return false;
   }
 
   void refresh_ctl() {
     ck(cudaMemcpyAsync(hctl_.get(), ctl_.get(), sizeof(Ctl), cudaMemcpyDeviceToHost, st_), "D2H ctl");
+    ck(cudaMemcpyAsync(hsh_.get(), shared_, sizeof(Shared), cudaMemcpyDefault, st_), "D2H shared");
     ck(cudaStreamSynchronize(st_), "ctl");
   }
 
-  bool failed() const { return hctl_.get()->err_key != kNoErr; }
+  bool failed() const { return hsh_.get()->err_key != kNoErr; }
+  const Shared& shared_host() const { return *hsh_.get(); }
 
   // CUDA-event times of the first sweep and the flux kernel of the last
   // iteration of the last graph replay (valid after iterate()).
@@ -776,33 +881,32 @@ class Domain {
     k_flush<<<148 * 8, 256, 0, st_>>>(flush_.get(), static_cast<long long>(flush_.size()), 1.0);
     ck(cudaStreamSynchronize(st_), "flush");
   }
-  const Ctl& ctl() const { return *hctl_.get(); }
 
-  // Builds the reference-format message for the recorded failure.
   // q / published dq read by 0-based iteration t (parities start at 0 per run).
   const D4* q_of_iter(int t) const { return q_[t & 1].get(); }
-  const D4* dq_of_flux(int t) const {
-    return order_ == 2 ? dq_[((t + 1) * inner_) & 1].get() : dq_[0].get();
+  const D4* dq_of_flux(int t) const { return order_ == 2 ? dq_[((t + 1) * inner_) & 1].get() : dq_[0].get(); }
+  Fault fault_in_run(int local) {
+    const int t = std::max(0, std::min(hsh_.get()->err_iter, std::max(0, capacity_ - 1)));
+    return fault(true, q_of_iter(t), dq_of_flux(t), local);
   }
-  Fault fault_in_run() {
-    const int t = std::max(0, hctl_.get()->err_iter);
-    return fault(true, q_of_iter(t), dq_of_flux(t));
-  }
+  Fault fault_in_run() { return fault_in_run(-1); }
 
-  Fault fault(bool with_iteration, const D4* qsrc, const D4* dqsrc) {
-    const unsigned long long key = hctl_.get()->err_key;
+  // Builds the reference-format message for the recorded failure; `local` is
+  // the failing point's local index (-1: the key's global id is local).
+  Fault fault(bool with_iteration, const D4* qsrc, const D4* dqsrc, int local = -1) {
+    const unsigned long long key = hsh_.get()->err_key;
     const unsigned phase = static_cast<unsigned>(key >> 61);
     const long long point = static_cast<long long>((key >> 22) & 0x7FFFFFFFull);
-    const int iter = hctl_.get()->err_iter + 1;
+    const int iter = hsh_.get()->err_iter + 1;
     if (phase == PH_RESIDUE)
-      return Fault(Status::positivity,
-                   "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
+      return Fault(Status::positivity, "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
+    const int li = local >= 0 ? local : static_cast<int>(point);
     if (strict_)
-      k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), mag_.get(), gas_,
-                                         key, diag_.get());
+      k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), which_.get(), gas_, key, li,
+                                         diag_.get());
     else
-      k_diagnose<false><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), mag_.get(), gas_,
-                                          key, diag_.get());
+      k_diagnose<false><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), which_.get(), gas_, key, li,
+                                          diag_.get());
     double d[6];
     ck(cudaMemcpyAsync(d, diag_.get(), sizeof d, cudaMemcpyDeviceToHost, st_), "D2H diag");
     ck(cudaStreamSynchronize(st_), "diagnose");
@@ -812,16 +916,16 @@ class Domain {
       msg = "invalid primitive state: rho=" + fmt_f(d[1]) + " p=" + fmt_f(d[2]);
     } else if (phase == PH_SWEEP) {
       code = Status::singular;
-      msg = "full stencil of point " + itos(point) + ": singular least-squares stencil (det=" +
-            fmt_f(d[1]) + ", n=" + itos(static_cast<long long>(d[2])) + ")";
+      msg = "full stencil of point " + itos(point) + ": singular least-squares stencil (det=" + fmt_f(d[1]) +
+            ", n=" + itos(static_cast<long long>(d[2])) + ")";
     } else if (phase == PH_FLUX) {
       if (d[0] == 2.0) {
         code = Status::singular;
-        msg = "split stencil of point " + itos(point) + ": singular least-squares stencil (det=" +
-              fmt_f(d[1]) + ", n=" + itos(static_cast<long long>(d[2])) + ")";
+        msg = "split stencil of point " + itos(point) + ": singular least-squares stencil (det=" + fmt_f(d[1]) +
+              ", n=" + itos(static_cast<long long>(d[2])) + ")";
       } else if (d[0] == 0.0) {
-        msg = "flux reconstruction failed on edge (" + itos(point) + ", " +
-              itos(static_cast<long long>(d[3])) + "): q-state with q3 >= 0 (q3=" + fmt_f(d[1]) + ")";
+        msg = "flux reconstruction failed on edge (" + itos(point) + ", " + itos(static_cast<long long>(d[3])) +
+              "): q-state with q3 >= 0 (q3=" + fmt_f(d[1]) + ")";
       } else {
         msg = "invalid primitive state: rho=" + fmt_f(d[1]) + " p=" + fmt_f(d[2]);
       }
@@ -836,25 +940,28 @@ class Domain {
   // ---- accessors for the run/session drivers ----
   int n() const { return n_; }
   int done() const { return done_; }
+  void set_done(int d) { done_ = d; }
   double total_ms() const { return total_ms_; }
+  void add_ms(double ms) { total_ms_ += ms; }
   cudaStream_t stream() const { return st_; }
   const D4* q_read_last() const { return q_of_iter(std::max(0, done_ - 1)); }
   const D4* q_buf(int k) const { return q_[k].get(); }
   D4* q_buf(int k) { return q_[k].get(); }
   D4* dq_buf(int k) { return dq_[k].get(); }
   const D4* dq_cur() const { return done_ > 0 ? dq_of_flux(done_ - 1) : dq_[0].get(); }
-  int parity_a() const { return a_; }
   D4* prim() { return prim_.get(); }
   D4* res() { return res_.get(); }
   double* dt() { return dt_.get(); }
   double* mind() { return mind_.get(); }
-  double* mag() { return mag_.get(); }
+  double* which() { return which_.get(); }
   Ctl* dctl() { return ctl_.get(); }
   const Gas& gas() const { return gas_; }
   int width() const { return W_; }
   int kmax() const { return kmax_; }
   std::size_t smem() const { return smem_; }
   void set_strict(bool s) { strict_ = s; }
+  int order() const { return order_; }
+  int inner() const { return inner_; }
 
   std::vector<double> residues() const {
     std::vector<double> out(static_cast<std::size_t>(done_));
@@ -901,7 +1008,8 @@ class Domain {
       }
     }
   };
-  int n_ = 0, device_ = 0;
+  int n_ = 0, n_loc_ = 0, device_ = 0;
+  long long n_res_ = 0;
   StreamHolder stream_holder_;
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, poll_ev_[kPolls] = {}, kev_[4] = {};
@@ -910,16 +1018,21 @@ class Domain {
   int kmax_ = 1, kfix_ = 0, W_ = 8, d1_ = 0;
   std::size_t smem_ = 0;
   int stride_ = 0;
+  std::vector<int> gid_host_;
   DBuf<double2> xy_, nrm_;
   DBuf<std::uint8_t> kind_, part_;
-  DBuf<int> off_, nbr_;
-  DBuf<double> mind_, dt_, mag_, pval_, hist_, diag_;
+  DBuf<int> off_, nbr_, gid_;
+  DBuf<double> mind_, dt_, which_, mag_, pval_, hist_, diag_;
+  double* mag_out_ = nullptr;
   DBuf<long long> psz_;
   DBuf<D4> prim_, q_[2], dq_[2], res_;
   DBuf<Ctl> ctl_;
+  DBuf<Shared> sh_;
+  Shared* shared_ = nullptr;
   DBuf<unsigned long long> it0_, it1_;
   HBuf<unsigned long long> hpoll_;
   HBuf<Ctl> hctl_;
+  HBuf<Shared> hsh_;
   int capacity_ = 1;
   int order_ = 2, inner_ = 3, chunk_ = 16;
   bool strict_ = false;
@@ -932,7 +1045,7 @@ class Domain {
 namespace {
 
 std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
-  auto d = std::make_unique<Domain>(ps, spec.device, spec.part_of, spec.gamma, spec.cfl,
+  auto d = std::make_unique<Domain>(view_of(ps, spec.part_of), spec.device, spec.gamma, spec.cfl,
                                     spec.det_tol, capacity);
   trace("engine: geometry uploaded");
   d->upload(ps.fields, false);
@@ -975,7 +1088,7 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
   if (d->failed()) {
     Fault f = d->fault_in_run();
     copy_back(*d, ps);
-    rec.abort_iteration = d->ctl().err_iter + 1;
+    rec.abort_iteration = d->shared_host().err_iter + 1;
     throw f;
   }
   copy_back(*d, ps);
@@ -988,6 +1101,236 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
   const double first = rec.residue.empty() ? 0.0 : rec.residue.front();
   for (double r : rec.residue)
     rec.log10_rel.push_back((first > 0.0 && r > 0.0) ? std::log10(r / first) : 0.0);
+  return rec;
+}
+
+// ===========================================================================
+// Multi-domain run.  Per iteration, on every domain d (own stream, own device):
+//   [t>0] wait residue(t-1) on the root   (iteration counter + residue buffer)
+//   [t>0] gather q halo from owners        (after their update(t-1))
+//   sweeps s: sweep -> gather dq halo       (after the owners' sweep s; a sweep
+//             that overwrites a buffer readers gathered two stages ago waits
+//             for their gather)
+//   flux -> update (residue summands into the root's global-id array)
+// and on the root: wait every update(t) -> midpoint-tree residue.
+// Stencils keep their global order in local ids, so all per-point arithmetic
+// and the residue tree are identical to the single-domain run.
+namespace {
+
+class EventRing {
+ public:
+  EventRing() = default;
+  EventRing(const EventRing&) = delete;
+  EventRing& operator=(const EventRing&) = delete;
+  void create(int device, int n) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ev_.resize(static_cast<std::size_t>(n));
+    for (auto& e : ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  ~EventRing() {
+    for (auto& e : ev_) cudaEventDestroy(e);
+  }
+  cudaEvent_t operator[](int k) const { return ev_[static_cast<std::size_t>(k) % ev_.size()]; }
+
+ private:
+  std::vector<cudaEvent_t> ev_;
+};
+
+void enable_peers(const std::vector<int>& devs) {
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, a, b), "cudaDeviceCanAccessPeer");
+      if (!can) raise(Status::argument, "devices " + itos(a) + " and " + itos(b) + " cannot access each other's memory");
+      ck(cudaSetDevice(a), "cudaSetDevice");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else ck(e, "cudaDeviceEnablePeerAccess");
+    }
+}
+
+GeomView view_of(const LocalGeom& g) {
+  GeomView v;
+  v.n_own = g.n_own;
+  v.n_loc = g.n_loc;
+  v.x = g.x.data();
+  v.y = g.y.data();
+  v.nx = g.nx.data();
+  v.ny = g.ny.data();
+  v.kind = g.kind.data();
+  v.off = g.off.data();
+  v.nbr = g.nbr.data();
+  v.part = g.part.data();
+  v.gid = g.gid.data();
+  v.nnz = static_cast<std::int64_t>(g.nbr.size());
+  return v;
+}
+
+}  // namespace
+
+RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms) {
+  const int P = static_cast<int>(geoms.size());
+  if (P < 1 || P > kMaxDomains) raise(Status::config, "gpus must lie in [1, " + itos(kMaxDomains) + "]");
+  RunRecord rec;
+  if (spec.iters == 0) return engine_run(ps, spec);
+  int ndev = engine_device_count();
+  if (ndev < 1) raise(Status::argument, "no CUDA device");
+  std::vector<int> dev(static_cast<std::size_t>(P));
+  for (int d = 0; d < P; ++d) dev[d] = (spec.device + d) % ndev;
+  {
+    std::vector<int> uniq(dev);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    enable_peers(uniq);
+  }
+  // sources (owners of my halo) and readers (domains whose halo I own)
+  std::vector<std::vector<int>> src(P), readers(P);
+  for (int d = 0; d < P; ++d) {
+    std::vector<int> s(geoms[d].halo_dom.begin(), geoms[d].halo_dom.end());
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    src[d] = s;
+    for (int o : s) readers[o].push_back(d);
+  }
+  std::vector<std::unique_ptr<Domain>> dom(P);
+  std::vector<std::unique_ptr<DBuf<int>>> hdom(P), hidx(P);
+  for (int d = 0; d < P; ++d) {
+    dom[d] = std::make_unique<Domain>(view_of(geoms[d]), dev[d], spec.gamma, spec.cfl, spec.det_tol, spec.iters);
+    const std::size_t nh = geoms[d].halo_dom.size();
+    hdom[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
+    hidx[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
+    if (nh) {
+      ck(cudaMemcpy(hdom[d]->get(), geoms[d].halo_dom.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hdom");
+      ck(cudaMemcpy(hidx[d]->get(), geoms[d].halo_idx.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hidx");
+    }
+  }
+  Domain& root = *dom[0];
+  root.set_residue_size(ps.n());
+  for (int d = 1; d < P; ++d) {
+    dom[d]->use_shared(root.shared());
+    dom[d]->use_mag(root.mag_buf());
+  }
+  for (int d = 0; d < P; ++d) dom[d]->upload(ps.fields, false);
+  root.reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);
+  root.set_diag(spec.iters - 1);
+  ck(cudaStreamSynchronize(root.stream()), "root init");
+  for (int d = 1; d < P; ++d) dom[d]->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, false);
+  for (int d = 0; d < P; ++d) dom[d]->first_q();
+  for (int d = 0; d < P; ++d) ck(cudaStreamSynchronize(dom[d]->stream()), "first q");
+  trace("engine: domains open");
+
+  std::vector<EventRing> ev_sw(P), ev_dqh(P), ev_upd(P);
+  for (int d = 0; d < P; ++d) {
+    ev_sw[d].create(dev[d], 4);
+    ev_dqh[d].create(dev[d], 4);
+    ev_upd[d].create(dev[d], 2);
+  }
+  EventRing ev_res;
+  ev_res.create(dev[0], 2);
+  cudaEvent_t t0, t1;
+  ck(cudaSetDevice(dev[0]), "cudaSetDevice");
+  ck(cudaEventCreate(&t0), "ev");
+  ck(cudaEventCreate(&t1), "ev");
+  auto wait = [&](int d, cudaEvent_t e) { ck(cudaStreamWaitEvent(dom[d]->stream(), e, 0), "StreamWaitEvent"); };
+  auto peers_q = [&](int a) {
+    PeerTab t{};
+    for (int o = 0; o < P; ++o) t.base[o] = dom[o]->q_buf(a);
+    return t;
+  };
+  auto peers_dq = [&](int b) {
+    PeerTab t{};
+    for (int o = 0; o < P; ++o) t.base[o] = dom[o]->dq_buf(b);
+    return t;
+  };
+  ck(cudaEventRecord(t0, root.stream()), "EventRecord");
+  int issued = 0, waited = 0;
+  bool failed = false;
+  int t = 0;
+  for (; t < spec.iters && !failed; ++t) {
+    const int a = t & 1;
+    if (t > 0) {
+      for (int d = 0; d < P; ++d) {
+        ck(cudaSetDevice(dev[d]), "cudaSetDevice");
+        wait(d, ev_res[t - 1]);
+        for (int o : src[d]) wait(d, ev_upd[o][t - 1]);
+        dom[d]->launch_halo(dom[d]->q_buf(a), 1, hdom[d]->get(), hidx[d]->get(), peers_q(a));
+      }
+    }
+    int bfin = 0;
+    if (spec.order == 2) {
+      for (int s = 0; s < spec.inner; ++s) {
+        const int k = t * spec.inner + s, b = k & 1;
+        for (int d = 0; d < P; ++d) {
+          ck(cudaSetDevice(dev[d]), "cudaSetDevice");
+          if (s >= 2)
+            for (int r : readers[d]) wait(d, ev_dqh[r][k - 2]);
+          dom[d]->launch_sweep(a, b, s == 0);
+          ck(cudaEventRecord(ev_sw[d][k], dom[d]->stream()), "EventRecord");
+        }
+        for (int d = 0; d < P; ++d) {
+          ck(cudaSetDevice(dev[d]), "cudaSetDevice");
+          for (int o : src[d]) wait(d, ev_sw[o][k]);
+          dom[d]->launch_halo(dom[d]->dq_buf(b ^ 1), 2, hdom[d]->get(), hidx[d]->get(), peers_dq(b ^ 1));
+          ck(cudaEventRecord(ev_dqh[d][k], dom[d]->stream()), "EventRecord");
+        }
+      }
+      bfin = ((t + 1) * spec.inner) & 1;
+    }
+    for (int d = 0; d < P; ++d) {
+      ck(cudaSetDevice(dev[d]), "cudaSetDevice");
+      dom[d]->launch_flux(a, bfin, spec.order != 2);
+      dom[d]->launch_update(a);
+      ck(cudaEventRecord(ev_upd[d][t], dom[d]->stream()), "EventRecord");
+    }
+    ck(cudaSetDevice(dev[0]), "cudaSetDevice");
+    for (int d = 1; d < P; ++d) wait(0, ev_upd[d][t]);
+    root.launch_residue();
+    ck(cudaEventRecord(ev_res[t], root.stream()), "EventRecord");
+    ck(cudaGetLastError(), "multi-domain launches");
+    failed = root.poll(issued, waited);
+  }
+  ck(cudaSetDevice(dev[0]), "cudaSetDevice");
+  ck(cudaEventRecord(t1, root.stream()), "EventRecord");
+  for (int d = 0; d < P; ++d) ck(cudaStreamSynchronize(dom[d]->stream()), "multi-domain iterate");
+  float ms = 0.0f;
+  ck(cudaEventElapsedTime(&ms, t0, t1), "EventElapsed");
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  root.refresh_ctl();
+  const int done = root.shared_host().iter;
+  for (int d = 0; d < P; ++d) dom[d]->set_done(done);
+  root.add_ms(ms);
+  trace("engine: iterated");
+  if (root.failed()) {
+    const unsigned long long key = root.shared_host().err_key;
+    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    int owner = 0, local = g;
+    if (static_cast<unsigned>(key >> 61) != PH_RESIDUE) {
+      for (int d = 0; d < P; ++d) {
+        const auto& own = geoms[d].gid;
+        const auto it = std::lower_bound(own.begin(), own.begin() + geoms[d].n_own, g);
+        if (it != own.begin() + geoms[d].n_own && *it == g) {
+          owner = d;
+          local = static_cast<int>(it - own.begin());
+          break;
+        }
+      }
+    }
+    dom[owner]->refresh_ctl();
+    Fault f = dom[owner]->fault_in_run(local);
+    rec.abort_iteration = root.shared_host().err_iter + 1;
+    throw f;
+  }
+  for (int d = 0; d < P; ++d) copy_back(*dom[d], ps);
+  trace("engine: copied back");
+  rec.iterations = done;
+  rec.residue = root.residues();
+  rec.wall_ms = root.wall_ms();
+  rec.kernels = root.kernel_times();
+  rec.total_seconds = root.total_ms() * 1e-3;
+  const double first = rec.residue.empty() ? 0.0 : rec.residue.front();
+  for (double r : rec.residue) rec.log10_rel.push_back((first > 0.0 && r > 0.0) ? std::log10(r / first) : 0.0);
   return rec;
 }
 
@@ -1077,10 +1420,10 @@ void session_close(Session* s) { delete s; }
 
 // ---- per-phase operators ----
 void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
-  Domain d(ps, spec.device, {}, spec.gamma, spec.cfl, spec.det_tol, 1);
+  Domain d(view_of(ps, {}), spec.device, spec.gamma, spec.cfl, spec.det_tol, 1);
   d.set_strict(spec.fp_mode == 1);
   d.upload(ps.fields, true);
-  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), -1);
+  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), d.shared(), 1, -1);
   const Geo g = d.geo();
   const int n = ps.n();
   const int blocks = (n + 255) / 256;
@@ -1120,7 +1463,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
       k_op_timestep<<<blocks, 256, 0, st>>>(g, d.prim(), d.dt(), d.gas());
       break;
     case Op::state_update:
-      k_op_update<<<blocks, 256, 0, st>>>(g, d.prim(), d.res(), d.dt(), d.gas(), d.dctl(), d.mag());
+      k_op_update<<<blocks, 256, 0, st>>>(g, d.prim(), d.res(), d.dt(), d.gas(), d.dctl(), d.which());
       break;
   }
   ck(cudaGetLastError(), "operator launch");
@@ -1141,7 +1484,8 @@ double engine_reduce(const double* v, std::int64_t n, int device) {
   DBuf<long long> ps(1024);
   DBuf<Ctl> ctl(1);
   ck(cudaMemcpy(dv.get(), v, n * sizeof(double), cudaMemcpyHostToDevice), "H2D reduce");
-  k_ctl_init<<<1, 1>>>(ctl.get(), -1);
+  DBuf<Shared> sh(1);
+  k_ctl_init<<<1, 1>>>(ctl.get(), sh.get(), 1, -1);
   const int d1 = tree_depth(n);
   k_tree_partial<<<1 << d1, kTreeThreads>>>(dv.get(), n, d1, pv.get(), ps.get(), ctl.get());
   k_tree_result<<<1, 1024>>>(pv.get(), ps.get(), d1, out.get());

@@ -50,13 +50,19 @@ struct KTimer {
 
 enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_UPDATE = 3, KT_RESIDUE = 4, KT_COUNT = 5 };
 
-// Device control block (one per domain).
-struct Ctl {
-  unsigned long long err_key;
-  int err_iter;  // 0-based iteration of the failure
-  int iter;      // 0-based index of the iteration in flight
-  int diag_iter; // iteration whose res/dt are kept for copy-back
+// Run-wide control word, shared by every domain of a run (lives on the first
+// domain's device; other domains reach it over peer memory).
+struct Shared {
+  unsigned long long err_key;  // min over failures (kNoErr = none)
+  int err_iter;                // 0-based iteration of the failure (min)
+  int iter;                    // 0-based index of the iteration in flight
+  int diag_iter;               // iteration whose res/dt are kept for copy-back
   int pad;
+};
+
+// Per-domain control block: the shared word + this domain's kernel timers.
+struct Ctl {
+  Shared* sh;
   KTimer kt[KT_COUNT];
 };
 
@@ -68,9 +74,12 @@ struct Geo {
   const int* off;
   const int* nbr;
   const double* mind;
-  int n;
-  int kfix;  // uniform stencil size (offsets are then i*kfix), 0 = use CSR offsets
+  const int* gid;  // local -> global point id (null: local ids are global)
+  int n;           // owned points (kernels loop over these)
+  int kfix;        // uniform stencil size (offsets are then i*kfix), 0 = use CSR offsets
 };
+
+__device__ __forceinline__ int gidx(const Geo& g, int i) { return g.gid ? g.gid[i] : i; }
 
 __device__ __forceinline__ void stencil_of(const Geo& g, int i, int& e0, int& k) {
   if (g.kfix > 0) {
@@ -87,8 +96,8 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 }
 
 __device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key) {
-  atomicMin(&ctl->err_key, key);
-  *reinterpret_cast<volatile int*>(&ctl->err_iter) = ctl->iter;
+  atomicMin(&ctl->sh->err_key, key);
+  atomicMin(&ctl->sh->err_iter, *reinterpret_cast<volatile int*>(&ctl->sh->iter));
 }
 
 // ---- per-kernel device timing (globaltimer; one record per kernel class) ----
@@ -108,7 +117,7 @@ __device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* 
       ctl->kt[k].done = 0;
       ctl->kt[k].total_ns += t1 - t0;
       ctl->kt[k].launches += 1;
-      if (iter_t0) iter_t0[ctl->iter] = t0;
+      if (iter_t0) iter_t0[ctl->sh->iter] = t0;
     }
   }
 }
@@ -138,7 +147,7 @@ __global__ void k_qvar(Geo g, const D4* prim, D4* q, Gas gas, Ctl* ctl) {
   if (i < g.n) {
     const D4 s = ld4_rw(prim + i);
     if (!(s.a > 0.0) || !(s.d > 0.0)) {
-      raise_err(ctl, err_key(PH_QVAR, g.part[i], i, 0, 0));
+      raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0));
     } else {
       st4(q + i, q_from_prim(s.a, s.b, s.c, s.d, gas.gm1));
     }
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
                                                unsigned long long* iter_t0) {
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_SWEEP);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n;
        i += gridDim.x * blockDim.x) {
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
     }
     const double det = X::sub(X::mul(sxx, syy), X::mul(sxy, sxy));
     if (!(det > gas.det_tol)) {
-      raise_err(ctl, err_key(PH_SWEEP, g.part[i], i, 0, 0));
+      raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0));
     } else {
       D4 fx, fy;
       fx.a = X::sub(X::mul(syy, bx[0]), X::mul(sxy, by[0])) / det;
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
   __shared__ int s_skip;
 
   ktimer_begin(a.ctl, KT_FLUX);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
   __syncthreads();
   const int lane = threadIdx.x % W;
   const int slot = threadIdx.x / W;
@@ -372,12 +381,12 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
           tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
         }
         if (!(ti[3] < 0.0) || !(tn[3] < 0.0)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dfirst, j));
           continue;
         }
         FluxState fi, fn;
         if (!reconstruct2<S>(ti, tn, a.gas, fi, fn)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, dfirst, j));
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dfirst, j));
           continue;
         }
         const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
         }
         const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
         if (!(det > a.gas.det_tol)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], i, d, kSolveSlot));
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot));
         } else {
   #pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
@@ -482,22 +491,23 @@ struct UpdateArgs {
   D4* prim;      // updated in place
   D4* q_next;
   double* dt;    // written on the diag (copy-back) iteration
-  double* mag;   // (dt * res0)^2
+  double* mag;   // (dt * res0)^2, indexed by GLOBAL point id (the residue tree's order)
+  double* which; // failure detail (density 0 / pressure 1), local index
   Ctl* ctl;
 };
 
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_UPDATE);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
   __syncthreads();
   const int ip = blockIdx.x * blockDim.x + threadIdx.x;
   const Geo& g = a.g;
   if (!s_skip && ip < g.n) {
-    const bool diag = a.ctl->iter == a.ctl->diag_iter;
+    const bool diag = a.ctl->sh->iter == a.ctl->sh->diag_iter;
     if (g.kind[ip] == KIND_OUTER) {
       st4(a.q_next + ip, ld4(a.q + ip));
-      a.mag[ip] = 0.0;
+      a.mag[gidx(g, ip)] = 0.0;
       if (diag) a.dt[ip] = 0.0;
     } else {
       const D4 r = ld4(a.res + ip);
@@ -523,8 +533,8 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
       if (!ok) {
         // keep the failing conserved value for the diagnostic message
         a.dt[ip] = m > 0.0 ? p : m;
-        a.mag[ip] = m > 0.0 ? 1.0 : 0.0;
-        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], ip, 0, 0));
+        a.which[ip] = m > 0.0 ? 1.0 : 0.0;
+        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0));
       } else {
         if (g.kind[ip] == KIND_WALL) {
           const double2 nv = g.nrm[ip];
@@ -535,13 +545,32 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
         st4(a.prim + ip, D4{m, u1, u2, p});
         st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
         const double dm = X::mul(dt, r.a);
-        a.mag[ip] = X::mul(dm, dm);
+        a.mag[gidx(g, ip)] = X::mul(dm, dm);
         if (diag) a.dt[ip] = dt;
       }
     }
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_UPDATE, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Halo exchange: ghost slot h of this domain (local index n_own + h) pulls its
+// `recs` 32-byte records from the owning domain's buffer, read directly over
+// peer memory (NVLink/NVSwitch when the domains sit on different GPUs).
+constexpr int kMaxDomains = 16;
+struct PeerTab {
+  const D4* base[kMaxDomains];
+};
+
+__global__ void k_halo(D4* dst, int recs, int n_own, int n_halo, const int* hdom, const int* hidx,
+                       PeerTab src, const Shared* sh) {
+  if (ld_volatile(&sh->err_key) != kNoErr) return;  // keep the failing iteration's halo intact
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_halo * recs; t += gridDim.x * blockDim.x) {
+    const int h = t / recs, r = t - h * recs;
+    const D4* s = src.base[hdom[h]] + static_cast<size_t>(hidx[h]) * recs + r;
+    st4(dst + static_cast<size_t>(n_own + h) * recs + r, ld4_rw(s));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -565,7 +594,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (i >= g.n || g.kind[i] == KIND_OUTER) return;
   const D4 s = ld4_rw(prim + i);
   if (!(s.a > 0.0) || !(s.d > 0.0)) {  // conserved_from_primitives require_valid
-    raise_err(ctl, err_key(PH_QVAR, g.part[i], i, 0, 0));
+    raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0));
     return;
   }
   const D4 r = ld4(res + i);
@@ -580,7 +609,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (!(m > 0.0)) {
     dt[i] = m;
     which[i] = 0.0;
-    raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0));
     return;
   }
   double u1 = mx / m, u2 = my_ / m;
@@ -588,7 +617,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (!(p > 0.0)) {
     dt[i] = p;
     which[i] = 1.0;
-    raise_err(ctl, err_key(PH_UPDATE, g.part[i], i, 0, 0));
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0));
     return;
   }
   if (g.kind[i] == KIND_WALL) {
@@ -668,7 +697,7 @@ __global__ void __launch_bounds__(kTreeThreads)
   __shared__ long long ss[2][kTreeThreads];
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_RESIDUE);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
   __syncthreads();
   if (!s_skip) {
     long long lo, hi, tlo, thi;
@@ -697,7 +726,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
   __shared__ int s_skip;
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
   __syncthreads();
   if (s_skip) return;
   const int m = 1 << d1;
@@ -709,13 +738,13 @@ __global__ void __launch_bounds__(1024)
   tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
   if (threadIdx.x == 0) {
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
-    const int it = ctl->iter;
+    const int it = ctl->sh->iter;
     if (!isfinite(res)) {
       raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0));
     } else {
       if (history) history[it] = res;
       if (iter_t1) iter_t1[it] = globaltimer();
-      ctl->iter = it + 1;
+      ctl->sh->iter = it + 1;
     }
   }
 }

@@ -31,6 +31,28 @@ EngineSpec prepare_run(const PointSet& ps, const Settings& s);
 // the reference's final 21-slot store.  Throws Fault like run_fixed_point.
 RunRecord engine_run(PointSet& ps, const EngineSpec& spec);
 
+// One device domain of a multi-domain run: the points of one RCB piece in
+// local numbering (owned [0, n_own), then halo [n_own, n_loc)), the local
+// stencil table, and where each halo point lives (owner domain, its local
+// index there).  Built on the host by decompose().
+struct LocalGeom {
+  std::int32_t n_own = 0, n_loc = 0;
+  std::vector<double> x, y, nx, ny;      // n_loc
+  std::vector<Kind> kind;                // n_loc
+  std::vector<std::int64_t> off;         // n_own + 1
+  std::vector<std::int32_t> nbr;         // local ids
+  std::vector<std::uint8_t> part;        // n_loc: reference partition (error tie-break)
+  std::vector<std::int32_t> gid;         // n_loc: local -> global id
+  std::vector<std::int32_t> halo_dom;    // n_loc - n_own
+  std::vector<std::int32_t> halo_idx;    // n_loc - n_own
+};
+std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of);
+
+// Multi-domain run: one Domain per RCB piece, devices assigned round-robin
+// from spec.device; halos exchanged by peer-memory gathers; residue summed
+// over global ids on the first domain (bitwise equal to engine_run).
+RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms);
+
 // Device-resident session (bench, ranks).
 class Session;
 Session* session_open(PointSet& ps, const EngineSpec& spec, int capacity);

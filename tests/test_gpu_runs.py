@@ -180,3 +180,30 @@ def test_200sq_matches_reference_history(cfg, golden):
         pc, res = bump_run(c, prim0, 20, order=2)
         assert rel_seq(res.residues(), want.residue) <= 1e-10
         assert rel_err(pc.fields()[:, :4], want.store[:, :4]) <= 1e-10
+
+
+@pytest.mark.parametrize("gpus", [2, 3, 4, 8])
+def test_multi_domain_halo_engine_is_bitwise_single_domain(bump_cloud_arrays, gpus):
+    """gpus=N splits the cloud into N RCB device domains (on distinct GPUs when
+    present, else sharing one) with peer-memory halo gathers; per-point
+    arithmetic and the residue tree are unchanged, so results are bitwise those
+    of the single-domain run (the reference's invariance across partitions,
+    tests/test_runtime.cpp:250-289)."""
+    c, prim0 = bump_cloud_arrays
+    base, rb = bump_run(c, prim0, 25)
+    for order in (2, 1):
+        if order == 1:
+            base, rb = bump_run(c, prim0, 25, order=1)
+        other, ro = bump_run(c, prim0, 25, order=order, gpus=gpus)
+        assert np.array_equal(ro.residues(), rb.residues()), (gpus, order)
+        assert other.fields_equal(base), (gpus, order)
+
+
+@pytest.mark.parametrize("gpus,parts", [(4, 1), (8, 8)])
+def test_multi_domain_abort_matches_reference(bump_cloud_arrays, golden, gpus, parts):
+    c, prim0 = bump_cloud_arrays
+    _, meta = golden
+    want = meta["o2_abort"] if parts == 1 else meta[f"o2_abort_parts{parts}"]
+    with pytest.raises(L.LskumError) as e:
+        bump_run(c, prim0, 2000, gpus=gpus, parts=parts)
+    assert (e.value.status, e.value.message) == (want["code"], want["message"])
