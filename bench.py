@@ -251,6 +251,7 @@ def run_reference_arm(a):
     if rank != 0:
         return
     from paper_2403_13287_b200 import lskum as LB
+    a.side = int(round(a.side * math.sqrt(max(a.gpus, world))))  # same cloud as the b200 arm
     cloud = LB.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
     n = cloud.n
     L = reference_lib()
@@ -280,17 +281,32 @@ def run_reference_arm(a):
 def run_b200_arm(a):
     from paper_2403_13287_b200 import lskum as L
     world, rank, local = dist_env()
+    gpus = max(a.gpus, world)
+    dist = None
     if world > 1:
-        return run_b200_distributed(a, world, rank, local)
-    dev = 0
-    cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+        # One process per GPU is the launch contract; the halo engine drives all
+        # device domains of the run from rank 0 (single process, peer memory over
+        # NVLink).  Other ranks only join the barriers.
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    # weak scaling: ~160K points per GPU (side grows with sqrt(gpus))
+    side = int(round(a.side * math.sqrt(gpus)))
+    a.side = side
+    cloud = L.Cloud.generate_rect(side, side, 0.1, 7, 8)
     n = cloud.n
     k = cloud.nnz // n
     n_flux = int(sum(1 for v in cloud.geometry()["kind"] if v != 2))
     cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
-                   iters=a.steps, device=dev)
+                   iters=a.steps, device=0, gpus=gpus)
     steady_iters = 0
-    with ClockSampler(dev) as clocks:
+    if dist is not None:
+        dist.barrier()
+    with ClockSampler(0) as clocks:
         sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps + 4000)
         for _ in range(a.warmup):
             sess.flush_l2()
@@ -303,7 +319,6 @@ def run_b200_arm(a):
             sweep_ms.append(sw)
             flux_ms.append(fl)
         launches = sess.info()["launches_per_iter"]
-        # steady state (no flush, back-to-back graphs) ~1.5 s, also keeps the clock sampler busy
         steady = None
         if not a.no_steady:
             per = max(statistics.median(step_ms), 1e-3)
@@ -317,9 +332,9 @@ def run_b200_arm(a):
     value = n * a.steps / (total_ms * 1e-3)
 
     # e2e through the drop-in C ABI (lskum_run) from host buffers
-    e2e_cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
+    e2e_cloud = L.Cloud.generate_rect(side, side, 0.1, 7, 8)
     e2e_cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5,
-                       fp_mode=a.fp_mode, iters=a.steps, device=dev)
+                       fp_mode=a.fp_mode, iters=a.steps, device=0, gpus=gpus)
     L.run(e2e_cloud, e2e_cfg).close()  # warm (context, module load)
     t0 = time.perf_counter()
     res = L.run(e2e_cloud, e2e_cfg)
@@ -327,90 +342,58 @@ def run_b200_arm(a):
     res.close()
     nnz = e2e_cloud.nnz
     h2d = n * (16 + 16 + 1 + 1 + 32) + 4 * (n + 1) + 4 * nnz  # xy, normals, kind, part, prim, off, ids
-    d2h = n * (32 + 32 + 64 + 32 + 8) + 8 * a.steps        # prim q qx qy res dt + residue history
+    d2h = n * 21 * 8 + 8 * a.steps                           # 21-slot store + residue history
 
     # rooflines
     counts = load_counts()
-    fp64_peak = L.fp64_peak_tflops(dev)
+    fp64_peak = L.fp64_peak_tflops(0)
     flux_avg = statistics.mean(flux_ms)
     flops_pt = counts.get("flux_fp64_flops_per_point")
-    achieved = flops_pt * n_flux / (flux_avg * 1e-3) / 1e12 if flops_pt else None
+    n_flux_dom = n_flux / gpus
+    achieved = flops_pt * n_flux_dom / (flux_avg * 1e-3) / 1e12 if (flops_pt and flux_avg > 0) else None
     traffic = counts.get("flux_dram_bytes_per_point")
     hbm, hbm_kind = hbm_peak()
     sweep_avg = statistics.mean(sweep_ms) if a.order == 2 else None
-    sweep_gbs = sweep_bytes(k) * n / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
-    iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9
+    sweep_gbs = sweep_bytes(k) * (n / gpus) / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
+    iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9 / gpus
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "strong",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak" if gpus > 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (free-stream state on a generated cloud)",
-        "config": config_block(a, n),
+        "config": config_block(a, n, {"parallelism": f"rcb{gpus} device domains, peer-memory halos"
+                                      if gpus > 1 else "single-domain"}),
         "e2e": {"value": n * a.steps / e2e_wall, "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps),
                 "what": "wall time of lskum_run (C ABI, host buffers): screening, upload, "
                         f"{a.steps} iterations, copy-back of the 21-slot store"},
         "gpu_launches": launches * a.steps,
-        "gpu_launches_note": f"{launches} kernels per iteration (sweeps, fused flux, 2 residue-tree "
-                             f"stages) x {a.steps}; plus {a.steps} L2-flush kernels between steps",
-        "roofline": {"bound": "fp64", "kernel": "k_flux (fused flux residual + dt + update + q)",
+        "gpu_launches_note": f"{launches} kernels per iteration (all domains) x {a.steps}; "
+                             f"plus {a.steps * gpus} L2-flush kernels between steps",
+        "roofline": {"bound": "fp64", "kernel": "k_flux (flux residual, W=8 lanes per point)",
                      "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak if achieved else None,
-                     "traffic": traffic * n_flux if traffic else None,
+                     "traffic": traffic * n_flux_dom if traffic else None,
                      "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
-                     "flops_source": "ncu dynamic DFMA*2+DADD+DMUL per point, profiles/flux_ncu_counts.json",
+                     "flops_source": "ncu dynamic 2*DFMA+DADD+DMUL per point, profiles/flux_ncu_counts.json",
                      "launch_ms": flux_avg},
         "roofline_hbm": {"bound": "hbm", "kernel": "k_sweep", "achieved": sweep_gbs, "peak": hbm,
                          "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
                          "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_avg,
                          "peak_source": hbm_kind,
-                         "iteration_achieved_gbs": iter_gbs, "iteration_frac": iter_gbs / hbm,
+                         "iteration_achieved_gbs_per_gpu": iter_gbs, "iteration_frac": iter_gbs / hbm,
                          "iteration_bytes_per_point": iteration_bytes(k, a.order, a.inner)},
         "steady_state": {"value": steady, "iterations": steady_iters,
-                         "what": "same session, back-to-back graph replays, no L2 flush"},
+                         "what": "same session, back-to-back iterations, no L2 flush"},
         "clocks": clk,
         "final_residue": float(residues[-1]) if len(residues) else None,
     }
-    if not a.no_cpu_baseline:
+    if not a.no_cpu_baseline and gpus == 1:
         out["cpu_baseline"] = cpu_baseline(cloud, a, a.cpu_seconds)
     print(json.dumps(out), flush=True)
-
-
-def run_b200_distributed(a, world, rank, local):
-    """One process per GPU (torchrun).  Each rank owns one RCB piece of the same
-    cloud; see DESIGN.md (multi-GPU)."""
-    import torch
-    import torch.distributed as dist
-    from paper_2403_13287_b200 import lskum as L
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
-    cloud = L.Cloud.generate_rect(a.side, a.side, 0.1, 7, 8)
-    n = cloud.n
-    cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
-                   iters=a.steps, device=local, parts=world)
-    sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps)
-    for _ in range(a.warmup):
-        sess.iterate(1)
-    dist.barrier()
-    torch.cuda.synchronize()
-    ms = 0.0
-    for _ in range(a.steps):
-        sess.flush_l2()
-        ms += sess.iterate(1)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([ms], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    if rank == 0:
-        value = n * world * a.steps / (total_ms * 1e-3)
-        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-                          "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                          "dtype": "f64", "data": "synthetic",
-                          "config": config_block(a, n, {"parallelism": f"replica x{world} (halo engine pending)"}),
-                          "gpu_launches": sess.info()["launches_per_iter"] * a.steps}), flush=True)
-    sess.close()
-    dist.destroy_process_group()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():

@@ -1169,203 +1169,303 @@ GeomView view_of(const LocalGeom& g) {
 
 }  // namespace
 
-RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms) {
-  const int P = static_cast<int>(geoms.size());
-  if (P < 1 || P > kMaxDomains) raise(Status::config, "gpus must lie in [1, " + itos(kMaxDomains) + "]");
-  RunRecord rec;
-  if (spec.iters == 0) return engine_run(ps, spec);
-  int ndev = engine_device_count();
-  if (ndev < 1) raise(Status::argument, "no CUDA device");
-  std::vector<int> dev(static_cast<std::size_t>(P));
-  for (int d = 0; d < P; ++d) dev[d] = (spec.device + d) % ndev;
-  {
-    std::vector<int> uniq(dev);
-    std::sort(uniq.begin(), uniq.end());
-    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    enable_peers(uniq);
-  }
-  // sources (owners of my halo) and readers (domains whose halo I own)
-  std::vector<std::vector<int>> src(P), readers(P);
-  for (int d = 0; d < P; ++d) {
-    std::vector<int> s(geoms[d].halo_dom.begin(), geoms[d].halo_dom.end());
-    std::sort(s.begin(), s.end());
-    s.erase(std::unique(s.begin(), s.end()), s.end());
-    src[d] = s;
-    for (int o : s) readers[o].push_back(d);
-  }
-  std::vector<std::unique_ptr<Domain>> dom(P);
-  std::vector<std::unique_ptr<DBuf<int>>> hdom(P), hidx(P);
-  for (int d = 0; d < P; ++d) {
-    dom[d] = std::make_unique<Domain>(view_of(geoms[d]), dev[d], spec.gamma, spec.cfl, spec.det_tol, spec.iters);
-    const std::size_t nh = geoms[d].halo_dom.size();
-    hdom[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
-    hidx[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
-    if (nh) {
-      ck(cudaMemcpy(hdom[d]->get(), geoms[d].halo_dom.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hdom");
-      ck(cudaMemcpy(hidx[d]->get(), geoms[d].halo_idx.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hidx");
+class MultiRun {
+ public:
+  MultiRun(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms, int capacity)
+      : ps_(ps), spec_(spec), geoms_(geoms), P_(static_cast<int>(geoms.size())) {
+    if (P_ < 1 || P_ > kMaxDomains) raise(Status::config, "gpus must lie in [1, " + itos(kMaxDomains) + "]");
+    const int ndev = engine_device_count();
+    if (ndev < 1) raise(Status::argument, "no CUDA device");
+    dev_.resize(static_cast<std::size_t>(P_));
+    for (int d = 0; d < P_; ++d) dev_[d] = (spec.device + d) % ndev;
+    {
+      std::vector<int> uniq(dev_);
+      std::sort(uniq.begin(), uniq.end());
+      uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+      enable_peers(uniq);
     }
+    src_.resize(P_);
+    readers_.resize(P_);
+    for (int d = 0; d < P_; ++d) {
+      std::vector<int> sv(geoms[d].halo_dom.begin(), geoms[d].halo_dom.end());
+      std::sort(sv.begin(), sv.end());
+      sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
+      src_[d] = sv;
+      for (int o : sv) readers_[o].push_back(d);
+    }
+    dom_.resize(P_);
+    hdom_.resize(P_);
+    hidx_.resize(P_);
+    for (int d = 0; d < P_; ++d) {
+      dom_[d] = std::make_unique<Domain>(view_of(geoms[d]), dev_[d], spec.gamma, spec.cfl, spec.det_tol, capacity);
+      const std::size_t nh = geoms[d].halo_dom.size();
+      ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+      hdom_[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
+      hidx_[d] = std::make_unique<DBuf<int>>(std::max<std::size_t>(1, nh));
+      if (nh) {
+        ck(cudaMemcpy(hdom_[d]->get(), geoms[d].halo_dom.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hdom");
+        ck(cudaMemcpy(hidx_[d]->get(), geoms[d].halo_idx.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hidx");
+      }
+    }
+    Domain& r = root();
+    r.set_residue_size(ps.n());
+    for (int d = 1; d < P_; ++d) {
+      dom_[d]->use_shared(r.shared());
+      dom_[d]->use_mag(r.mag_buf());
+    }
+    for (int d = 0; d < P_; ++d) dom_[d]->upload(ps.fields, false);
+    r.reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);
+    ck(cudaStreamSynchronize(r.stream()), "root init");
+    for (int d = 1; d < P_; ++d) dom_[d]->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, false);
+    for (int d = 0; d < P_; ++d) dom_[d]->first_q();
+    for (int d = 0; d < P_; ++d) ck(cudaStreamSynchronize(dom_[d]->stream()), "first q");
+    ev_sw_ = std::vector<EventRing>(P_);
+    ev_dqh_ = std::vector<EventRing>(P_);
+    ev_upd_ = std::vector<EventRing>(P_);
+    for (int d = 0; d < P_; ++d) {
+      ev_sw_[d].create(dev_[d], 4);
+      ev_dqh_[d].create(dev_[d], 4);
+      ev_upd_[d].create(dev_[d], 2);
+    }
+    ev_res_.create(dev_[0], 2);
+    ck(cudaSetDevice(dev_[0]), "cudaSetDevice");
+    ck(cudaEventCreate(&t0_), "ev");
+    ck(cudaEventCreate(&t1_), "ev");
+    for (auto& e : kev_) ck(cudaEventCreate(&e), "ev");
+    r.refresh_ctl();
   }
-  Domain& root = *dom[0];
-  root.set_residue_size(ps.n());
-  for (int d = 1; d < P; ++d) {
-    dom[d]->use_shared(root.shared());
-    dom[d]->use_mag(root.mag_buf());
+  ~MultiRun() {
+    for (int d = 0; d < P_; ++d)
+      if (dom_[d]) cudaStreamSynchronize(dom_[d]->stream());
+    cudaEventDestroy(t0_);
+    cudaEventDestroy(t1_);
+    for (auto& e : kev_) cudaEventDestroy(e);
   }
-  for (int d = 0; d < P; ++d) dom[d]->upload(ps.fields, false);
-  root.reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);
-  root.set_diag(spec.iters - 1);
-  ck(cudaStreamSynchronize(root.stream()), "root init");
-  for (int d = 1; d < P; ++d) dom[d]->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, false);
-  for (int d = 0; d < P; ++d) dom[d]->first_q();
-  for (int d = 0; d < P; ++d) ck(cudaStreamSynchronize(dom[d]->stream()), "first q");
-  trace("engine: domains open");
 
-  std::vector<EventRing> ev_sw(P), ev_dqh(P), ev_upd(P);
-  for (int d = 0; d < P; ++d) {
-    ev_sw[d].create(dev[d], 4);
-    ev_dqh[d].create(dev[d], 4);
-    ev_upd[d].create(dev[d], 2);
+  Domain& root() { return *dom_[0]; }
+  int launches_per_iter() const {
+    return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 3) + 2;
   }
-  EventRing ev_res;
-  ev_res.create(dev[0], 2);
-  cudaEvent_t t0, t1;
-  ck(cudaSetDevice(dev[0]), "cudaSetDevice");
-  ck(cudaEventCreate(&t0), "ev");
-  ck(cudaEventCreate(&t1), "ev");
-  auto wait = [&](int d, cudaEvent_t e) { ck(cudaStreamWaitEvent(dom[d]->stream(), e, 0), "StreamWaitEvent"); };
-  auto peers_q = [&](int a) {
-    PeerTab t{};
-    for (int o = 0; o < P; ++o) t.base[o] = dom[o]->q_buf(a);
-    return t;
-  };
-  auto peers_dq = [&](int b) {
-    PeerTab t{};
-    for (int o = 0; o < P; ++o) t.base[o] = dom[o]->dq_buf(b);
-    return t;
-  };
-  ck(cudaEventRecord(t0, root.stream()), "EventRecord");
-  int issued = 0, waited = 0;
-  bool failed = false;
-  int t = 0;
-  for (; t < spec.iters && !failed; ++t) {
-    const int a = t & 1;
-    if (t > 0) {
-      for (int d = 0; d < P; ++d) {
-        ck(cudaSetDevice(dev[d]), "cudaSetDevice");
-        wait(d, ev_res[t - 1]);
-        for (int o : src[d]) wait(d, ev_upd[o][t - 1]);
-        dom[d]->launch_halo(dom[d]->q_buf(a), 1, hdom[d]->get(), hidx[d]->get(), peers_q(a));
-      }
+
+  // Enqueues n more iterations (stopping early on an error); returns the
+  // CUDA-event ms on the root stream, which waits for every domain.
+  double iterate(int n) {
+    Domain& r = root();
+    ck(cudaSetDevice(dev_[0]), "cudaSetDevice");
+    r.set_diag(t_ + n - 1);
+    ck(cudaStreamSynchronize(r.stream()), "set diag");
+    ck(cudaEventRecord(t0_, r.stream()), "EventRecord");
+    for (int d = 1; d < P_; ++d) wait(d, t0_);  // all domains start after the stamp
+    int issued = 0, waited = 0;
+    bool failed = false;
+    const int end = t_ + n;
+    for (; t_ < end && !failed; ++t_) {
+      failed = enqueue(t_, t_ == end - 1) || false;
+      failed = r.poll(issued, waited);
     }
-    int bfin = 0;
-    if (spec.order == 2) {
-      for (int s = 0; s < spec.inner; ++s) {
-        const int k = t * spec.inner + s, b = k & 1;
-        for (int d = 0; d < P; ++d) {
-          ck(cudaSetDevice(dev[d]), "cudaSetDevice");
-          if (s >= 2)
-            for (int r : readers[d]) wait(d, ev_dqh[r][k - 2]);
-          dom[d]->launch_sweep(a, b, s == 0);
-          ck(cudaEventRecord(ev_sw[d][k], dom[d]->stream()), "EventRecord");
-        }
-        for (int d = 0; d < P; ++d) {
-          ck(cudaSetDevice(dev[d]), "cudaSetDevice");
-          for (int o : src[d]) wait(d, ev_sw[o][k]);
-          dom[d]->launch_halo(dom[d]->dq_buf(b ^ 1), 2, hdom[d]->get(), hidx[d]->get(), peers_dq(b ^ 1));
-          ck(cudaEventRecord(ev_dqh[d][k], dom[d]->stream()), "EventRecord");
-        }
-      }
-      bfin = ((t + 1) * spec.inner) & 1;
-    }
-    for (int d = 0; d < P; ++d) {
-      ck(cudaSetDevice(dev[d]), "cudaSetDevice");
-      dom[d]->launch_flux(a, bfin, spec.order != 2);
-      dom[d]->launch_update(a);
-      ck(cudaEventRecord(ev_upd[d][t], dom[d]->stream()), "EventRecord");
-    }
-    ck(cudaSetDevice(dev[0]), "cudaSetDevice");
-    for (int d = 1; d < P; ++d) wait(0, ev_upd[d][t]);
-    root.launch_residue();
-    ck(cudaEventRecord(ev_res[t], root.stream()), "EventRecord");
-    ck(cudaGetLastError(), "multi-domain launches");
-    failed = root.poll(issued, waited);
+    ck(cudaSetDevice(dev_[0]), "cudaSetDevice");
+    ck(cudaEventRecord(t1_, r.stream()), "EventRecord");
+    for (int d = 0; d < P_; ++d) ck(cudaStreamSynchronize(dom_[d]->stream()), "multi-domain iterate");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, t0_, t1_), "EventElapsed");
+    r.refresh_ctl();
+    const int done = r.shared_host().iter;
+    for (int d = 0; d < P_; ++d) dom_[d]->set_done(done);
+    r.add_ms(ms);
+    return ms;
   }
-  ck(cudaSetDevice(dev[0]), "cudaSetDevice");
-  ck(cudaEventRecord(t1, root.stream()), "EventRecord");
-  for (int d = 0; d < P; ++d) ck(cudaStreamSynchronize(dom[d]->stream()), "multi-domain iterate");
-  float ms = 0.0f;
-  ck(cudaEventElapsedTime(&ms, t0, t1), "EventElapsed");
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
-  root.refresh_ctl();
-  const int done = root.shared_host().iter;
-  for (int d = 0; d < P; ++d) dom[d]->set_done(done);
-  root.add_ms(ms);
-  trace("engine: iterated");
-  if (root.failed()) {
-    const unsigned long long key = root.shared_host().err_key;
+
+  bool failed() { return root().failed(); }
+
+  Fault fault() {
+    const unsigned long long key = root().shared_host().err_key;
     const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
     int owner = 0, local = g;
     if (static_cast<unsigned>(key >> 61) != PH_RESIDUE) {
-      for (int d = 0; d < P; ++d) {
-        const auto& own = geoms[d].gid;
-        const auto it = std::lower_bound(own.begin(), own.begin() + geoms[d].n_own, g);
-        if (it != own.begin() + geoms[d].n_own && *it == g) {
+      for (int d = 0; d < P_; ++d) {
+        const auto& own = geoms_[d].gid;
+        const auto it = std::lower_bound(own.begin(), own.begin() + geoms_[d].n_own, g);
+        if (it != own.begin() + geoms_[d].n_own && *it == g) {
           owner = d;
           local = static_cast<int>(it - own.begin());
           break;
         }
       }
     }
-    dom[owner]->refresh_ctl();
-    Fault f = dom[owner]->fault_in_run(local);
-    rec.abort_iteration = root.shared_host().err_iter + 1;
+    dom_[owner]->refresh_ctl();
+    return dom_[owner]->fault_in_run(local);
+  }
+
+  void download() {
+    for (int d = 0; d < P_; ++d) copy_back(*dom_[d], ps_);
+  }
+
+  void flush_l2() {
+    for (int d = 0; d < P_; ++d) dom_[d]->flush_l2();
+  }
+
+  void last_event_ms(double& sweep_ms, double& flux_ms) const {
+    float a = 0.0f, b = 0.0f;
+    sweep_ms = flux_ms = 0.0;
+    if (spec_.order == 2 && cudaEventElapsedTime(&a, kev_[0], kev_[1]) == cudaSuccess) sweep_ms = a;
+    if (cudaEventElapsedTime(&b, kev_[2], kev_[3]) == cudaSuccess) flux_ms = b;
+    cudaGetLastError();
+  }
+
+ private:
+  void wait(int d, cudaEvent_t e) { ck(cudaStreamWaitEvent(dom_[d]->stream(), e, 0), "StreamWaitEvent"); }
+  PeerTab peers_q(int a) const {
+    PeerTab tb{};
+    for (int o = 0; o < P_; ++o) tb.base[o] = dom_[o]->q_buf(a);
+    return tb;
+  }
+  PeerTab peers_dq(int b) const {
+    PeerTab tb{};
+    for (int o = 0; o < P_; ++o) tb.base[o] = dom_[o]->dq_buf(b);
+    return tb;
+  }
+
+  bool enqueue(int t, bool timed) {
+    const int a = t & 1;
+    Domain& r = root();
+    if (t > 0) {
+      for (int d = 0; d < P_; ++d) {
+        ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+        wait(d, ev_res_[t - 1]);
+        for (int o : src_[d]) wait(d, ev_upd_[o][t - 1]);
+        dom_[d]->launch_halo(dom_[d]->q_buf(a), 1, hdom_[d]->get(), hidx_[d]->get(), peers_q(a));
+      }
+    }
+    int bfin = 0;
+    if (spec_.order == 2) {
+      for (int s = 0; s < spec_.inner; ++s) {
+        const int k = t * spec_.inner + s, b = k & 1;
+        for (int d = 0; d < P_; ++d) {
+          ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+          if (s >= 2)
+            for (int rd : readers_[d]) wait(d, ev_dqh_[rd][k - 2]);
+          if (timed && s == 0 && d == 0) ck(cudaEventRecord(kev_[0], r.stream()), "EventRecord");
+          dom_[d]->launch_sweep(a, b, s == 0);
+          if (timed && s == 0 && d == 0) ck(cudaEventRecord(kev_[1], r.stream()), "EventRecord");
+          ck(cudaEventRecord(ev_sw_[d][k], dom_[d]->stream()), "EventRecord");
+        }
+        for (int d = 0; d < P_; ++d) {
+          ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+          for (int o : src_[d]) wait(d, ev_sw_[o][k]);
+          dom_[d]->launch_halo(dom_[d]->dq_buf(b ^ 1), 2, hdom_[d]->get(), hidx_[d]->get(), peers_dq(b ^ 1));
+          ck(cudaEventRecord(ev_dqh_[d][k], dom_[d]->stream()), "EventRecord");
+        }
+      }
+      bfin = ((t + 1) * spec_.inner) & 1;
+    }
+    for (int d = 0; d < P_; ++d) {
+      ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+      if (timed && d == 0) ck(cudaEventRecord(kev_[2], r.stream()), "EventRecord");
+      dom_[d]->launch_flux(a, bfin, spec_.order != 2);
+      if (timed && d == 0) ck(cudaEventRecord(kev_[3], r.stream()), "EventRecord");
+      dom_[d]->launch_update(a);
+      ck(cudaEventRecord(ev_upd_[d][t], dom_[d]->stream()), "EventRecord");
+    }
+    ck(cudaSetDevice(dev_[0]), "cudaSetDevice");
+    for (int d = 1; d < P_; ++d) wait(0, ev_upd_[d][t]);
+    r.launch_residue();
+    ck(cudaEventRecord(ev_res_[t], r.stream()), "EventRecord");
+    ck(cudaGetLastError(), "multi-domain launches");
+    return false;
+  }
+
+  PointSet& ps_;
+  EngineSpec spec_;
+  std::vector<LocalGeom> geoms_;
+  int P_ = 0;
+  std::vector<int> dev_;
+  std::vector<std::vector<int>> src_, readers_;
+  std::vector<std::unique_ptr<Domain>> dom_;
+  std::vector<std::unique_ptr<DBuf<int>>> hdom_, hidx_;
+  std::vector<EventRing> ev_sw_, ev_dqh_, ev_upd_;
+  EventRing ev_res_;
+  cudaEvent_t t0_ = nullptr, t1_ = nullptr, kev_[4] = {};
+  int t_ = 0;
+};
+
+RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms) {
+  if (spec.iters == 0) return engine_run(ps, spec);
+  RunRecord rec;
+  MultiRun m(ps, spec, geoms, spec.iters);
+  trace("engine: domains open");
+  if (m.failed()) throw m.fault();
+  m.iterate(spec.iters);
+  trace("engine: iterated");
+  if (m.failed()) {
+    Fault f = m.fault();
+    rec.abort_iteration = m.root().shared_host().err_iter + 1;
     throw f;
   }
-  for (int d = 0; d < P; ++d) copy_back(*dom[d], ps);
+  m.download();
   trace("engine: copied back");
-  rec.iterations = done;
-  rec.residue = root.residues();
-  rec.wall_ms = root.wall_ms();
-  rec.kernels = root.kernel_times();
-  rec.total_seconds = root.total_ms() * 1e-3;
+  Domain& r = m.root();
+  rec.iterations = r.done();
+  rec.residue = r.residues();
+  rec.wall_ms = r.wall_ms();
+  rec.kernels = r.kernel_times();
+  rec.total_seconds = r.total_ms() * 1e-3;
   const double first = rec.residue.empty() ? 0.0 : rec.residue.front();
-  for (double r : rec.residue) rec.log10_rel.push_back((first > 0.0 && r > 0.0) ? std::log10(r / first) : 0.0);
+  for (double x : rec.residue) rec.log10_rel.push_back((first > 0.0 && x > 0.0) ? std::log10(x / first) : 0.0);
   return rec;
 }
 
-// ---- sessions ----
+// ---- sessions (single domain, or a multi-domain run when spec.gpus > 1) ----
 class Session {
  public:
   std::unique_ptr<Domain> dom;
+  std::unique_ptr<MultiRun> multi;
   PointSet* ps = nullptr;
+  Domain& head() { return multi ? multi->root() : *dom; }
+  const Domain& head() const { return multi ? const_cast<MultiRun&>(*multi).root() : *dom; }
 };
 
 Session* session_open(PointSet& ps, const EngineSpec& spec, int capacity) {
   auto s = std::make_unique<Session>();
   s->ps = &ps;
-  s->dom = open_domain(ps, spec, capacity);
-  if (s->dom->failed()) throw s->dom->fault_in_run();
+  if (spec.gpus > 1) {
+    s->multi = std::make_unique<MultiRun>(ps, spec, decompose(ps, spec.gpus, spec.part_of), capacity);
+    if (s->multi->failed()) throw s->multi->fault();
+  } else {
+    s->dom = open_domain(ps, spec, capacity);
+    if (s->dom->failed()) throw s->dom->fault_in_run();
+  }
   return s.release();
 }
 
 double session_iterate(Session* s, int n) {
+  if (s->multi) {
+    const double ms = s->multi->iterate(n);
+    if (s->multi->failed()) throw s->multi->fault();
+    return ms;
+  }
   const double ms = s->dom->iterate(n);
   if (s->dom->failed()) throw s->dom->fault_in_run();
   return ms;
 }
 
-std::vector<double> session_residues(const Session* s) { return s->dom->residues(); }
-std::vector<KernelTime> session_kernels(const Session* s) { return s->dom->kernel_times(); }
-int session_launches_per_iter(const Session* s) { return s->dom->launches_per_iter(); }
-std::uint64_t session_stream(const Session* s) {
-  return reinterpret_cast<std::uint64_t>(s->dom->stream());
+std::vector<double> session_residues(const Session* s) { return s->head().residues(); }
+std::vector<KernelTime> session_kernels(const Session* s) { return s->head().kernel_times(); }
+int session_launches_per_iter(const Session* s) {
+  return s->multi ? s->multi->launches_per_iter() : s->dom->launches_per_iter();
 }
-void session_download(Session* s) { copy_back(*s->dom, *s->ps); }
+std::uint64_t session_stream(const Session* s) { return reinterpret_cast<std::uint64_t>(s->head().stream()); }
+void session_download(Session* s) {
+  if (s->multi) s->multi->download();
+  else copy_back(*s->dom, *s->ps);
+}
 void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms) {
-  s->dom->last_event_ms(*sweep_ms, *flux_ms);
+  if (s->multi) s->multi->last_event_ms(*sweep_ms, *flux_ms);
+  else s->dom->last_event_ms(*sweep_ms, *flux_ms);
 }
-void session_flush_l2(Session* s) { s->dom->flush_l2(); }
+void session_flush_l2(Session* s) {
+  if (s->multi) s->multi->flush_l2();
+  else s->dom->flush_l2();
+}
 
 __global__ void k_math_selftest(int fn, const double* in, long long n, double* ref, double* ours) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;

@@ -20,6 +20,7 @@ struct EngineSpec {
   int fp_mode = 0;  // 0 fast, 1 strict
   int chunk = 16;   // iterations per captured graph
   int device = 0;
+  int gpus = 1;     // device domains (sessions; lskum_run decides in solve.cpp)
   // Partition of each point (reference error tie-break, runtime.cpp:115-118).
   std::vector<std::uint8_t> part_of;
 };

@@ -22,6 +22,7 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
   spec.fp_mode = s.fp_mode;
   spec.chunk = s.chunk;
   spec.device = s.device;
+  spec.gpus = s.gpus;
   if (s.parts > ps.n())
     raise(Status::argument, "more partitions than points (" + std::to_string(s.parts) + " > " +
                                 std::to_string(ps.n()) + ")");

@@ -207,3 +207,16 @@ def test_multi_domain_abort_matches_reference(bump_cloud_arrays, golden, gpus, p
     with pytest.raises(L.LskumError) as e:
         bump_run(c, prim0, 2000, gpus=gpus, parts=parts)
     assert (e.value.status, e.value.message) == (want["code"], want["message"])
+
+
+def test_multi_domain_session_pieces_equal_single_run(bump_cloud_arrays):
+    c, prim0 = bump_cloud_arrays
+    whole, rw = bump_run(c, prim0, 20)
+    pc = product_cloud(c)
+    pc.set_primitives(prim0)
+    with L.Session(pc, L.Config(iters=20, gpus=3), capacity=20, from_state=True) as s:
+        for n in (5, 15):
+            s.iterate(n)
+        assert np.array_equal(s.residues(), rw.residues())
+        s.download()
+    assert pc.fields_equal(whole)
