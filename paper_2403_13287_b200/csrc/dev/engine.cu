@@ -157,17 +157,45 @@ void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   k_flux<W, S, MB, ST><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
 }
 
-int sweep_grid(int n) {
+// Derivative sweep launch: strict (bitwise) or FMA variant, resident blocks per
+// SM from LSKUM_SWEEP_MINB (2 | 3 | 4, default 3), persistent grid.
+int sweep_min_blocks() {
+  static int mb = [] {
+    const char* e = std::getenv("LSKUM_SWEEP_MINB");
+    const int v = e ? std::atoi(e) : 3;
+    return (v >= 2 && v <= 4) ? v : 3;
+  }();
+  return mb;
+}
+
+template <bool S, int MB>
+void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                    unsigned long long* it0, cudaStream_t st) {
   static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!resident[dev & 63]) {
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep, 256, 0), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<S, MB>, 256, 0), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
-  return std::max(1, std::min((n + 255) / 256, resident[dev & 63]));
+  const int grid = std::max(1, std::min((g.n + 255) / 256, resident[dev & 63]));
+  k_sweep<S, MB><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0);
+}
+
+void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                  unsigned long long* it0, cudaStream_t st) {
+  const int mb = sweep_min_blocks();
+  if (strict) {
+    if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    else sweep_launch_t<true, 3>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+  } else {
+    if (mb == 2) sweep_launch_t<false, 2>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+  }
 }
 
 // Register/occupancy trade-off of the unstaged W=8 kernel: minimum resident
@@ -191,8 +219,50 @@ bool flux_staging() {
   return on;
 }
 
+// Lane-per-state flux kernel (k_flux_split) for stencils of <= 8 neighbours:
+// LSKUM_FLUX_SPLIT = 1 (default) | 0, resident blocks LSKUM_FLUX_SPLIT_MB = 3 | 4.
+int flux_split_mode() {
+  static int m = [] {
+    const char* e = std::getenv("LSKUM_FLUX_SPLIT");
+    const char* b = std::getenv("LSKUM_FLUX_SPLIT_MB");
+    if (e && e[0] == '0') return 0;
+    return (b && b[0] == '4') ? 4 : 3;
+  }();
+  return m;
+}
+
+template <bool S, int MB>
+void flux_split_launch_t(FluxArgs a, cudaStream_t st) {
+  constexpr int P = 16;
+  a.stride = flux_stride(a.kcap);
+  const std::size_t smem = (static_cast<std::size_t>(P) * a.stride + P * 16) * sizeof(double);
+  static std::size_t configured[64] = {};
+  static int resident[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > configured[dev & 63]) {
+    ck(cudaFuncSetAttribute(k_flux_split<S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+       "cudaFuncSetAttribute(k_flux_split)");
+    configured[dev & 63] = smem;
+    resident[dev & 63] = 0;
+  }
+  if (!resident[dev & 63]) {
+    int per_sm = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_split<S, MB>, 256, smem), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    resident[dev & 63] = std::max(1, per_sm) * sms;
+  }
+  const int groups = (a.g.n + P - 1) / P;
+  k_flux_split<S, MB><<<std::max(1, std::min(groups, resident[dev & 63])), 256, smem, st>>>(a);
+}
+
 template <bool S>
 void flux_launch_s(int W, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
+  if (W == 8 && flux_split_mode() && a.kcap <= 8) {
+    if (flux_split_mode() == 4) flux_split_launch_t<S, 4>(a, st);
+    else flux_split_launch_t<S, 3>(a, st);
+    return;
+  }
   if (W == 8) {
     if (flux_staging() && a.g.kfix > 0 && a.g.kfix <= 8) {
       flux_launch_t<8, S, 2, true>(a, smem, st);
@@ -714,8 +784,8 @@ class Domain {
 
   // ---- building blocks of one iteration (also used by the multi-domain driver) ----
   void launch_sweep(int a, int b, bool first) {
-    k_sweep<<<sweep_grid(n_), 256, 0, st_>>>(geo(), q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_,
-                                             ctl_.get(), first ? it0_.get() : nullptr);
+    sweep_launch(strict_, geo(), q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
+                 first ? it0_.get() : nullptr, st_);
   }
   void launch_flux(int a, int b, bool stamp) {
     FluxArgs fa;
@@ -1535,8 +1605,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
       k_qvar<<<blocks, 256, 0, st>>>(g, d.prim(), d.q_buf(0), d.gas(), d.dctl());
       break;
     case Op::q_derivatives:
-      k_sweep<<<sweep_grid(n), 256, 0, st>>>(g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(),
-                                             nullptr);
+      sweep_launch(spec.fp_mode == 1, g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(), nullptr, st);
       break;
     case Op::publish:
       ck(cudaMemcpyAsync(d.dq_buf(1), scratch, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D scratch");

@@ -156,18 +156,19 @@ __global__ void k_qvar(Geo g, const D4* prim, D4* q, Gas gas, Ctl* ctl) {
   ktimer_end(ctl, KT_QVAR, nullptr);
 }
 
-// One Jacobi sweep of the derivative system (kernels.cpp:82-106): bitwise
-// equal to the reference (exact operation sequence, ascending stencil order).
-__global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
-                                               const D4* __restrict__ dq_in,
-                                               D4* __restrict__ dq_out, Gas gas, Ctl* ctl,
-                                               unsigned long long* iter_t0) {
+// One Jacobi sweep of the derivative system (kernels.cpp:82-106).  S = true
+// (fp_mode strict): bitwise equal to the reference (exact operation sequence,
+// ascending stencil order).  S = false: the same sums with FMA contraction.
+template <bool S, int MB>
+__global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__ q,
+                                                   const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
+                                                   Gas gas, Ctl* ctl, unsigned long long* iter_t0) {
+  using A = Ar<S>;
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_SWEEP);
   if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n;
-       i += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n; i += gridDim.x * blockDim.x) {
     const double2 pi = g.xy[i];
     const D4 qi = ld4(q + i), qxi = ld4(dq_in + 2 * i), qyi = ld4(dq_in + 2 * i + 1);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
@@ -179,30 +180,30 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, const D4* __restrict__ q,
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
       const D4 qn = ld4(q + nb), qxn = ld4(dq_in + 2 * nb), qyn = ld4(dq_in + 2 * nb + 1);
-      sxx = X::add(sxx, X::mul(dx, dx));
-      sxy = X::add(sxy, X::mul(dx, dy));
-      syy = X::add(syy, X::mul(dy, dy));
+      sxx = A::add(sxx, A::mul(dx, dx));
+      sxy = A::add(sxy, A::mul(dx, dy));
+      syy = A::add(syy, A::mul(dy, dy));
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const double df = X::sub(corrected<true>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy),
-                                 corrected<true>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy));
-        bx[c] = X::add(bx[c], X::mul(dx, df));
-        by[c] = X::add(by[c], X::mul(dy, df));
+        const double df = X::sub(corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy),
+                                 corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy));
+        bx[c] = A::add(bx[c], A::mul(dx, df));
+        by[c] = A::add(by[c], A::mul(dy, df));
       }
     }
-    const double det = X::sub(X::mul(sxx, syy), X::mul(sxy, sxy));
+    const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
     if (!(det > gas.det_tol)) {
       raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0));
     } else {
       D4 fx, fy;
-      fx.a = X::sub(X::mul(syy, bx[0]), X::mul(sxy, by[0])) / det;
-      fx.b = X::sub(X::mul(syy, bx[1]), X::mul(sxy, by[1])) / det;
-      fx.c = X::sub(X::mul(syy, bx[2]), X::mul(sxy, by[2])) / det;
-      fx.d = X::sub(X::mul(syy, bx[3]), X::mul(sxy, by[3])) / det;
-      fy.a = X::sub(X::mul(sxx, by[0]), X::mul(sxy, bx[0])) / det;
-      fy.b = X::sub(X::mul(sxx, by[1]), X::mul(sxy, bx[1])) / det;
-      fy.c = X::sub(X::mul(sxx, by[2]), X::mul(sxy, bx[2])) / det;
-      fy.d = X::sub(X::mul(sxx, by[3]), X::mul(sxy, bx[3])) / det;
+      fx.a = A::sub(A::mul(syy, bx[0]), A::mul(sxy, by[0])) / det;
+      fx.b = A::sub(A::mul(syy, bx[1]), A::mul(sxy, by[1])) / det;
+      fx.c = A::sub(A::mul(syy, bx[2]), A::mul(sxy, by[2])) / det;
+      fx.d = A::sub(A::mul(syy, bx[3]), A::mul(sxy, by[3])) / det;
+      fy.a = A::sub(A::mul(sxx, by[0]), A::mul(sxy, bx[0])) / det;
+      fy.b = A::sub(A::mul(sxx, by[1]), A::mul(sxy, bx[1])) / det;
+      fy.c = A::sub(A::mul(sxx, by[2]), A::mul(sxy, bx[2])) / det;
+      fy.d = A::sub(A::mul(sxx, by[3]), A::mul(sxy, bx[3])) / det;
       st4(dq_out + 2 * i, fx);
       st4(dq_out + 2 * i + 1, fy);
     }
@@ -477,6 +478,145 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
     __syncthreads();  // terms/records/staging are reused by later groups
   }
   if constexpr (STAGED) cp_async_wait<0>();
+  __syncthreads();
+  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+}
+
+// Flux residual, one lane per (pair, state): 16 lanes per point, lanes 2j and
+// 2j+1 evaluate the own-point and the neighbour state of pair j (each state's
+// reconstruction, erf/exp and split fluxes), and the pair's Delta G is formed
+// with one register shuffle.  Half the per-thread state of k_flux, twice the
+// resident warps.  Same arithmetic per value, same accumulation order.
+template <bool S, int MB>
+__global__ void __launch_bounds__(256, MB) k_flux_split(FluxArgs a) {
+  constexpr int W = 16, P = 16, JMAX = 8;
+  using A = Ar<S>;
+  extern __shared__ double smem[];
+  double* terms = smem + static_cast<size_t>(P) * a.stride;  // [P][16]
+  __shared__ int s_skip;
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+
+  ktimer_begin(a.ctl, KT_FLUX);
+  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
+  __syncthreads();
+  const int lane = threadIdx.x % W;
+  const int slot = threadIdx.x / W;
+  const int jj = lane >> 1, side = lane & 1;
+  const Geo& g = a.g;
+  PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
+  const int groups = (g.n + P - 1) / P;
+  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x) {
+    const int i = grp * P + slot;
+    const bool live = i < g.n && g.kind[i] != KIND_OUTER;
+    int k = 0, e0 = 0;
+    if (live) stencil_of(g, i, e0, k);
+    // uniform trip count across the warp (the pair shuffles need every lane)
+    const int kwarp = __reduce_max_sync(kFull, max((k + JMAX - 1) / JMAX * JMAX, JMAX));
+    // ---- phase A ----
+    for (int j = jj; j < kwarp; j += JMAX) {
+      const bool act = live && j < k;
+      double dx = 0.0, dy = 0.0;
+      D4 qs{0.0, 0.0, 0.0, -1.0}, qxs{0.0, 0.0, 0.0, 0.0}, qys{0.0, 0.0, 0.0, 0.0};
+      if (act) {
+        const int nb = g.nbr[e0 + j];
+        const double2 pi = g.xy[i], pn = g.xy[nb];
+        dx = X::sub(pn.x, pi.x);
+        dy = X::sub(pn.y, pi.y);
+        const int src = side ? nb : i;
+        qs = ld4(a.q + src);
+        qxs = ld4(a.dq + 2 * src);
+        qys = ld4(a.dq + 2 * src + 1);
+      }
+      double t[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) t[c] = corrected<S>(comp(qs, c), comp(qxs, c), comp(qys, c), dx, dy);
+      FluxState f;
+      bool ok = t[3] < 0.0;
+      if (ok) ok = reconstruct<S>(t, a.gas, f);
+      const bool pair_ok = __shfl_xor_sync(kFull, ok ? 1 : 0, 1) && ok;
+      if (act && !pair_ok && side == 0)
+        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j));
+      if (!pair_ok) {  // keep the state finite; this pair's results are never used
+        f.rho = 1.0; f.u1 = 0.0; f.u2 = 0.0; f.p = 1.0; f.sb = 1.0; f.inv2s = 0.28209479177387814; f.e = 2.5;
+      }
+      AxisTerms at[2];
+      axis_terms2<S>(f, at);
+      const bool xplus = dx <= 0.0, yplus = dy <= 0.0;
+      double gx[4], gy[4];
+      split_flux<S>(f, at[0], 0, !xplus, gx);
+      split_flux<S>(f, at[1], 1, !yplus, gy);
+      PairRec& r = my[j];
+      const bool write = act && pair_ok && side == 1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double ox = __shfl_xor_sync(kFull, gx[c], 1);
+        const double oy = __shfl_xor_sync(kFull, gy[c], 1);
+        if (write) {
+          r.dg[xplus ? 0 : 1][c] = X::sub(gx[c], ox);
+          r.dg[yplus ? 2 : 3][c] = X::sub(gy[c], oy);
+        }
+      }
+      if (write) {
+        r.dx = dx;
+        r.dy = dy;
+      }
+      // a zero offset belongs to both half stencils: also the minus direction
+      const bool xz = act && dx == 0.0, yz = act && dy == 0.0;
+      if (__any_sync(kFull, xz || yz)) {
+        split_flux<S>(f, at[0], 0, true, gx);
+        split_flux<S>(f, at[1], 1, true, gy);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double ox = __shfl_xor_sync(kFull, gx[c], 1);
+          const double oy = __shfl_xor_sync(kFull, gy[c], 1);
+          if (write && xz) r.dg[1][c] = X::sub(gx[c], ox);
+          if (write && yz) r.dg[3][c] = X::sub(gy[c], oy);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- phase B: ordered least-squares sums + 2x2 solve, lane = (direction, component) ----
+    if (live) {
+      const int d = lane >> 2, c0 = lane & 3;
+      if (a.mask & (1 << d)) {
+        double sxx = 0.0, sxy = 0.0, syy = 0.0, bx = 0.0, by = 0.0;
+        for (int j = 0; j < k; ++j) {
+          const double dx = my[j].dx, dy = my[j].dy;
+          const double dd = d < 2 ? dx : dy;
+          const bool member = (d & 1) ? dd >= 0.0 : dd <= 0.0;
+          if (!member) continue;
+          sxx = A::add(sxx, A::mul(dx, dx));
+          sxy = A::add(sxy, A::mul(dx, dy));
+          syy = A::add(syy, A::mul(dy, dy));
+          const double df = my[j].dg[d][c0];
+          bx = A::add(bx, A::mul(dx, df));
+          by = A::add(by, A::mul(dy, df));
+        }
+        const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
+        if (!(det > a.gas.det_tol)) {
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot));
+        } else {
+          terms[slot * 16 + d * 4 + c0] = d < 2 ? A::sub(A::mul(syy, bx), A::mul(sxy, by)) / det
+                                                : A::sub(A::mul(sxx, by), A::mul(sxy, bx)) / det;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 * P) {
+      const int sl = threadIdx.x >> 2, c = threadIdx.x & 3;
+      const int ip = grp * P + sl;
+      if (ip < g.n && g.kind[ip] != KIND_OUTER) {
+        double* rp = reinterpret_cast<double*>(a.res + ip) + c;
+        double acc = a.first ? 0.0 : *rp;
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+          if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
+        *rp = acc;
+      }
+    }
+    __syncthreads();
+  }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
 }
