@@ -133,14 +133,13 @@ std::size_t flux_smem_bytes(int W, int kcap) {
   return (static_cast<std::size_t>(P) * flux_stride(kcap) + static_cast<std::size_t>(P) * 16) * sizeof(double);
 }
 
-template <int W, bool S, int MB, bool ST>
+template <int W, bool S, int MB>
 void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
-  if (ST) smem += flux_stage_bytes(W, flux_points_per_block(W));
   static std::size_t configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > configured[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux<W, S, MB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_flux<W, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux)");
     configured[dev & 63] = smem;
@@ -149,12 +148,12 @@ void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
   static int resident[64] = {};
   if (!resident[dev & 63]) {
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux<W, S, MB, ST>, W * P, smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux<W, S, MB>, W * P, smem), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int groups = (a.g.n + P - 1) / P;
-  k_flux<W, S, MB, ST><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
+  k_flux<W, S, MB><<<std::max(1, std::min(groups, resident[dev & 63])), W * P, smem, st>>>(a);
 }
 
 // Derivative sweep launch: strict (bitwise) or FMA variant, resident blocks per
@@ -209,72 +208,16 @@ int flux_min_blocks() {
   return mb;
 }
 
-// Gather staging (cp.async) for uniform stencils: opt-in (LSKUM_FLUX_STAGE=1);
-// measured slower so far (shared-memory footprint limits residency).
-bool flux_staging() {
-  static bool on = [] {
-    const char* e = std::getenv("LSKUM_FLUX_STAGE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-// Lane-per-state flux kernel (k_flux_split) for stencils of <= 8 neighbours:
-// LSKUM_FLUX_SPLIT = 1 (default) | 0, resident blocks LSKUM_FLUX_SPLIT_MB = 3 | 4.
-int flux_split_mode() {
-  static int m = [] {
-    const char* e = std::getenv("LSKUM_FLUX_SPLIT");
-    const char* b = std::getenv("LSKUM_FLUX_SPLIT_MB");
-    if (e && e[0] == '0') return 0;
-    return (b && b[0] == '4') ? 4 : 3;
-  }();
-  return m;
-}
-
-template <bool S, int MB>
-void flux_split_launch_t(FluxArgs a, cudaStream_t st) {
-  constexpr int P = 16;
-  a.stride = flux_stride(a.kcap);
-  const std::size_t smem = (static_cast<std::size_t>(P) * a.stride + P * 16) * sizeof(double);
-  static std::size_t configured[64] = {};
-  static int resident[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (smem > configured[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux_split<S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-       "cudaFuncSetAttribute(k_flux_split)");
-    configured[dev & 63] = smem;
-    resident[dev & 63] = 0;
-  }
-  if (!resident[dev & 63]) {
-    int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_split<S, MB>, 256, smem), "occupancy");
-    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-    resident[dev & 63] = std::max(1, per_sm) * sms;
-  }
-  const int groups = (a.g.n + P - 1) / P;
-  k_flux_split<S, MB><<<std::max(1, std::min(groups, resident[dev & 63])), 256, smem, st>>>(a);
-}
-
 template <bool S>
 void flux_launch_s(int W, const FluxArgs& a, std::size_t smem, cudaStream_t st) {
-  if (W == 8 && flux_split_mode() && a.kcap <= 8) {
-    if (flux_split_mode() == 4) flux_split_launch_t<S, 4>(a, st);
-    else flux_split_launch_t<S, 3>(a, st);
-    return;
-  }
   if (W == 8) {
-    if (flux_staging() && a.g.kfix > 0 && a.g.kfix <= 8) {
-      flux_launch_t<8, S, 2, true>(a, smem, st);
-      return;
-    }
     const int mb = flux_min_blocks();
-    if (mb == 2) flux_launch_t<8, S, 2, false>(a, smem, st);
-    else flux_launch_t<8, S, 3, false>(a, smem, st);
+    if (mb == 2) flux_launch_t<8, S, 2>(a, smem, st);
+    else flux_launch_t<8, S, 3>(a, smem, st);
   } else if (W == 16) {
-    flux_launch_t<16, S, 2, false>(a, smem, st);
+    flux_launch_t<16, S, 2>(a, smem, st);
   } else {
-    flux_launch_t<32, S, 1, false>(a, smem, st);
+    flux_launch_t<32, S, 1>(a, smem, st);
   }
 }
 

@@ -226,30 +226,6 @@ struct PairRec {
   double dg[4][4];  // Delta G for Gx+, Gx-, Gy+, Gy- (only member directions valid)
 };
 
-// Staged neighbour data for one lane (cp.async, 7 x 16 B).
-struct alignas(16) Gathered {
-  double2 xy;
-  D4 q, qx, qy;
-};
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__device__ __forceinline__ void stage_point(Gathered* dst, const double2* xy, const D4* q, const D4* dq, int p) {
-  cp_async16(&dst->xy, xy + p);
-  cp_async16(&dst->q, q + p);
-  cp_async16(reinterpret_cast<char*>(&dst->q) + 16, reinterpret_cast<const char*>(q + p) + 16);
-  const char* d = reinterpret_cast<const char*>(dq + 2 * p);
-  char* o = reinterpret_cast<char*>(&dst->qx);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) cp_async16(o + 16 * k, d + 16 * k);
-}
-
 struct FluxArgs {
   Geo g;
   Gas gas;
@@ -264,11 +240,6 @@ struct FluxArgs {
   int first;      // zero the accumulator before adding
 };
 
-// Shared-memory bytes of the gather staging area (two buffers of P points x
-// (W neighbours + the point itself)).
-__host__ __device__ constexpr int flux_stage_bytes(int W, int P) {
-  return 2 * P * (W + 1) * static_cast<int>(sizeof(Gathered));
-}
 
 __host__ __device__ constexpr int flux_points_per_block(int W) { return W >= 32 ? 8 : (W >= 16 ? 16 : 32); }
 
@@ -280,14 +251,19 @@ __host__ __device__ inline int flux_stride(int kcap) {
   return s;
 }
 
-// STAGED (uniform stencils with k <= W): the neighbour and own-point records
-// of the next group are copied into shared memory with cp.async while the
-// current group computes, hiding the dependent index -> gather latency.
-template <int W, bool S, int MB, bool STAGED>
+// Phase A is convergent: every lane of a warp runs the same instruction
+// stream (inactive lanes evaluate their own point with zero offsets and store
+// nothing), so constant tables go through the uniform datapath and no lane
+// waits on another's branch.  Each pair evaluates one x and one y split flux,
+// with the sign chosen per lane (the half stencil the neighbour falls in); a
+// zero offset also needs the other sign, handled in a rarely taken
+// warp-uniform branch.
+template <int W, bool S, int MB>
 __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxArgs a) {
   constexpr int P = flux_points_per_block(W);
   constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
   constexpr int NC = 16 / NOWN;                 // components per owning lane
+  constexpr unsigned kFull = 0xFFFFFFFFu;
   using A = Ar<S>;
   extern __shared__ double smem[];
   double* terms = smem + static_cast<size_t>(P) * a.stride;  // [P][16]
@@ -301,119 +277,69 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
   const Geo& g = a.g;
   PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
   const int groups = (g.n + P - 1) / P;
-  Gathered* stage = reinterpret_cast<Gathered*>(terms + P * 16);  // [2][P * (W + 1)]
-  // index of this lane's neighbour in group G (-1 if none)
-  auto next_index = [&](int G) {
-    const int ip = G * P + slot;
-    return (G < groups && ip < g.n && lane < g.kfix) ? g.nbr[ip * g.kfix + lane] : -1;
-  };
-  auto stage_group = [&](int G, int buf, int nb) {
-    Gathered* base = stage + buf * P * (W + 1);
-    const int ip = G * P + slot;
-    if (G < groups && ip < g.n) {
-      if (nb >= 0) stage_point(base + threadIdx.x, g.xy, a.q, a.dq, nb);
-      if (lane == 0) stage_point(base + P * W + slot, g.xy, a.q, a.dq, ip);
-    }
-    cp_async_commit();
-  };
-  int nb_next = -1;
-  if constexpr (STAGED) {
-    if (!s_skip) {
-      stage_group(blockIdx.x, 0, next_index(blockIdx.x));
-      nb_next = next_index(blockIdx.x + gridDim.x);
-    }
-  }
   // Persistent blocks: one resident block per slot walks groups of P points,
   // amortising the start-up latency and the timer atomics.
-  int t = 0;
-  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x, ++t) {
+  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x) {
     const int i = grp * P + slot;
-    if constexpr (STAGED) {
-      stage_group(grp + gridDim.x, (t + 1) & 1, nb_next);
-      nb_next = next_index(grp + 2 * gridDim.x);
-      cp_async_wait<1>();
-      __syncthreads();
-    }
-    const bool live = i < g.n && g.kind[i] != KIND_OUTER;
+    const int ic = i < g.n ? i : g.n - 1;  // clamped for loads
+    const bool live = i < g.n && g.kind[ic] != KIND_OUTER;
     int k = 0, e0 = 0;
     if (live) stencil_of(g, i, e0, k);
+    const int kwarp = __reduce_max_sync(kFull, k);
 
     // ---- phase A: one lane per (point, neighbour) pair ----
-    if (live) {
-      double2 pi;
-      D4 qi, qxi, qyi;
-      if constexpr (STAGED) {
-        const Gathered& o = stage[(t & 1) * P * (W + 1) + P * W + slot];
-        pi = o.xy;
-        qi = o.q;
-        qxi = o.qx;
-        qyi = o.qy;
-      } else {
-        pi = g.xy[i];
-        qi = ld4(a.q + i);
-        qxi = ld4(a.dq + 2 * i);
-        qyi = ld4(a.dq + 2 * i + 1);
+    const double2 pi = g.xy[ic];
+    const D4 qi = ld4(a.q + ic), qxi = ld4(a.dq + 2 * ic), qyi = ld4(a.dq + 2 * ic + 1);
+    for (int jb = 0; jb < kwarp; jb += W) {
+      const int j = jb + lane;
+      const bool act = live && j < k;
+      const int nb = act ? g.nbr[e0 + j] : ic;
+      const double2 pn = g.xy[nb];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+      double ti[4], tn[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
+        tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
       }
-      for (int j = lane; j < k; j += W) {
-        const int nb = g.nbr[e0 + j];
-        double2 pn;
-        D4 qn, qxn, qyn;
-        if constexpr (STAGED) {
-          const Gathered& o = stage[(t & 1) * P * (W + 1) + threadIdx.x];
-          pn = o.xy;
-          qn = o.q;
-          qxn = o.qx;
-          qyn = o.qy;
-        } else {
-          pn = g.xy[nb];
-          qn = ld4(a.q + nb);
-          qxn = ld4(a.dq + 2 * nb);
-          qyn = ld4(a.dq + 2 * nb + 1);
-        }
-        const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-        PairRec& r = my[j];
+      bool ok = ti[3] < 0.0 && tn[3] < 0.0;
+      if (!ok) {  // q3 >= 0 has no state: evaluate a dummy one, store nothing
+        ti[3] = -1.0;
+        tn[3] = -1.0;
+      }
+      FluxState fi, fn;
+      ok = reconstruct2<S>(ti, tn, a.gas, fi, fn) && ok;
+      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j));
+      AxisTerms at[4];
+      axis_terms4<S>(fi, fn, at);
+      const bool store = act && ok;
+      const bool xplus = dx <= 0.0, yplus = dy <= 0.0;
+      PairRec& r = my[j < a.kcap ? j : 0];
+      double gi[4], gn[4];
+      split_flux<S>(fi, at[0], 0, !xplus, gi);
+      split_flux<S>(fn, at[1], 0, !xplus, gn);
+      if (store) {
         r.dx = dx;
         r.dy = dy;
-        const unsigned dfirst = dx <= 0.0 ? 0u : 1u;
-        double ti[4], tn[4];
-  #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
-          tn[c] = corrected<S>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
-        }
-        if (!(ti[3] < 0.0) || !(tn[3] < 0.0)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dfirst, j));
-          continue;
-        }
-        FluxState fi, fn;
-        if (!reconstruct2<S>(ti, tn, a.gas, fi, fn)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dfirst, j));
-          continue;
-        }
-        const bool xp = dx <= 0.0 && (a.mask & 1), xm = dx >= 0.0 && (a.mask & 2);
-        const bool yp = dy <= 0.0 && (a.mask & 4), ym = dy >= 0.0 && (a.mask & 8);
-        AxisTerms at[4];
-        axis_terms4<S>(fi, fn, at);
-        double gi[4], gn[4];
-        if (xp) {
-          split_flux<S>(fi, at[0], 0, false, gi);
-          split_flux<S>(fn, at[1], 0, false, gn);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[0][c] = X::sub(gn[c], gi[c]);
-        }
-        if (xm) {
+        for (int c = 0; c < 4; ++c) r.dg[xplus ? 0 : 1][c] = X::sub(gn[c], gi[c]);
+      }
+      split_flux<S>(fi, at[2], 1, !yplus, gi);
+      split_flux<S>(fn, at[3], 1, !yplus, gn);
+      if (store) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r.dg[yplus ? 2 : 3][c] = X::sub(gn[c], gi[c]);
+      }
+      // a zero offset belongs to both half stencils: add the minus direction
+      if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
+        if (store && dx == 0.0) {
           split_flux<S>(fi, at[0], 0, true, gi);
           split_flux<S>(fn, at[1], 0, true, gn);
 #pragma unroll
           for (int c = 0; c < 4; ++c) r.dg[1][c] = X::sub(gn[c], gi[c]);
         }
-        if (yp) {
-          split_flux<S>(fi, at[2], 1, false, gi);
-          split_flux<S>(fn, at[3], 1, false, gn);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) r.dg[2][c] = X::sub(gn[c], gi[c]);
-        }
-        if (ym) {
+        if (store && dy == 0.0) {
           split_flux<S>(fi, at[2], 1, true, gi);
           split_flux<S>(fn, at[3], 1, true, gn);
 #pragma unroll
@@ -429,7 +355,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
       const int c0 = (lane % (4 / NC)) * NC;        // first component owned
       if (a.mask & (1 << d)) {
         double sxx = 0.0, sxy = 0.0, syy = 0.0, bx[NC], by[NC];
-  #pragma unroll
+#pragma unroll
         for (int cc = 0; cc < NC; ++cc) bx[cc] = by[cc] = 0.0;
         for (int j = 0; j < k; ++j) {
           const double dx = my[j].dx, dy = my[j].dy;
@@ -439,7 +365,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
           sxx = A::add(sxx, A::mul(dx, dx));
           sxy = A::add(sxy, A::mul(dx, dy));
           syy = A::add(syy, A::mul(dy, dy));
-  #pragma unroll
+#pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
             const double df = my[j].dg[d][c0 + cc];
             bx[cc] = A::add(bx[cc], A::mul(dx, df));
@@ -450,7 +376,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
         if (!(det > a.gas.det_tol)) {
           raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot));
         } else {
-  #pragma unroll
+#pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
             const double t = d < 2 ? A::sub(A::mul(syy, bx[cc]), A::mul(sxy, by[cc])) / det
                                    : A::sub(A::mul(sxx, by[cc]), A::mul(sxy, bx[cc])) / det;
@@ -469,153 +395,13 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
       if (ip < g.n && g.kind[ip] != KIND_OUTER) {
         double* rp = reinterpret_cast<double*>(a.res + ip) + c;
         double acc = a.first ? 0.0 : *rp;
-  #pragma unroll
-        for (int d = 0; d < 4; ++d)
-          if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
-        *rp = acc;
-      }
-    }
-    __syncthreads();  // terms/records/staging are reused by later groups
-  }
-  if constexpr (STAGED) cp_async_wait<0>();
-  __syncthreads();
-  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
-}
-
-// Flux residual, one lane per (pair, state): 16 lanes per point, lanes 2j and
-// 2j+1 evaluate the own-point and the neighbour state of pair j (each state's
-// reconstruction, erf/exp and split fluxes), and the pair's Delta G is formed
-// with one register shuffle.  Half the per-thread state of k_flux, twice the
-// resident warps.  Same arithmetic per value, same accumulation order.
-template <bool S, int MB>
-__global__ void __launch_bounds__(256, MB) k_flux_split(FluxArgs a) {
-  constexpr int W = 16, P = 16, JMAX = 8;
-  using A = Ar<S>;
-  extern __shared__ double smem[];
-  double* terms = smem + static_cast<size_t>(P) * a.stride;  // [P][16]
-  __shared__ int s_skip;
-  constexpr unsigned kFull = 0xFFFFFFFFu;
-
-  ktimer_begin(a.ctl, KT_FLUX);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
-  __syncthreads();
-  const int lane = threadIdx.x % W;
-  const int slot = threadIdx.x / W;
-  const int jj = lane >> 1, side = lane & 1;
-  const Geo& g = a.g;
-  PairRec* my = reinterpret_cast<PairRec*>(smem + static_cast<size_t>(slot) * a.stride);
-  const int groups = (g.n + P - 1) / P;
-  for (int grp = blockIdx.x; !s_skip && grp < groups; grp += gridDim.x) {
-    const int i = grp * P + slot;
-    const bool live = i < g.n && g.kind[i] != KIND_OUTER;
-    int k = 0, e0 = 0;
-    if (live) stencil_of(g, i, e0, k);
-    // uniform trip count across the warp (the pair shuffles need every lane)
-    const int kwarp = __reduce_max_sync(kFull, max((k + JMAX - 1) / JMAX * JMAX, JMAX));
-    // ---- phase A ----
-    for (int j = jj; j < kwarp; j += JMAX) {
-      const bool act = live && j < k;
-      double dx = 0.0, dy = 0.0;
-      D4 qs{0.0, 0.0, 0.0, -1.0}, qxs{0.0, 0.0, 0.0, 0.0}, qys{0.0, 0.0, 0.0, 0.0};
-      if (act) {
-        const int nb = g.nbr[e0 + j];
-        const double2 pi = g.xy[i], pn = g.xy[nb];
-        dx = X::sub(pn.x, pi.x);
-        dy = X::sub(pn.y, pi.y);
-        const int src = side ? nb : i;
-        qs = ld4(a.q + src);
-        qxs = ld4(a.dq + 2 * src);
-        qys = ld4(a.dq + 2 * src + 1);
-      }
-      double t[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) t[c] = corrected<S>(comp(qs, c), comp(qxs, c), comp(qys, c), dx, dy);
-      FluxState f;
-      bool ok = t[3] < 0.0;
-      if (ok) ok = reconstruct<S>(t, a.gas, f);
-      const bool pair_ok = __shfl_xor_sync(kFull, ok ? 1 : 0, 1) && ok;
-      if (act && !pair_ok && side == 0)
-        raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j));
-      if (!pair_ok) {  // keep the state finite; this pair's results are never used
-        f.rho = 1.0; f.u1 = 0.0; f.u2 = 0.0; f.p = 1.0; f.sb = 1.0; f.inv2s = 0.28209479177387814; f.e = 2.5;
-      }
-      AxisTerms at[2];
-      axis_terms2<S>(f, at);
-      const bool xplus = dx <= 0.0, yplus = dy <= 0.0;
-      double gx[4], gy[4];
-      split_flux<S>(f, at[0], 0, !xplus, gx);
-      split_flux<S>(f, at[1], 1, !yplus, gy);
-      PairRec& r = my[j];
-      const bool write = act && pair_ok && side == 1;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double ox = __shfl_xor_sync(kFull, gx[c], 1);
-        const double oy = __shfl_xor_sync(kFull, gy[c], 1);
-        if (write) {
-          r.dg[xplus ? 0 : 1][c] = X::sub(gx[c], ox);
-          r.dg[yplus ? 2 : 3][c] = X::sub(gy[c], oy);
-        }
-      }
-      if (write) {
-        r.dx = dx;
-        r.dy = dy;
-      }
-      // a zero offset belongs to both half stencils: also the minus direction
-      const bool xz = act && dx == 0.0, yz = act && dy == 0.0;
-      if (__any_sync(kFull, xz || yz)) {
-        split_flux<S>(f, at[0], 0, true, gx);
-        split_flux<S>(f, at[1], 1, true, gy);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double ox = __shfl_xor_sync(kFull, gx[c], 1);
-          const double oy = __shfl_xor_sync(kFull, gy[c], 1);
-          if (write && xz) r.dg[1][c] = X::sub(gx[c], ox);
-          if (write && yz) r.dg[3][c] = X::sub(gy[c], oy);
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- phase B: ordered least-squares sums + 2x2 solve, lane = (direction, component) ----
-    if (live) {
-      const int d = lane >> 2, c0 = lane & 3;
-      if (a.mask & (1 << d)) {
-        double sxx = 0.0, sxy = 0.0, syy = 0.0, bx = 0.0, by = 0.0;
-        for (int j = 0; j < k; ++j) {
-          const double dx = my[j].dx, dy = my[j].dy;
-          const double dd = d < 2 ? dx : dy;
-          const bool member = (d & 1) ? dd >= 0.0 : dd <= 0.0;
-          if (!member) continue;
-          sxx = A::add(sxx, A::mul(dx, dx));
-          sxy = A::add(sxy, A::mul(dx, dy));
-          syy = A::add(syy, A::mul(dy, dy));
-          const double df = my[j].dg[d][c0];
-          bx = A::add(bx, A::mul(dx, df));
-          by = A::add(by, A::mul(dy, df));
-        }
-        const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
-        if (!(det > a.gas.det_tol)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot));
-        } else {
-          terms[slot * 16 + d * 4 + c0] = d < 2 ? A::sub(A::mul(syy, bx), A::mul(sxy, by)) / det
-                                                : A::sub(A::mul(sxx, by), A::mul(sxy, bx)) / det;
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 4 * P) {
-      const int sl = threadIdx.x >> 2, c = threadIdx.x & 3;
-      const int ip = grp * P + sl;
-      if (ip < g.n && g.kind[ip] != KIND_OUTER) {
-        double* rp = reinterpret_cast<double*>(a.res + ip) + c;
-        double acc = a.first ? 0.0 : *rp;
 #pragma unroll
         for (int d = 0; d < 4; ++d)
           if (a.mask & (1 << d)) acc = X::add(acc, terms[sl * 16 + d * 4 + c]);
         *rp = acc;
       }
     }
-    __syncthreads();
+    __syncthreads();  // terms/records are reused by the next group
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
