@@ -197,13 +197,13 @@ void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* d
   }
 }
 
-// Register/occupancy trade-off of the unstaged W=8 kernel: minimum resident
-// blocks per SM (LSKUM_FLUX_MINB = 2 | 3, default 3).
+// Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per
+// SM (LSKUM_FLUX_MINB = 2 | 3, default 2: 128 registers, no spills).
 int flux_min_blocks() {
   static int mb = [] {
     const char* e = std::getenv("LSKUM_FLUX_MINB");
-    const int v = e ? std::atoi(e) : 3;
-    return (v >= 2 && v <= 4) ? v : 3;
+    const int v = e ? std::atoi(e) : 2;
+    return (v >= 2 && v <= 3) ? v : 2;
   }();
   return mb;
 }

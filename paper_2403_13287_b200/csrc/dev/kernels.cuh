@@ -349,6 +349,12 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
     }
     __syncthreads();
 
+    // next group's stencil entry for this lane: its neighbour records are
+    // prefetched into L2 after phase B so the next gathers hit L2
+    const int i_next = (grp + gridDim.x) * P + slot;
+    const bool pf = g.kfix > 0 && lane < g.kfix && i_next < g.n;
+    const int nb_next = pf ? g.nbr[i_next * g.kfix + lane] : 0;
+
     // ---- phase B: ordered least-squares sums + 2x2 solve per direction ----
     if (live && lane < NOWN) {
       const int d = lane / (4 / NC);                // direction owned
@@ -383,6 +389,15 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
             terms[slot * 16 + d * 4 + c0 + cc] = t;
           }
         }
+      }
+    }
+    if (pf) {
+      prefetch_l2(g.xy + nb_next);
+      prefetch_l2(a.q + nb_next);
+      prefetch_l2(a.dq + 2 * nb_next);
+      if (lane == 0) {
+        prefetch_l2(a.q + i_next);
+        prefetch_l2(a.dq + 2 * i_next);
       }
     }
     __syncthreads();
