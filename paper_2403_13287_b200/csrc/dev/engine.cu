@@ -313,11 +313,11 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
 // the domain that owns it) resets that word.
 __global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter) {
   ctl->sh = sh;
+  ctl->diag_iter = diag_iter;
   if (own_shared) {
     sh->err_key = kNoErr;
     sh->err_iter = 0x7FFFFFFF;
     sh->iter = 0;
-    sh->diag_iter = diag_iter;
   }
   for (int k = 0; k < KT_COUNT; ++k) {
     ctl->kt[k].t0 = ~0ull;
@@ -328,7 +328,7 @@ __global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter) 
   }
 }
 
-__global__ void k_set_diag(Shared* sh, int diag_iter) { sh->diag_iter = diag_iter; }
+__global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter; }
 
 // Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
 // major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
@@ -426,8 +426,11 @@ GeomView view_of(const PointSet& ps, const std::vector<std::uint8_t>& part) {
 
 class Domain {
  public:
-  Domain(const GeomView& gv, int device, double gamma, double cfl, double det_tol, int capacity)
-      : n_(gv.n_own), n_loc_(gv.n_loc), device_(device), stream_holder_(device) {
+  // ipc: buffers that peers read (q, dq, the shared word, the residue array)
+  // come from plain cudaMalloc so they can be exported as CUDA IPC handles.
+  Domain(const GeomView& gv, int device, double gamma, double cfl, double det_tol, int capacity,
+         bool ipc = false)
+      : n_(gv.n_own), n_loc_(gv.n_loc), device_(device), ipc_(ipc), stream_holder_(device) {
     st_ = stream_holder_.st;
     ck(cudaEventCreate(&ev0_), "cudaEventCreate");
     ck(cudaEventCreate(&ev1_), "cudaEventCreate");
@@ -500,11 +503,12 @@ class Domain {
       ck(cudaMemcpyAsync(gid_.get(), hgid, b_gid, cudaMemcpyHostToDevice, st_), "H2D gid");
     }
     // state: q / dq carry halo slots; prim covers them for the first q_variables
+    cudaStream_t shared_st = ipc ? nullptr : st_;
     prim_.alloc(nl, st_);
-    q_[0].alloc(nl, st_);
-    q_[1].alloc(nl, st_);
-    dq_[0].alloc(2 * nl, st_);
-    dq_[1].alloc(2 * nl, st_);
+    q_[0].alloc(nl, shared_st);
+    q_[1].alloc(nl, shared_st);
+    dq_[0].alloc(2 * nl, shared_st);
+    dq_[1].alloc(2 * nl, shared_st);
     res_.alloc(n, st_);
     dt_.alloc(n, st_);
     which_.alloc(n, st_);
@@ -513,7 +517,7 @@ class Domain {
     pval_.alloc(1024, st_);
     psz_.alloc(1024, st_);
     ctl_.alloc(1, st_);
-    sh_.alloc(1, st_);
+    sh_.alloc(1, shared_st);
     shared_ = sh_.get();
     diag_.alloc(8, st_);
     capacity_ = std::max(capacity, 1);
@@ -565,12 +569,13 @@ class Domain {
   void set_residue_size(long long n_total) {
     n_res_ = n_total;
     d1_ = tree_depth(n_total);
-    if (n_total != n_) {
-      mag_.alloc(static_cast<std::size_t>(n_total), st_);
+    if (n_total != n_ || ipc_) {
+      mag_.alloc(static_cast<std::size_t>(n_total), ipc_ ? nullptr : st_);
       mag_out_ = mag_.get();
     }
   }
   double* mag_buf() { return mag_.get(); }
+  Shared* own_shared() { return sh_.get(); }
   int n_loc() const { return n_loc_; }
   int device() const { return device_; }
   int global_of(int local) const { return gid_host_.empty() ? local : gid_host_[local]; }
@@ -813,7 +818,7 @@ class Domain {
     if (order_ == 2 && ((c * inner_) & 1)) b ^= 1;
   }
 
-  void set_diag(int it) { k_set_diag<<<1, 1, 0, st_>>>(shared_, it); }
+  void set_diag(int it) { k_set_diag<<<1, 1, 0, st_>>>(ctl_.get(), it); }
 
   // Runs up to n iterations; stops early on a device error.  Returns the
   // CUDA-event milliseconds around the enqueued work.
@@ -1022,6 +1027,7 @@ class Domain {
     }
   };
   int n_ = 0, n_loc_ = 0, device_ = 0;
+  bool ipc_ = false;
   long long n_res_ = 0;
   StreamHolder stream_holder_;
   cudaStream_t st_ = nullptr;
@@ -1228,7 +1234,7 @@ class MultiRun {
     }
     for (int d = 0; d < P_; ++d) dom_[d]->upload(ps.fields, false);
     r.reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);
-    ck(cudaStreamSynchronize(r.stream()), "root init");
+    ck(cudaStreamSynchronize(r.stream()), "root init");  // shared word initialised before others use it
     for (int d = 1; d < P_; ++d) dom_[d]->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, false);
     for (int d = 0; d < P_; ++d) dom_[d]->first_q();
     for (int d = 0; d < P_; ++d) ck(cudaStreamSynchronize(dom_[d]->stream()), "first q");
@@ -1264,9 +1270,11 @@ class MultiRun {
   // CUDA-event ms on the root stream, which waits for every domain.
   double iterate(int n) {
     Domain& r = root();
+    for (int d = 0; d < P_; ++d) {
+      ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
+      dom_[d]->set_diag(t_ + n - 1);
+    }
     ck(cudaSetDevice(dev_[0]), "cudaSetDevice");
-    r.set_diag(t_ + n - 1);
-    ck(cudaStreamSynchronize(r.stream()), "set diag");
     ck(cudaEventRecord(t0_, r.stream()), "EventRecord");
     for (int d = 1; d < P_; ++d) wait(d, t0_);  // all domains start after the stamp
     int issued = 0, waited = 0;

@@ -56,13 +56,14 @@ struct Shared {
   unsigned long long err_key;  // min over failures (kNoErr = none)
   int err_iter;                // 0-based iteration of the failure (min)
   int iter;                    // 0-based index of the iteration in flight
-  int diag_iter;               // iteration whose res/dt are kept for copy-back
-  int pad;
+  int pad[2];
 };
 
 // Per-domain control block: the shared word + this domain's kernel timers.
 struct Ctl {
   Shared* sh;
+  int diag_iter;  // iteration whose res/dt are kept for copy-back (this domain)
+  int pad;
   KTimer kt[KT_COUNT];
 };
 
@@ -349,12 +350,6 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
     }
     __syncthreads();
 
-    // next group's stencil entry for this lane: its neighbour records are
-    // prefetched into L2 after phase B so the next gathers hit L2
-    const int i_next = (grp + gridDim.x) * P + slot;
-    const bool pf = g.kfix > 0 && lane < g.kfix && i_next < g.n;
-    const int nb_next = pf ? g.nbr[i_next * g.kfix + lane] : 0;
-
     // ---- phase B: ordered least-squares sums + 2x2 solve per direction ----
     if (live && lane < NOWN) {
       const int d = lane / (4 / NC);                // direction owned
@@ -389,15 +384,6 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
             terms[slot * 16 + d * 4 + c0 + cc] = t;
           }
         }
-      }
-    }
-    if (pf) {
-      prefetch_l2(g.xy + nb_next);
-      prefetch_l2(a.q + nb_next);
-      prefetch_l2(a.dq + 2 * nb_next);
-      if (lane == 0) {
-        prefetch_l2(a.q + i_next);
-        prefetch_l2(a.dq + 2 * i_next);
       }
     }
     __syncthreads();
@@ -445,7 +431,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   const int ip = blockIdx.x * blockDim.x + threadIdx.x;
   const Geo& g = a.g;
   if (!s_skip && ip < g.n) {
-    const bool diag = a.ctl->sh->iter == a.ctl->sh->diag_iter;
+    const bool diag = a.ctl->sh->iter == a.ctl->diag_iter;
     if (g.kind[ip] == KIND_OUTER) {
       st4(a.q_next + ip, ld4(a.q + ip));
       a.mag[gidx(g, ip)] = 0.0;
