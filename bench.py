@@ -282,18 +282,8 @@ def run_b200_arm(a):
     from paper_2403_13287_b200 import lskum as L
     world, rank, local = dist_env()
     gpus = max(a.gpus, world)
-    dist = None
     if world > 1:
-        # One process per GPU is the launch contract; the halo engine drives all
-        # device domains of the run from rank 0 (single process, peer memory over
-        # NVLink).  Other ranks only join the barriers.
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
-        if rank != 0:
-            dist.barrier()
-            dist.barrier()
-            dist.destroy_process_group()
-            return
+        return run_b200_ranks(a, L, world, rank, local)
     # weak scaling: ~160K points per GPU (side grows with sqrt(gpus))
     side = int(round(a.side * math.sqrt(gpus)))
     a.side = side
@@ -304,8 +294,6 @@ def run_b200_arm(a):
     cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
                    iters=a.steps, device=0, gpus=gpus)
     steady_iters = 0
-    if dist is not None:
-        dist.barrier()
     with ClockSampler(0) as clocks:
         sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps + 4000)
         for _ in range(a.warmup):
@@ -391,9 +379,115 @@ def run_b200_arm(a):
     if not a.no_cpu_baseline and gpus == 1:
         out["cpu_baseline"] = cpu_baseline(cloud, a, a.cpu_seconds)
     print(json.dumps(out), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+
+
+def run_b200_ranks(a, L, world, rank, local):
+    """torchrun: one process per GPU, each running its RCB piece (RankSession).
+
+    Halo exchange and the residue tree are device-to-device over CUDA IPC
+    (NVLink peer memory), ordered by device-side progress counters; the gloo
+    group only carries setup, per-step barriers and the max-over-ranks timing.
+    """
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    ndev = max(1, torch.cuda.device_count())
+    device = local % ndev
+    side = int(round(a.side * math.sqrt(world)))
+    a.side, a.gpus = side, world
+    cloud = L.Cloud.generate_rect(side, side, 0.1, 7, 8)
+    n = cloud.n
+    k = cloud.nnz // n
+    n_flux = int(sum(1 for v in cloud.geometry()["kind"] if v != 2))
+    cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
+                   iters=a.steps)
+    step_ms, sweep_ms, flux_ms = [], [], []
+    with ClockSampler(device) as clocks:
+        sess = L.RankSession(cloud, cfg, rank, world, device, capacity=a.warmup + a.steps + 4000)
+        for _ in range(a.warmup):
+            sess.flush_l2()
+            dist.barrier()
+            sess.iterate(1)
+        for _ in range(a.steps):
+            sess.flush_l2()
+            dist.barrier()
+            step_ms.append(sess.iterate(1))
+            sw, fl = sess.event_ms()
+            sweep_ms.append(sw)
+            flux_ms.append(fl)
+        launches = sess.info()["launches_per_iter"]
+        residues = sess.residues()
+        sess.close()
+    # e2e: host arrays -> this rank's piece on its GPU -> K iterations -> copy-back
+    e2e_cloud = L.Cloud.generate_rect(side, side, 0.1, 7, 8)
+    dist.barrier()
+    t0 = time.perf_counter()
+    with L.RankSession(e2e_cloud, cfg, rank, world, device, capacity=a.steps) as es:
+        es.iterate(a.steps)
+        es.download()
+    e2e_wall = time.perf_counter() - t0
+    mine = {"step_ms": step_ms, "sweep_ms": statistics.mean(sweep_ms) if a.order == 2 else None,
+            "flux_ms": statistics.mean(flux_ms), "e2e_wall": e2e_wall, "launches": launches,
+            "clocks": clocks.summary()}
+    everyone = [None] * world
+    dist.all_gather_object(everyone, mine)
+    if rank == 0:
+        step_max = np.max(np.array([e["step_ms"] for e in everyone]), axis=0)  # max over ranks, per step
+        total_ms = float(step_max.sum())
+        value = n * a.steps / (total_ms * 1e-3)
+        e2e_wall = max(e["e2e_wall"] for e in everyone)
+        flux_avg = max(e["flux_ms"] for e in everyone)
+        counts = load_counts()
+        fp64_peak = L.fp64_peak_tflops(device)
+        flops_pt = counts.get("flux_fp64_flops_per_point")
+        n_flux_dom = n_flux / world
+        achieved = flops_pt * n_flux_dom / (flux_avg * 1e-3) / 1e12 if (flops_pt and flux_avg > 0) else None
+        traffic = counts.get("flux_dram_bytes_per_point")
+        hbm, hbm_kind = hbm_peak()
+        sweep_avg = max(e["sweep_ms"] for e in everyone) if a.order == 2 else None
+        sweep_gbs = sweep_bytes(k) * (n / world) / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
+        iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9 / world
+        nnz = e2e_cloud.nnz
+        h2d = n * (16 + 16 + 1 + 1 + 32) + 4 * (n + 1) + 4 * nnz
+        d2h = n * 21 * 8 + 8 * a.steps
+        clk = everyone[0]["clocks"]
+        clk["reasons"] = sorted({r for e in everyone for r in e["clocks"]["reasons"]})
+        launches = sum(e["launches"] for e in everyone)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (free-stream state on a generated cloud)",
+            "config": config_block(a, n, {"parallelism": f"rcb{world}: one process per GPU, CUDA-IPC peer-memory "
+                                                         "halos, device-side progress counters"}),
+            "e2e": {"value": n * a.steps / e2e_wall, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps),
+                    "what": "max over ranks of RankSession create (screening, upload of the rank's piece), "
+                            f"{a.steps} iterations, copy-back of owned points"},
+            "gpu_launches": launches * a.steps,
+            "gpu_launches_note": f"{launches} kernels per iteration summed over ranks (compute, halo, "
+                                 f"signal, wait) x {a.steps}; plus {a.steps * world} L2-flush kernels",
+            "roofline": {"bound": "fp64", "kernel": "k_flux (flux residual, W=8 lanes per point)",
+                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak if achieved else None,
+                         "traffic": traffic * n_flux_dom if traffic else None,
+                         "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
+                         "flops_source": "ncu dynamic 2*DFMA+DADD+DMUL per point, profiles/flux_ncu_counts.json",
+                         "launch_ms": flux_avg},
+            "roofline_hbm": {"bound": "hbm", "kernel": "k_sweep", "achieved": sweep_gbs, "peak": hbm,
+                             "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
+                             "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_avg,
+                             "peak_source": hbm_kind, "iteration_achieved_gbs_per_gpu": iter_gbs,
+                             "iteration_frac": iter_gbs / hbm,
+                             "iteration_bytes_per_point": iteration_bytes(k, a.order, a.inner)},
+            "clocks": clk,
+            "final_residue": float(residues[-1]) if len(residues) else None,
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -115,6 +115,31 @@ int lskum_b200_session_flush_l2(lskum_b200_session* s);
 int lskum_b200_fp64_peak(int device, double* tflops);
 void lskum_b200_session_destroy(lskum_b200_session* s);
 
+/* ---- one process per GPU (torchrun ranks) ----
+ * Every rank calls rank_create on the same cloud/config with its rank, the
+ * world size and its CUDA device; the rank builds only its own RCB piece
+ * (owned points + halo) in IPC-exportable memory.  The caller exchanges the
+ * opaque blobs (rank_blob_size() bytes each, e.g. an all_gather) and passes
+ * all `world` of them, in rank order, to rank_connect.  Stage ordering across
+ * processes is device-side (release/acquire progress counters), so iterate
+ * only enqueues and synchronises its own stream.  Residues are available on
+ * rank 0; download fills this rank's owned points of the cloud's store.
+ * rank_info: kernels enqueued per iteration and, after a failure, the rank
+ * that owns the failing point (its message is the reference's). */
+typedef struct lskum_b200_rank lskum_b200_rank;
+int lskum_b200_rank_create(lskum_cloud* cloud, const lskum_config* cfg, int rank, int world,
+                           int device, int capacity, int from_state, lskum_b200_rank** out);
+int lskum_b200_rank_blob_size(void);
+int lskum_b200_rank_blob(const lskum_b200_rank* r, void* out);
+int lskum_b200_rank_connect(lskum_b200_rank* r, const void* blobs, int world);
+int lskum_b200_rank_iterate(lskum_b200_rank* r, int n, double* device_ms);
+int lskum_b200_rank_residues(const lskum_b200_rank* r, double* out, int cap, int* n_out);
+int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, int* fault_owner);
+int lskum_b200_rank_download(lskum_b200_rank* r);
+int lskum_b200_rank_event_ms(const lskum_b200_rank* r, double* sweep_ms, double* flux_ms);
+int lskum_b200_rank_flush_l2(lskum_b200_rank* r);
+void lskum_b200_rank_destroy(lskum_b200_rank* r);
+
 /* ---- verification hook ----
  * Evaluates CUDA libdevice erf (fn 0) / exp (fn 1) into ref[] and the engine's
  * constant-table replicas used by the flux kernel into ours[] (must be bitwise equal). */

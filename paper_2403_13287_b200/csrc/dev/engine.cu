@@ -918,6 +918,7 @@ class Domain {
     const int iter = hsh_.get()->err_iter + 1;
     if (phase == PH_RESIDUE)
       return Fault(Status::positivity, "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
+    if (phase == PH_STALL) return Fault(Status::argument, "peer rank stopped making progress (wait timed out)");
     const int li = local >= 0 ? local : static_cast<int>(point);
     if (strict_)
       k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), which_.get(), gas_, key, li,
@@ -1408,6 +1409,334 @@ class MultiRun {
   cudaEvent_t t0_ = nullptr, t1_ = nullptr, kev_[4] = {};
   int t_ = 0;
 };
+
+// ===========================================================================
+// One process per GPU (torchrun ranks).  Every rank derives the same RCB
+// decomposition and builds only its own domain.  Peers' q/dq buffers, the
+// root's shared control word and residue array are mapped with CUDA IPC; the
+// stage ordering that MultiRun gets from cross-stream events comes from
+// monotonic 64-bit progress counters written with release semantics by
+// k_signal and awaited with acquire loads by k_wait (device-side, so no host
+// ordering between processes is needed).
+namespace {
+
+enum : int { FL_SW = 0, FL_DQH = 1, FL_UPD = 2, FL_RES = 3, FL_COUNT = 4 };
+
+struct WaitList {
+  const unsigned long long* ptr[kMaxDomains];
+  int n;
+};
+
+__global__ void k_signal(unsigned long long* flag, unsigned long long v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+}
+
+// Spins (acquire, system scope) until every listed counter reaches `target`.
+// Gives up once the run has failed (every later kernel skips, so nothing is
+// left to order) or after kStallNs, recording PH_STALL so the host raises
+// instead of hanging the device.
+constexpr unsigned long long kStallNs = 30ull * 1000 * 1000 * 1000;
+
+__global__ void k_wait(WaitList w, unsigned long long target, Shared* sh) {
+  const int m = threadIdx.x;
+  if (m >= w.n) return;
+  const unsigned long long t0 = globaltimer();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w.ptr[m]) : "memory");
+    if (v >= target || ld_volatile(&sh->err_key) != kNoErr) return;
+    if (globaltimer() - t0 > kStallNs) {
+      atomicMin(&sh->err_key, static_cast<unsigned long long>(PH_STALL) << 61);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
+struct RankBlob {
+  int rank = 0, world = 0, device = 0, pad = 0;
+  cudaIpcMemHandle_t q[2], dq[2], flags, sh, mag;
+};
+
+template <class T>
+T* open_ipc(const cudaIpcMemHandle_t& h) {
+  void* p = nullptr;
+  ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+class RankRun {
+ public:
+  RankRun(PointSet& ps, const EngineSpec& spec, int rank, int world, int device, int capacity)
+      : ps_(ps), spec_(spec), rank_(rank), world_(world), device_(device) {
+    if (world < 1 || world > kMaxDomains || rank < 0 || rank >= world)
+      raise(Status::argument, "rank/world out of range");
+    geoms_ = decompose(ps, world, spec.part_of);
+    const LocalGeom& g = geoms_[rank];
+    dom_ = std::make_unique<Domain>(view_of(g), device, spec.gamma, spec.cfl, spec.det_tol, capacity, true);
+    std::vector<int> srcs(g.halo_dom.begin(), g.halo_dom.end());
+    std::sort(srcs.begin(), srcs.end());
+    srcs.erase(std::unique(srcs.begin(), srcs.end()), srcs.end());
+    src_ = srcs;
+    for (int d = 0; d < world; ++d) {
+      if (d == rank) continue;
+      for (int o : geoms_[d].halo_dom)
+        if (o == rank) {
+          readers_.push_back(d);
+          break;
+        }
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    const std::size_t nh = g.halo_dom.size();
+    hdom_.alloc(std::max<std::size_t>(1, nh));
+    hidx_.alloc(std::max<std::size_t>(1, nh));
+    if (nh) {
+      ck(cudaMemcpy(hdom_.get(), g.halo_dom.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hdom");
+      ck(cudaMemcpy(hidx_.get(), g.halo_idx.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hidx");
+    }
+    flags_.alloc(FL_COUNT);
+    ck(cudaMemset(flags_.get(), 0, FL_COUNT * sizeof(unsigned long long)), "zero flags");
+    if (rank == 0) {
+      dom_->set_residue_size(ps.n());
+      dom_->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);  // shared word
+      ck(cudaStreamSynchronize(dom_->stream()), "root init");
+    }
+    ck(cudaEventCreate(&t0_), "ev");
+    ck(cudaEventCreate(&t1_), "ev");
+    for (auto& e : kev_) ck(cudaEventCreate(&e), "ev");
+    blob_.rank = rank;
+    blob_.world = world;
+    blob_.device = device;
+    ck(cudaIpcGetMemHandle(&blob_.q[0], dom_->q_buf(0)), "IpcGetMemHandle q0");
+    ck(cudaIpcGetMemHandle(&blob_.q[1], dom_->q_buf(1)), "IpcGetMemHandle q1");
+    ck(cudaIpcGetMemHandle(&blob_.dq[0], dom_->dq_buf(0)), "IpcGetMemHandle dq0");
+    ck(cudaIpcGetMemHandle(&blob_.dq[1], dom_->dq_buf(1)), "IpcGetMemHandle dq1");
+    ck(cudaIpcGetMemHandle(&blob_.flags, flags_.get()), "IpcGetMemHandle flags");
+    if (rank == 0) {
+      ck(cudaIpcGetMemHandle(&blob_.sh, dom_->own_shared()), "IpcGetMemHandle shared");
+      ck(cudaIpcGetMemHandle(&blob_.mag, dom_->mag_buf()), "IpcGetMemHandle mag");
+    }
+  }
+
+  ~RankRun() {
+    if (dom_) cudaStreamSynchronize(dom_->stream());
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    cudaEventDestroy(t0_);
+    cudaEventDestroy(t1_);
+    for (auto& e : kev_) cudaEventDestroy(e);
+  }
+
+  const RankBlob& blob() const { return blob_; }
+
+  // Maps every peer's buffers, uploads this rank's state and computes its
+  // first q (owned and halo points).
+  void connect(const std::vector<RankBlob>& blobs) {
+    if (static_cast<int>(blobs.size()) != world_) raise(Status::argument, "need one blob per rank");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    for (int o = 0; o < world_; ++o) {
+      if (o == rank_) {
+        for (int k = 0; k < 2; ++k) {
+          qp_[k].base[o] = dom_->q_buf(k);
+          dqp_[k].base[o] = dom_->dq_buf(k);
+        }
+        flag_[o] = flags_.get();
+        continue;
+      }
+      const RankBlob& b = blobs[o];
+      for (int k = 0; k < 2; ++k) {
+        qp_[k].base[o] = open(open_ipc<D4>(b.q[k]));
+        dqp_[k].base[o] = open(open_ipc<D4>(b.dq[k]));
+      }
+      flag_[o] = open(open_ipc<unsigned long long>(b.flags));
+      if (o == 0) {
+        dom_->use_shared(open(open_ipc<Shared>(b.sh)));
+        dom_->use_mag(open(open_ipc<double>(b.mag)));
+      }
+    }
+    dom_->upload(ps_.fields, false);
+    if (rank_ != 0) dom_->reset_run(spec_.order, spec_.inner, spec_.fp_mode, spec_.chunk, false);
+    dom_->first_q();
+    ck(cudaStreamSynchronize(dom_->stream()), "first q");
+    dom_->refresh_ctl();
+  }
+
+  double iterate(int n) {
+    Domain& d = *dom_;
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    d.set_diag(t_ + n - 1);
+    ck(cudaEventRecord(t0_, d.stream()), "EventRecord");
+    int issued = 0, waited = 0;
+    bool failed = false;
+    const int end = t_ + n;
+    for (; t_ < end && !failed; ++t_) {
+      enqueue(t_, t_ == end - 1);
+      failed = d.poll(issued, waited);
+    }
+    // Every rank returns only after the root's residue of the last enqueued
+    // iteration, so all of them observe the same error word.
+    if (rank_ != 0) wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t_));
+    ck(cudaEventRecord(t1_, d.stream()), "EventRecord");
+    ck(cudaStreamSynchronize(d.stream()), "rank iterate");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, t0_, t1_), "EventElapsed");
+    d.refresh_ctl();
+    d.set_done(d.shared_host().iter);
+    d.add_ms(ms);
+    return ms;
+  }
+
+  bool failed() { return dom_->failed(); }
+  // The failing point's owner builds the reference message; the other ranks
+  // report where it failed (the Python driver forwards the owner's text).
+  Fault fault() {
+    const unsigned long long key = dom_->shared_host().err_key;
+    const unsigned phase = static_cast<unsigned>(key >> 61);
+    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    const LocalGeom& lg = geoms_[rank_];
+    const auto end = lg.gid.begin() + lg.n_own;
+    const auto it = std::lower_bound(lg.gid.begin(), end, g);
+    if (phase == PH_RESIDUE || phase == PH_STALL || (it != end && *it == g))
+      return dom_->fault_in_run(phase == PH_RESIDUE || phase == PH_STALL ? -1 : static_cast<int>(it - lg.gid.begin()));
+    return Fault(phase == PH_SWEEP ? Status::singular : Status::positivity,
+                 "iteration " + itos(dom_->shared_host().err_iter + 1) + ": failure at point " + itos(g) +
+                     " owned by another rank");
+  }
+  // Rank owning the failing point (-1: none / not point-specific).
+  int fault_owner() const {
+    const unsigned long long key = dom_->shared_host().err_key;
+    if (key == kNoErr || (key >> 61) >= PH_RESIDUE) return -1;
+    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    for (int d = 0; d < world_; ++d) {
+      const LocalGeom& lg = geoms_[d];
+      if (std::binary_search(lg.gid.begin(), lg.gid.begin() + lg.n_own, g)) return d;
+    }
+    return -1;
+  }
+  Domain& dom() { return *dom_; }
+  bool is_root() const { return rank_ == 0; }
+  void download() { copy_back(*dom_, ps_); }
+  void flush_l2() { dom_->flush_l2(); }
+  // Kernels (compute, halo, signal, wait) this rank enqueued for its last iteration.
+  int launches_per_iter() const { return launches_; }
+  void last_event_ms(double& sweep_ms, double& flux_ms) const {
+    float a = 0.0f, b = 0.0f;
+    sweep_ms = flux_ms = 0.0;
+    if (spec_.order == 2 && cudaEventElapsedTime(&a, kev_[0], kev_[1]) == cudaSuccess) sweep_ms = a;
+    if (cudaEventElapsedTime(&b, kev_[2], kev_[3]) == cudaSuccess) flux_ms = b;
+    cudaGetLastError();
+  }
+
+ private:
+  template <class T>
+  T* open(T* p) {
+    opened_.push_back(p);
+    return p;
+  }
+  void signal(int slot, unsigned long long v) {
+    k_signal<<<1, 1, 0, dom_->stream()>>>(flags_.get() + slot, v);
+    ++launches_;
+  }
+  void wait_for(const std::vector<int>& ranks, int slot, unsigned long long v) {
+    if (ranks.empty()) return;
+    WaitList w{};
+    w.n = static_cast<int>(ranks.size());
+    for (int m = 0; m < w.n; ++m) w.ptr[m] = flag_[ranks[m]] + slot;
+    k_wait<<<1, 32, 0, dom_->stream()>>>(w, v, dom_->shared());
+    ++launches_;
+  }
+
+  void enqueue(int t, bool timed) {
+    Domain& d = *dom_;
+    cudaStream_t st = d.stream();
+    const int a = t & 1;
+    launches_ = 0;
+    if (t > 0) {
+      wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t));  // residue(t-1) done
+      wait_for(src_, FL_UPD, static_cast<unsigned long long>(t));                  // owners' q(t) ready
+      d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a]);
+      ++launches_;
+    }
+    int bfin = 0;
+    if (spec_.order == 2) {
+      for (int s = 0; s < spec_.inner; ++s) {
+        const int k = t * spec_.inner + s, b = k & 1;
+        if (s >= 2) wait_for(readers_, FL_DQH, static_cast<unsigned long long>(k - 1));  // readers gathered k-2
+        if (timed && s == 0) ck(cudaEventRecord(kev_[0], st), "EventRecord");
+        d.launch_sweep(a, b, s == 0);
+        launches_ += 2;  // sweep + dq halo
+        if (timed && s == 0) ck(cudaEventRecord(kev_[1], st), "EventRecord");
+        signal(FL_SW, static_cast<unsigned long long>(k + 1));
+        wait_for(src_, FL_SW, static_cast<unsigned long long>(k + 1));
+        d.launch_halo(d.dq_buf(b ^ 1), 2, hdom_.get(), hidx_.get(), dqp_[b ^ 1]);
+        signal(FL_DQH, static_cast<unsigned long long>(k + 1));
+      }
+      bfin = ((t + 1) * spec_.inner) & 1;
+    }
+    if (timed) ck(cudaEventRecord(kev_[2], st), "EventRecord");
+    d.launch_flux(a, bfin, spec_.order != 2);
+    if (timed) ck(cudaEventRecord(kev_[3], st), "EventRecord");
+    d.launch_update(a);
+    launches_ += 2;  // flux + update
+    signal(FL_UPD, static_cast<unsigned long long>(t + 1));
+    if (rank_ == 0) {
+      std::vector<int> all;
+      for (int o = 1; o < world_; ++o) all.push_back(o);
+      wait_for(all, FL_UPD, static_cast<unsigned long long>(t + 1));
+      d.launch_residue();
+      launches_ += 2;  // tree partial + final
+      signal(FL_RES, static_cast<unsigned long long>(t + 1));
+    }
+    ck(cudaGetLastError(), "rank launches");
+  }
+
+  PointSet& ps_;
+  EngineSpec spec_;
+  int rank_ = 0, world_ = 1, device_ = 0;
+  std::vector<LocalGeom> geoms_;
+  std::unique_ptr<Domain> dom_;
+  std::vector<int> src_, readers_;
+  DBuf<int> hdom_, hidx_;
+  DBuf<unsigned long long> flags_;
+  PeerTab qp_[2]{}, dqp_[2]{};
+  unsigned long long* flag_[kMaxDomains] = {};
+  std::vector<void*> opened_;
+  RankBlob blob_{};
+  cudaEvent_t t0_ = nullptr, t1_ = nullptr, kev_[4] = {};
+  int t_ = 0, launches_ = 0;
+};
+
+RankRun* rank_open(PointSet& ps, const EngineSpec& spec, int rank, int world, int device, int capacity) {
+  return new RankRun(ps, spec, rank, world, device, capacity);
+}
+std::size_t rank_blob_bytes() { return sizeof(RankBlob); }
+std::vector<unsigned char> rank_blob(const RankRun* r) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&r->blob());
+  return std::vector<unsigned char>(p, p + sizeof(RankBlob));
+}
+void rank_connect(RankRun* r, const std::vector<std::vector<unsigned char>>& blobs) {
+  std::vector<RankBlob> bs(blobs.size());
+  for (std::size_t i = 0; i < blobs.size(); ++i) {
+    if (blobs[i].size() != sizeof(RankBlob)) raise(Status::argument, "malformed rank blob");
+    std::memcpy(&bs[i], blobs[i].data(), sizeof(RankBlob));
+  }
+  r->connect(bs);
+  if (r->failed()) throw r->fault();
+}
+double rank_iterate(RankRun* r, int n) {
+  const double ms = r->iterate(n);
+  if (r->failed()) throw r->fault();
+  return ms;
+}
+std::vector<double> rank_residues(RankRun* r) { return r->is_root() ? r->dom().residues() : std::vector<double>(); }
+void rank_download(RankRun* r) { r->download(); }
+void rank_flush_l2(RankRun* r) { r->flush_l2(); }
+void rank_event_ms(const RankRun* r, double* sweep_ms, double* flux_ms) { r->last_event_ms(*sweep_ms, *flux_ms); }
+int rank_launches_per_iter(const RankRun* r) { return r->launches_per_iter(); }
+int rank_fault_owner(const RankRun* r) { return r->fault_owner(); }
+void rank_close(RankRun* r) { delete r; }
 
 RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms) {
   if (spec.iters == 0) return engine_run(ps, spec);

@@ -26,7 +26,8 @@
 namespace lskd {
 
 constexpr unsigned long long kNoErr = ~0ull;
-enum : unsigned { PH_QVAR = 0, PH_SWEEP = 1, PH_FLUX = 2, PH_UPDATE = 3, PH_RESIDUE = 4 };
+// PH_STALL: a cross-process wait timed out (per-rank runs only).
+enum : unsigned { PH_QVAR = 0, PH_SWEEP = 1, PH_FLUX = 2, PH_UPDATE = 3, PH_RESIDUE = 4, PH_STALL = 5 };
 enum : unsigned { KIND_INTERIOR = 0, KIND_WALL = 1, KIND_OUTER = 2 };
 constexpr unsigned kSolveSlot = 0xFFFFFu;  // "after every neighbour" in the error key
 

@@ -70,6 +70,23 @@ double engine_fp64_peak_tflops(int device);
 void engine_math_selftest(int fn, const double* in, std::int64_t n, double* ref, double* ours);
 void session_close(Session* s);
 
+// One process per GPU: this rank's domain of a `world`-way RCB run.  The
+// opaque blob (CUDA IPC handles) is exchanged by the caller (e.g. an
+// all_gather over torch.distributed) and passed back to rank_connect.
+class RankRun;
+RankRun* rank_open(PointSet& ps, const EngineSpec& spec, int rank, int world, int device, int capacity);
+std::size_t rank_blob_bytes();
+std::vector<unsigned char> rank_blob(const RankRun* r);
+void rank_connect(RankRun* r, const std::vector<std::vector<unsigned char>>& blobs);
+double rank_iterate(RankRun* r, int n);
+std::vector<double> rank_residues(RankRun* r);
+void rank_download(RankRun* r);
+void rank_flush_l2(RankRun* r);
+void rank_event_ms(const RankRun* r, double* sweep_ms, double* flux_ms);
+int rank_launches_per_iter(const RankRun* r);
+int rank_fault_owner(const RankRun* r);
+void rank_close(RankRun* r);
+
 // Per-phase operators on the whole cloud (reference kernels.hpp:25-63).
 enum class Op { q_variables, q_derivatives, publish, flux_fused, flux_direction, timestep,
                 state_update };

@@ -67,6 +67,13 @@ struct lskum_b200_session {
   }
 };
 
+struct lskum_b200_rank {
+  lskb::RankRun* run = nullptr;
+  ~lskum_b200_rank() {
+    if (run) lskb::rank_close(run);
+  }
+};
+
 #define NONNULL(...)                                                    \
   do {                                                                  \
     const void* ptrs_[] = {__VA_ARGS__};                                \
@@ -527,5 +534,88 @@ int lskum_b200_math_selftest(int fn, const double* in, int64_t n, double* ref, d
 }
 
 void lskum_b200_session_destroy(lskum_b200_session* s) { delete s; }
+
+// ---------------------------------------------------------------- ranks
+int lskum_b200_rank_create(lskum_cloud* cloud, const lskum_config* cfg, int rank, int world, int device,
+                           int capacity, int from_state, lskum_b200_rank** out) {
+  NONNULL(cloud, cfg, out);
+  if (capacity < 1) return fail(LSKUM_ERR_ARGUMENT, "capacity must be >= 1");
+  return guard([&] {
+    if (!from_state) {
+      cfg->s.check();
+      cloud->ps.reset_fields(cfg->s.layout);
+      lskb::freestream(cloud->ps, cfg->s.mach, cfg->s.aoa, cfg->s.gamma);
+    }
+    const lskb::EngineSpec spec = lskb::prepare_run(cloud->ps, cfg->s);
+    auto r = std::make_unique<lskum_b200_rank>();
+    r->run = lskb::rank_open(cloud->ps, spec, rank, world, device, capacity);
+    *out = r.release();
+  });
+}
+
+int lskum_b200_rank_blob_size(void) { return static_cast<int>(lskb::rank_blob_bytes()); }
+
+int lskum_b200_rank_blob(const lskum_b200_rank* r, void* out) {
+  NONNULL(r, out);
+  return guard([&] {
+    const std::vector<unsigned char> b = lskb::rank_blob(r->run);
+    std::memcpy(out, b.data(), b.size());
+  });
+}
+
+int lskum_b200_rank_connect(lskum_b200_rank* r, const void* blobs, int world) {
+  NONNULL(r, blobs);
+  return guard([&] {
+    const std::size_t sz = lskb::rank_blob_bytes();
+    const unsigned char* p = static_cast<const unsigned char*>(blobs);
+    std::vector<std::vector<unsigned char>> v;
+    for (int i = 0; i < world; ++i) v.emplace_back(p + i * sz, p + (i + 1) * sz);
+    lskb::rank_connect(r->run, v);
+  });
+}
+
+int lskum_b200_rank_iterate(lskum_b200_rank* r, int n, double* device_ms) {
+  NONNULL(r);
+  if (n < 0) return fail(LSKUM_ERR_ARGUMENT, "iteration count must be >= 0");
+  return guard([&] {
+    const double ms = n > 0 ? lskb::rank_iterate(r->run, n) : 0.0;
+    if (device_ms) *device_ms = ms;
+  });
+}
+
+int lskum_b200_rank_residues(const lskum_b200_rank* r, double* out, int cap, int* n_out) {
+  NONNULL(r, n_out);
+  return guard([&] {
+    const std::vector<double> v = lskb::rank_residues(r->run);
+    *n_out = static_cast<int>(v.size());
+    if (out)
+      for (int i = 0; i < std::min<int>(cap, static_cast<int>(v.size())); ++i) out[i] = v[i];
+  });
+}
+
+int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, int* fault_owner) {
+  NONNULL(r);
+  return guard([&] {
+    if (launches_per_iter) *launches_per_iter = lskb::rank_launches_per_iter(r->run);
+    if (fault_owner) *fault_owner = lskb::rank_fault_owner(r->run);
+  });
+}
+
+int lskum_b200_rank_download(lskum_b200_rank* r) {
+  NONNULL(r);
+  return guard([&] { lskb::rank_download(r->run); });
+}
+
+int lskum_b200_rank_event_ms(const lskum_b200_rank* r, double* sweep_ms, double* flux_ms) {
+  NONNULL(r, sweep_ms, flux_ms);
+  return guard([&] { lskb::rank_event_ms(r->run, sweep_ms, flux_ms); });
+}
+
+int lskum_b200_rank_flush_l2(lskum_b200_rank* r) {
+  NONNULL(r);
+  return guard([&] { lskb::rank_flush_l2(r->run); });
+}
+
+void lskum_b200_rank_destroy(lskum_b200_rank* r) { delete r; }
 
 }  // extern "C"
