@@ -124,8 +124,11 @@ void lskum_b200_session_destroy(lskum_b200_session* s);
  * processes is device-side (release/acquire progress counters), so iterate
  * only enqueues and synchronises its own stream.  Residues are available on
  * rank 0; download fills this rank's owned points of the cloud's store.
- * rank_info: kernels enqueued per iteration and, after a failure, the rank
- * that owns the failing point (its message is the reference's). */
+ * rank_info: kernels enqueued per iteration and this rank's failure record:
+ * the stage (iteration * (sweeps + 4) + phase slot) and ordering key of its
+ * first failure (UINT64_MAX: none) and whether it owns the failing point.
+ * The run's failure is the record with the smallest (stage, key) over the
+ * ranks; the owning rank's lskum_last_error() text is the reference's. */
 typedef struct lskum_b200_rank lskum_b200_rank;
 int lskum_b200_rank_create(lskum_cloud* cloud, const lskum_config* cfg, int rank, int world,
                            int device, int capacity, int from_state, lskum_b200_rank** out);
@@ -134,7 +137,8 @@ int lskum_b200_rank_blob(const lskum_b200_rank* r, void* out);
 int lskum_b200_rank_connect(lskum_b200_rank* r, const void* blobs, int world);
 int lskum_b200_rank_iterate(lskum_b200_rank* r, int n, double* device_ms);
 int lskum_b200_rank_residues(const lskum_b200_rank* r, double* out, int cap, int* n_out);
-int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, int* fault_owner);
+int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, uint64_t* err_stage,
+                         uint64_t* err_key, int* owns_failure);
 int lskum_b200_rank_download(lskum_b200_rank* r);
 int lskum_b200_rank_event_ms(const lskum_b200_rank* r, double* sweep_ms, double* flux_ms);
 int lskum_b200_rank_flush_l2(lskum_b200_rank* r);

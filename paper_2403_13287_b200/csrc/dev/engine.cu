@@ -167,33 +167,54 @@ int sweep_min_blocks() {
   return mb;
 }
 
-template <bool S, int MB>
-void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                    unsigned long long* it0, cudaStream_t st) {
-  static int resident[64] = {};
+// Sweep variant: LSKUM_SWEEP_LANES = 2 (default, k_sweep2) | 1 (k_sweep).
+int sweep_lanes() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_SWEEP_LANES");
+    return (e && std::atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
+template <class K>
+int resident_blocks(K kern, int slot) {
+  static int resident[8][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!resident[dev & 63]) {
+  int& r = resident[slot & 7][dev & 63];
+  if (!r) {
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<S, MB>, 256, 0), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-    resident[dev & 63] = std::max(1, per_sm) * sms;
+    r = std::max(1, per_sm) * sms;
   }
-  const int grid = std::max(1, std::min((g.n + 255) / 256, resident[dev & 63]));
-  k_sweep<S, MB><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0);
+  return r;
+}
+
+template <bool S, int MB>
+void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                    unsigned long long* it0, int sweep, cudaStream_t st) {
+  const int slot = (S ? 4 : 0) + MB - 2;
+  if (sweep_lanes() == 2) {
+    const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
+    k_sweep2<S, MB><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0, sweep);
+  } else {
+    const int grid = std::max(1, std::min((g.n + 255) / 256, resident_blocks(k_sweep<S, MB>, slot)));
+    k_sweep<S, MB><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0, sweep);
+  }
 }
 
 void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                  unsigned long long* it0, cudaStream_t st) {
+                  unsigned long long* it0, int sweep, cudaStream_t st) {
   const int mb = sweep_min_blocks();
   if (strict) {
-    if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, st);
-    else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, st);
-    else sweep_launch_t<true, 3>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep_launch_t<true, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   } else {
-    if (mb == 2) sweep_launch_t<false, 2>(g, q, dq_in, dq_out, gas, ctl, it0, st);
-    else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, st);
-    else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, st);
+    if (mb == 2) sweep_launch_t<false, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   }
 }
 
@@ -311,12 +332,14 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
 
 // Resets this domain's timers, points it at the run's shared word and (for
 // the domain that owns it) resets that word.
-__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter) {
+__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, int spi) {
   ctl->sh = sh;
   ctl->diag_iter = diag_iter;
+  ctl->spi = spi;
+  ctl->err_stage = kNoErr;
+  ctl->err_key = kNoErr;
   if (own_shared) {
-    sh->err_key = kNoErr;
-    sh->err_iter = 0x7FFFFFFF;
+    sh->err_stage = kNoErr;
     sh->iter = 0;
   }
   for (int k = 0; k < KT_COUNT; ++k) {
@@ -529,7 +552,7 @@ class Domain {
     hsh_.alloc(1);
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
     ck(cudaGetLastError(), "k_min_dist");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0);
     ck(cudaStreamSynchronize(st_), "geometry upload");
   }
 
@@ -696,7 +719,7 @@ class Domain {
     ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(res_.get(), 0, n * sizeof(D4), st_), "zero res");
     ck(cudaMemsetAsync(dt_.get(), 0, n * sizeof(double), st_), "zero dt");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1, (order == 2 ? inner : 0) + 4);
     a_ = 0;
     b_ = 0;
     done_ = 0;
@@ -731,9 +754,10 @@ class Domain {
   }
 
   // ---- building blocks of one iteration (also used by the multi-domain driver) ----
-  void launch_sweep(int a, int b, bool first) {
+  // Derivative sweep s of the iteration (s = 0 stamps the iteration start).
+  void launch_sweep(int a, int b, int s) {
     sweep_launch(strict_, geo(), q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
-                 first ? it0_.get() : nullptr, st_);
+                 s == 0 ? it0_.get() : nullptr, s, st_);
   }
   void launch_flux(int a, int b, bool stamp) {
     FluxArgs fa;
@@ -769,12 +793,13 @@ class Domain {
                                                       ctl_.get());
     k_tree_final<<<1, 1024, 0, st_>>>(pval_.get(), psz_.get(), d1_, n_res_, hist_.get(), it1_.get(), ctl_.get());
   }
-  // Halo gather of `recs` records per point from the owners' buffers.
-  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src) {
+  // Halo gather of `recs` records per point from the owners' buffers, as
+  // part of stage `sub` of the iteration (0: q; 1+s: derivatives of sweep s).
+  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src, int sub) {
     const int nh = n_loc_ - n_;
     if (nh <= 0) return;
     k_halo<<<std::min((nh * recs + 255) / 256, 4096), 256, 0, st_>>>(dst, recs, n_, nh, hdom, hidx, src,
-                                                                       shared_);
+                                                                       ctl_.get(), sub);
   }
 
   // One iteration starting at parity (a, b); `timed` brackets the first sweep
@@ -783,7 +808,7 @@ class Domain {
     if (order_ == 2) {
       for (int s = 0; s < inner_; ++s) {
         if (timed && s == 0) record_ext(kev_[0]);
-        launch_sweep(a, b, s == 0);
+        launch_sweep(a, b, s);
         if (timed && s == 0) record_ext(kev_[1]);
         b ^= 1;
       }
@@ -861,7 +886,7 @@ class Domain {
   // kPolls-1 are in flight.  True once an error has been observed.
   bool poll(int& issued, int& waited) {
     const int s = issued % kPolls;
-    ck(cudaMemcpyAsync(hpoll_.get() + s, &shared_->err_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    ck(cudaMemcpyAsync(hpoll_.get() + s, &shared_->err_stage, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        st_),
        "poll copy");
     ck(cudaEventRecord(poll_ev_[s], st_), "poll event");
@@ -881,7 +906,16 @@ class Domain {
     ck(cudaStreamSynchronize(st_), "ctl");
   }
 
-  bool failed() const { return hsh_.get()->err_key != kNoErr; }
+  bool failed() const { return hsh_.get()->err_stage != kNoErr; }
+  // This domain's own failure record (valid after refresh_ctl).
+  bool has_error() const { return hctl_.get()->err_stage != kNoErr; }
+  unsigned long long err_stage() const { return hctl_.get()->err_stage; }
+  unsigned long long err_key() const { return hctl_.get()->err_key; }
+  int err_iter() const {
+    const int spi = hctl_.get()->spi;
+    const unsigned long long st = hctl_.get()->err_stage;
+    return (st == kNoErr || spi <= 0) ? 0 : static_cast<int>(st / static_cast<unsigned>(spi));
+  }
   const Shared& shared_host() const { return *hsh_.get(); }
 
   // CUDA-event times of the first sweep and the flux kernel of the last
@@ -904,7 +938,7 @@ class Domain {
   const D4* q_of_iter(int t) const { return q_[t & 1].get(); }
   const D4* dq_of_flux(int t) const { return order_ == 2 ? dq_[((t + 1) * inner_) & 1].get() : dq_[0].get(); }
   Fault fault_in_run(int local) {
-    const int t = std::max(0, std::min(hsh_.get()->err_iter, std::max(0, capacity_ - 1)));
+    const int t = std::max(0, std::min(err_iter(), std::max(0, capacity_ - 1)));
     return fault(true, q_of_iter(t), dq_of_flux(t), local);
   }
   Fault fault_in_run() { return fault_in_run(-1); }
@@ -912,10 +946,14 @@ class Domain {
   // Builds the reference-format message for the recorded failure; `local` is
   // the failing point's local index (-1: the key's global id is local).
   Fault fault(bool with_iteration, const D4* qsrc, const D4* dqsrc, int local = -1) {
-    const unsigned long long key = hsh_.get()->err_key;
+    return fault_for(err_key(), err_iter(), with_iteration, qsrc, dqsrc, local);
+  }
+  // Message for `key` (another domain's record when this domain owns the point).
+  Fault fault_for(unsigned long long key, int err_it, bool with_iteration, const D4* qsrc, const D4* dqsrc,
+                  int local = -1) {
     const unsigned phase = static_cast<unsigned>(key >> 61);
     const long long point = static_cast<long long>((key >> 22) & 0x7FFFFFFFull);
-    const int iter = hsh_.get()->err_iter + 1;
+    const int iter = err_it + 1;
     if (phase == PH_RESIDUE)
       return Fault(Status::positivity, "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
     if (phase == PH_STALL) return Fault(Status::argument, "peer rank stopped making progress (wait timed out)");
@@ -1108,7 +1146,7 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
   if (d->failed()) {
     Fault f = d->fault_in_run();
     copy_back(*d, ps);
-    rec.abort_iteration = d->shared_host().err_iter + 1;
+    rec.abort_iteration = d->err_iter() + 1;
     throw f;
   }
   copy_back(*d, ps);
@@ -1299,11 +1337,30 @@ class MultiRun {
 
   bool failed() { return root().failed(); }
 
+  // The run's failure: min (stage, key) over the domains' own records; the
+  // message is built by the domain owning the failing point.
+  int first_failing_domain() {
+    int best = -1;
+    for (int d = 0; d < P_; ++d) {
+      dom_[d]->refresh_ctl();
+      if (!dom_[d]->has_error()) continue;
+      if (best < 0 || std::make_pair(dom_[d]->err_stage(), dom_[d]->err_key()) <
+                          std::make_pair(dom_[best]->err_stage(), dom_[best]->err_key()))
+        best = d;
+    }
+    return best;
+  }
+  int abort_iteration() {
+    const int d = first_failing_domain();
+    return d < 0 ? 0 : dom_[d]->err_iter() + 1;
+  }
   Fault fault() {
-    const unsigned long long key = root().shared_host().err_key;
+    const int rec = first_failing_domain();
+    if (rec < 0) return Fault(Status::argument, "multi-domain run failed without a failure record");
+    const unsigned long long key = dom_[rec]->err_key();
     const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
-    int owner = 0, local = g;
-    if (static_cast<unsigned>(key >> 61) != PH_RESIDUE) {
+    int owner = rec, local = -1;
+    if (static_cast<unsigned>(key >> 61) < PH_RESIDUE) {
       for (int d = 0; d < P_; ++d) {
         const auto& own = geoms_[d].gid;
         const auto it = std::lower_bound(own.begin(), own.begin() + geoms_[d].n_own, g);
@@ -1314,8 +1371,9 @@ class MultiRun {
         }
       }
     }
-    dom_[owner]->refresh_ctl();
-    return dom_[owner]->fault_in_run(local);
+    Domain& o = *dom_[owner];
+    const int t = std::max(0, dom_[rec]->err_iter());
+    return o.fault_for(key, dom_[rec]->err_iter(), true, o.q_of_iter(t), o.dq_of_flux(t), local);
   }
 
   void download() {
@@ -1355,7 +1413,7 @@ class MultiRun {
         ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
         wait(d, ev_res_[t - 1]);
         for (int o : src_[d]) wait(d, ev_upd_[o][t - 1]);
-        dom_[d]->launch_halo(dom_[d]->q_buf(a), 1, hdom_[d]->get(), hidx_[d]->get(), peers_q(a));
+        dom_[d]->launch_halo(dom_[d]->q_buf(a), 1, hdom_[d]->get(), hidx_[d]->get(), peers_q(a), 0);
       }
     }
     int bfin = 0;
@@ -1367,14 +1425,14 @@ class MultiRun {
           if (s >= 2)
             for (int rd : readers_[d]) wait(d, ev_dqh_[rd][k - 2]);
           if (timed && s == 0 && d == 0) ck(cudaEventRecord(kev_[0], r.stream()), "EventRecord");
-          dom_[d]->launch_sweep(a, b, s == 0);
+          dom_[d]->launch_sweep(a, b, s);
           if (timed && s == 0 && d == 0) ck(cudaEventRecord(kev_[1], r.stream()), "EventRecord");
           ck(cudaEventRecord(ev_sw_[d][k], dom_[d]->stream()), "EventRecord");
         }
         for (int d = 0; d < P_; ++d) {
           ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
           for (int o : src_[d]) wait(d, ev_sw_[o][k]);
-          dom_[d]->launch_halo(dom_[d]->dq_buf(b ^ 1), 2, hdom_[d]->get(), hidx_[d]->get(), peers_dq(b ^ 1));
+          dom_[d]->launch_halo(dom_[d]->dq_buf(b ^ 1), 2, hdom_[d]->get(), hidx_[d]->get(), peers_dq(b ^ 1), 1 + s);
           ck(cudaEventRecord(ev_dqh_[d][k], dom_[d]->stream()), "EventRecord");
         }
       }
@@ -1433,21 +1491,26 @@ __global__ void k_signal(unsigned long long* flag, unsigned long long v) {
 }
 
 // Spins (acquire, system scope) until every listed counter reaches `target`.
-// Gives up once the run has failed (every later kernel skips, so nothing is
-// left to order) or after kStallNs, recording PH_STALL so the host raises
-// instead of hanging the device.
+// Gives up early only when a failure at a stage before `guard` (the stage of
+// the kernel this wait protects) is recorded — that kernel and everything
+// after it skip, so nothing is left to order — or after kStallNs, recording
+// PH_STALL (stage 0) so the host raises instead of hanging the device.
 constexpr unsigned long long kStallNs = 30ull * 1000 * 1000 * 1000;
 
-__global__ void k_wait(WaitList w, unsigned long long target, Shared* sh) {
+__global__ void k_wait(WaitList w, unsigned long long target, Ctl* ctl, unsigned long long guard) {
   const int m = threadIdx.x;
   if (m >= w.n) return;
   const unsigned long long t0 = globaltimer();
   for (;;) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w.ptr[m]) : "memory");
-    if (v >= target || ld_volatile(&sh->err_key) != kNoErr) return;
+    if (v >= target) return;
+    const unsigned long long first = min(ld_volatile(&ctl->sh->err_stage), ld_volatile(&ctl->err_stage));
+    if (first != kNoErr && first < guard) return;
     if (globaltimer() - t0 > kStallNs) {
-      atomicMin(&sh->err_key, static_cast<unsigned long long>(PH_STALL) << 61);
+      atomicMin(&ctl->err_stage, 0ull);
+      atomicMin(&ctl->err_key, static_cast<unsigned long long>(PH_STALL) << 61);
+      atomicMin(&ctl->sh->err_stage, 0ull);
       return;
     }
     __nanosleep(256);
@@ -1475,6 +1538,7 @@ class RankRun {
     if (world < 1 || world > kMaxDomains || rank < 0 || rank >= world)
       raise(Status::argument, "rank/world out of range");
     geoms_ = decompose(ps, world, spec.part_of);
+    spi_ = (spec.order == 2 ? spec.inner : 0) + 4;
     const LocalGeom& g = geoms_[rank];
     dom_ = std::make_unique<Domain>(view_of(g), device, spec.gamma, spec.cfl, spec.det_tol, capacity, true);
     std::vector<int> srcs(g.halo_dom.begin(), g.halo_dom.end());
@@ -1577,7 +1641,7 @@ class RankRun {
     }
     // Every rank returns only after the root's residue of the last enqueued
     // iteration, so all of them observe the same error word.
-    if (rank_ != 0) wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t_));
+    if (rank_ != 0) wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t_), t_, 0);
     ck(cudaEventRecord(t1_, d.stream()), "EventRecord");
     ck(cudaStreamSynchronize(d.stream()), "rank iterate");
     float ms = 0.0f;
@@ -1589,31 +1653,36 @@ class RankRun {
   }
 
   bool failed() { return dom_->failed(); }
-  // The failing point's owner builds the reference message; the other ranks
-  // report where it failed (the Python driver forwards the owner's text).
-  Fault fault() {
-    const unsigned long long key = dom_->shared_host().err_key;
-    const unsigned phase = static_cast<unsigned>(key >> 61);
+  // This rank's own failure record (the Python driver takes the min over
+  // ranks) and the message for it: built here when the failing point is
+  // owned by this rank (or the failure is not point-specific).
+  bool has_error() const { return dom_->has_error(); }
+  unsigned long long err_stage() const { return dom_->err_stage(); }
+  unsigned long long err_key() const { return dom_->err_key(); }
+  bool owns_failure() const {
+    if (!dom_->has_error()) return false;
+    const unsigned long long key = dom_->err_key();
+    if ((key >> 61) >= PH_RESIDUE) return true;
     const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
     const LocalGeom& lg = geoms_[rank_];
-    const auto end = lg.gid.begin() + lg.n_own;
-    const auto it = std::lower_bound(lg.gid.begin(), end, g);
-    if (phase == PH_RESIDUE || phase == PH_STALL || (it != end && *it == g))
-      return dom_->fault_in_run(phase == PH_RESIDUE || phase == PH_STALL ? -1 : static_cast<int>(it - lg.gid.begin()));
-    return Fault(phase == PH_SWEEP ? Status::singular : Status::positivity,
-                 "iteration " + itos(dom_->shared_host().err_iter + 1) + ": failure at point " + itos(g) +
-                     " owned by another rank");
+    return std::binary_search(lg.gid.begin(), lg.gid.begin() + lg.n_own, g);
   }
-  // Rank owning the failing point (-1: none / not point-specific).
-  int fault_owner() const {
-    const unsigned long long key = dom_->shared_host().err_key;
-    if (key == kNoErr || (key >> 61) >= PH_RESIDUE) return -1;
+  Fault fault() {
+    if (!dom_->has_error())
+      return Fault(Status::positivity, "the run failed on another rank");
+    const unsigned long long key = dom_->err_key();
+    const unsigned phase = static_cast<unsigned>(key >> 61);
     const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
-    for (int d = 0; d < world_; ++d) {
-      const LocalGeom& lg = geoms_[d];
-      if (std::binary_search(lg.gid.begin(), lg.gid.begin() + lg.n_own, g)) return d;
+    if (!owns_failure())
+      return Fault(phase == PH_SWEEP ? Status::singular : Status::positivity,
+                   "iteration " + itos(dom_->err_iter() + 1) + ": failure at point " + itos(g) +
+                       " owned by another rank");
+    int local = -1;
+    if (phase < PH_RESIDUE) {
+      const LocalGeom& lg = geoms_[rank_];
+      local = static_cast<int>(std::lower_bound(lg.gid.begin(), lg.gid.begin() + lg.n_own, g) - lg.gid.begin());
     }
-    return -1;
+    return dom_->fault_in_run(local);
   }
   Domain& dom() { return *dom_; }
   bool is_root() const { return rank_ == 0; }
@@ -1639,12 +1708,15 @@ class RankRun {
     k_signal<<<1, 1, 0, dom_->stream()>>>(flags_.get() + slot, v);
     ++launches_;
   }
-  void wait_for(const std::vector<int>& ranks, int slot, unsigned long long v) {
+  // Waits for the ranks' `slot` counters to reach v, guarding stage `sub` of
+  // iteration t (see k_wait).
+  void wait_for(const std::vector<int>& ranks, int slot, unsigned long long v, int t, int sub) {
     if (ranks.empty()) return;
     WaitList w{};
     w.n = static_cast<int>(ranks.size());
     for (int m = 0; m < w.n; ++m) w.ptr[m] = flag_[ranks[m]] + slot;
-    k_wait<<<1, 32, 0, dom_->stream()>>>(w, v, dom_->shared());
+    const unsigned long long guard = static_cast<unsigned long long>(t) * spi_ + static_cast<unsigned>(sub);
+    k_wait<<<1, 32, 0, dom_->stream()>>>(w, v, dom_->dctl(), guard);
     ++launches_;
   }
 
@@ -1654,23 +1726,23 @@ class RankRun {
     const int a = t & 1;
     launches_ = 0;
     if (t > 0) {
-      wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t));  // residue(t-1) done
-      wait_for(src_, FL_UPD, static_cast<unsigned long long>(t));                  // owners' q(t) ready
-      d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a]);
+      wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t), t, 0);  // residue(t-1) done
+      wait_for(src_, FL_UPD, static_cast<unsigned long long>(t), t, 0);                  // owners' q(t) ready
+      d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a], 0);
       ++launches_;
     }
     int bfin = 0;
     if (spec_.order == 2) {
       for (int s = 0; s < spec_.inner; ++s) {
         const int k = t * spec_.inner + s, b = k & 1;
-        if (s >= 2) wait_for(readers_, FL_DQH, static_cast<unsigned long long>(k - 1));  // readers gathered k-2
+        if (s >= 2) wait_for(readers_, FL_DQH, static_cast<unsigned long long>(k - 1), t, 1 + s);  // readers gathered k-2
         if (timed && s == 0) ck(cudaEventRecord(kev_[0], st), "EventRecord");
-        d.launch_sweep(a, b, s == 0);
+        d.launch_sweep(a, b, s);
         launches_ += 2;  // sweep + dq halo
         if (timed && s == 0) ck(cudaEventRecord(kev_[1], st), "EventRecord");
         signal(FL_SW, static_cast<unsigned long long>(k + 1));
-        wait_for(src_, FL_SW, static_cast<unsigned long long>(k + 1));
-        d.launch_halo(d.dq_buf(b ^ 1), 2, hdom_.get(), hidx_.get(), dqp_[b ^ 1]);
+        wait_for(src_, FL_SW, static_cast<unsigned long long>(k + 1), t, 1 + s);
+        d.launch_halo(d.dq_buf(b ^ 1), 2, hdom_.get(), hidx_.get(), dqp_[b ^ 1], 1 + s);
         signal(FL_DQH, static_cast<unsigned long long>(k + 1));
       }
       bfin = ((t + 1) * spec_.inner) & 1;
@@ -1684,7 +1756,7 @@ class RankRun {
     if (rank_ == 0) {
       std::vector<int> all;
       for (int o = 1; o < world_; ++o) all.push_back(o);
-      wait_for(all, FL_UPD, static_cast<unsigned long long>(t + 1));
+      wait_for(all, FL_UPD, static_cast<unsigned long long>(t + 1), t, spi_ - 1);
       d.launch_residue();
       launches_ += 2;  // tree partial + final
       signal(FL_RES, static_cast<unsigned long long>(t + 1));
@@ -1705,7 +1777,7 @@ class RankRun {
   std::vector<void*> opened_;
   RankBlob blob_{};
   cudaEvent_t t0_ = nullptr, t1_ = nullptr, kev_[4] = {};
-  int t_ = 0, launches_ = 0;
+  int t_ = 0, launches_ = 0, spi_ = 4;
 };
 
 RankRun* rank_open(PointSet& ps, const EngineSpec& spec, int rank, int world, int device, int capacity) {
@@ -1735,7 +1807,11 @@ void rank_download(RankRun* r) { r->download(); }
 void rank_flush_l2(RankRun* r) { r->flush_l2(); }
 void rank_event_ms(const RankRun* r, double* sweep_ms, double* flux_ms) { r->last_event_ms(*sweep_ms, *flux_ms); }
 int rank_launches_per_iter(const RankRun* r) { return r->launches_per_iter(); }
-int rank_fault_owner(const RankRun* r) { return r->fault_owner(); }
+void rank_error(const RankRun* r, unsigned long long* stage, unsigned long long* key, int* owns) {
+  *stage = r->has_error() ? r->err_stage() : kNoErr;
+  *key = r->has_error() ? r->err_key() : kNoErr;
+  *owns = r->owns_failure() ? 1 : 0;
+}
 void rank_close(RankRun* r) { delete r; }
 
 RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vector<LocalGeom>& geoms) {
@@ -1748,7 +1824,7 @@ RunRecord engine_run_multi(PointSet& ps, const EngineSpec& spec, const std::vect
   trace("engine: iterated");
   if (m.failed()) {
     Fault f = m.fault();
-    rec.abort_iteration = m.root().shared_host().err_iter + 1;
+    rec.abort_iteration = m.abort_iteration();
     throw f;
   }
   m.download();
@@ -1873,7 +1949,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
   Domain d(view_of(ps, {}), spec.device, spec.gamma, spec.cfl, spec.det_tol, 1);
   d.set_strict(spec.fp_mode == 1);
   d.upload(ps.fields, true);
-  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), d.shared(), 1, -1);
+  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), d.shared(), 1, -1, 0);
   const Geo g = d.geo();
   const int n = ps.n();
   const int blocks = (n + 255) / 256;
@@ -1885,7 +1961,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
       k_qvar<<<blocks, 256, 0, st>>>(g, d.prim(), d.q_buf(0), d.gas(), d.dctl());
       break;
     case Op::q_derivatives:
-      sweep_launch(spec.fp_mode == 1, g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(), nullptr, st);
+      sweep_launch(spec.fp_mode == 1, g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(), nullptr, 0, st);
       break;
     case Op::publish:
       ck(cudaMemcpyAsync(d.dq_buf(1), scratch, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D scratch");
@@ -1934,7 +2010,7 @@ double engine_reduce(const double* v, std::int64_t n, int device) {
   DBuf<Ctl> ctl(1);
   ck(cudaMemcpy(dv.get(), v, n * sizeof(double), cudaMemcpyHostToDevice), "H2D reduce");
   DBuf<Shared> sh(1);
-  k_ctl_init<<<1, 1>>>(ctl.get(), sh.get(), 1, -1);
+  k_ctl_init<<<1, 1>>>(ctl.get(), sh.get(), 1, -1, 0);
   const int d1 = tree_depth(n);
   k_tree_partial<<<1 << d1, kTreeThreads>>>(dv.get(), n, d1, pv.get(), ps.get(), ctl.get());
   k_tree_result<<<1, 1024>>>(pv.get(), ps.get(), d1, out.get());

@@ -51,20 +51,30 @@ struct KTimer {
 
 enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_UPDATE = 3, KT_RESIDUE = 4, KT_COUNT = 5 };
 
+// Failures are ordered by STAGE first: stage = iteration * spi + sub, with
+// sub 0 = q_variables, 1+s = derivative sweep s, then flux, update, residue
+// (spi = sweeps + 4).  A kernel skips only when a failure at an EARLIER stage
+// is already recorded, so every domain still runs the stage of the first
+// failure and records its own failures there; the run's failure is the
+// minimum (stage, key) over the domains' records — exactly the reference's
+// first throw whatever the relative progress of the domains.
+
 // Run-wide control word, shared by every domain of a run (lives on the first
 // domain's device; other domains reach it over peer memory).
 struct Shared {
-  unsigned long long err_key;  // min over failures (kNoErr = none)
-  int err_iter;                // 0-based iteration of the failure (min)
-  int iter;                    // 0-based index of the iteration in flight
-  int pad[2];
+  unsigned long long err_stage;  // min failing stage over all domains (kNoErr = none)
+  int iter;                      // 0-based index of the iteration in flight
+  int pad[3];
 };
 
-// Per-domain control block: the shared word + this domain's kernel timers.
+// Per-domain control block: the shared word, this domain's own failure
+// record (all at one stage, see above) and its kernel timers.
 struct Ctl {
   Shared* sh;
   int diag_iter;  // iteration whose res/dt are kept for copy-back (this domain)
-  int pad;
+  int spi;        // stages per iteration
+  unsigned long long err_stage;  // this domain's failing stage (kNoErr = none)
+  unsigned long long err_key;    // min key at that stage
   KTimer kt[KT_COUNT];
 };
 
@@ -97,9 +107,27 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key) {
-  atomicMin(&ctl->sh->err_key, key);
-  atomicMin(&ctl->sh->err_iter, *reinterpret_cast<volatile int*>(&ctl->sh->iter));
+__device__ __forceinline__ unsigned long long stage_of(const Ctl* ctl, int sub) {
+  const int it = *reinterpret_cast<const volatile int*>(&ctl->sh->iter);
+  return static_cast<unsigned long long>(it) * static_cast<unsigned>(ctl->spi) + static_cast<unsigned>(sub);
+}
+// Stage subs of the per-iteration kernels after the sweeps.
+__device__ __forceinline__ int sub_flux(const Ctl* ctl) { return ctl->spi - 3; }
+__device__ __forceinline__ int sub_update(const Ctl* ctl) { return ctl->spi - 2; }
+__device__ __forceinline__ int sub_residue(const Ctl* ctl) { return ctl->spi - 1; }
+
+// True when a failure at a stage before `sub` of this iteration is recorded.
+__device__ __forceinline__ bool skip_stage(const Ctl* ctl, int sub) {
+  const unsigned long long first =
+      min(ld_volatile(&ctl->sh->err_stage), ld_volatile(&ctl->err_stage));
+  return first != kNoErr && first < stage_of(ctl, sub);
+}
+
+__device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int sub) {
+  const unsigned long long st = stage_of(ctl, sub);
+  atomicMin(&ctl->err_stage, st);
+  atomicMin(&ctl->err_key, key);
+  atomicMin(&ctl->sh->err_stage, st);
 }
 
 // ---- per-kernel device timing (globaltimer; one record per kernel class) ----
@@ -149,7 +177,7 @@ __global__ void k_qvar(Geo g, const D4* prim, D4* q, Gas gas, Ctl* ctl) {
   if (i < g.n) {
     const D4 s = ld4_rw(prim + i);
     if (!(s.a > 0.0) || !(s.d > 0.0)) {
-      raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0));
+      raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0), 0);
     } else {
       st4(q + i, q_from_prim(s.a, s.b, s.c, s.d, gas.gm1));
     }
@@ -164,11 +192,11 @@ __global__ void k_qvar(Geo g, const D4* prim, D4* q, Gas gas, Ctl* ctl) {
 template <bool S, int MB>
 __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__ q,
                                                    const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
-                                                   Gas gas, Ctl* ctl, unsigned long long* iter_t0) {
+                                                   Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
   using A = Ar<S>;
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_SWEEP);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, 1 + sweep);
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n; i += gridDim.x * blockDim.x) {
     const double2 pi = g.xy[i];
@@ -195,7 +223,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
     }
     const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
     if (!(det > gas.det_tol)) {
-      raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0));
+      raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0), 1 + sweep);
     } else {
       D4 fx, fy;
       fx.a = A::sub(A::mul(syy, bx[0]), A::mul(sxy, by[0])) / det;
@@ -208,6 +236,92 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
       fy.d = A::sub(A::mul(sxx, by[3]), A::mul(sxy, bx[3])) / det;
       st4(dq_out + 2 * i, fx);
       st4(dq_out + 2 * i + 1, fy);
+    }
+  }
+  __syncthreads();
+  ktimer_end(ctl, KT_SWEEP, iter_t0);
+}
+
+// Two lanes per point: lane h owns components {2h, 2h+1} of q, qx, qy and
+// loads only its 16-byte halves (the pair of lanes still touches each 32-byte
+// sector once per record), which halves the registers per thread and doubles
+// the loads in flight.  Both lanes form the geometric sums and det (identical
+// values); per-component arithmetic is unchanged, so S = true stays bitwise.
+// S = false regroups the defect correction as
+//   df = (qn - qi) - 0.5 (dx (qxn - qxi) + dy (qyn - qyi))
+// and divides once (det reciprocal).
+__device__ __forceinline__ double2 ld2(const double* p) {
+  double2 v;
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st2(double* p, double2 v) {
+  asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+template <bool S, int MB>
+__global__ void __launch_bounds__(256, MB) k_sweep2(Geo g, const D4* __restrict__ q,
+                                                    const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
+                                                    Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
+  using A = Ar<S>;
+  __shared__ int s_skip;
+  ktimer_begin(ctl, KT_SWEEP);
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, 1 + sweep);
+  __syncthreads();
+  const int h = threadIdx.x & 1;
+  const double* qd = reinterpret_cast<const double*>(q) + 2 * h;
+  const double* dd = reinterpret_cast<const double*>(dq_in) + 2 * h;
+  const long long n2 = 2ll * g.n;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; !s_skip && t < n2;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(t >> 1);
+    const double2 pi = g.xy[i];
+    const double2 qi = ld2(qd + 4 * i), qxi = ld2(dd + 8 * i), qyi = ld2(dd + 8 * i + 4);
+    double sxx = 0.0, sxy = 0.0, syy = 0.0;
+    double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
+    int e0, k;
+    stencil_of(g, i, e0, k);
+    for (int e = e0; e < e0 + k; ++e) {
+      const int nb = g.nbr[e];
+      const double2 pn = g.xy[nb];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const double2 qn = ld2(qd + 4 * nb), qxn = ld2(dd + 8 * nb), qyn = ld2(dd + 8 * nb + 4);
+      sxx = A::add(sxx, A::mul(dx, dx));
+      sxy = A::add(sxy, A::mul(dx, dy));
+      syy = A::add(syy, A::mul(dy, dy));
+      double df0, df1;
+      if constexpr (S) {
+        df0 = X::sub(corrected<true>(qn.x, qxn.x, qyn.x, dx, dy), corrected<true>(qi.x, qxi.x, qyi.x, dx, dy));
+        df1 = X::sub(corrected<true>(qn.y, qxn.y, qyn.y, dx, dy), corrected<true>(qi.y, qxi.y, qyi.y, dx, dy));
+      } else {
+        df0 = fma(-0.5, fma(dx, qxn.x - qxi.x, dy * (qyn.x - qyi.x)), qn.x - qi.x);
+        df1 = fma(-0.5, fma(dx, qxn.y - qxi.y, dy * (qyn.y - qyi.y)), qn.y - qi.y);
+      }
+      bx0 = A::add(bx0, A::mul(dx, df0));
+      by0 = A::add(by0, A::mul(dy, df0));
+      bx1 = A::add(bx1, A::mul(dx, df1));
+      by1 = A::add(by1, A::mul(dy, df1));
+    }
+    const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
+    if (!(det > gas.det_tol)) {
+      if (h == 0) raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0), 1 + sweep);
+    } else {
+      double2 fx, fy;
+      if constexpr (S) {
+        fx.x = A::sub(A::mul(syy, bx0), A::mul(sxy, by0)) / det;
+        fx.y = A::sub(A::mul(syy, bx1), A::mul(sxy, by1)) / det;
+        fy.x = A::sub(A::mul(sxx, by0), A::mul(sxy, bx0)) / det;
+        fy.y = A::sub(A::mul(sxx, by1), A::mul(sxy, bx1)) / det;
+      } else {
+        const double r = 1.0 / det;
+        fx.x = (syy * bx0 - sxy * by0) * r;
+        fx.y = (syy * bx1 - sxy * by1) * r;
+        fy.x = (sxx * by0 - sxy * bx0) * r;
+        fy.y = (sxx * by1 - sxy * bx1) * r;
+      }
+      double* o = reinterpret_cast<double*>(dq_out) + 8 * static_cast<long long>(i) + 2 * h;
+      st2(o, fx);
+      st2(o + 4, fy);
     }
   }
   __syncthreads();
@@ -272,7 +386,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
   __shared__ int s_skip;
 
   ktimer_begin(a.ctl, KT_FLUX);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_flux(a.ctl));
   __syncthreads();
   const int lane = threadIdx.x % W;
   const int slot = threadIdx.x / W;
@@ -312,7 +426,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
       }
       FluxState fi, fn;
       ok = reconstruct2<S>(ti, tn, a.gas, fi, fn) && ok;
-      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j));
+      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
       AxisTerms at[4];
       axis_terms4<S>(fi, fn, at);
       const bool store = act && ok;
@@ -376,7 +490,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
         }
         const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
         if (!(det > a.gas.det_tol)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot));
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot), sub_flux(a.ctl));
         } else {
 #pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
@@ -427,7 +541,7 @@ struct UpdateArgs {
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_UPDATE);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&a.ctl->sh->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_update(a.ctl));
   __syncthreads();
   const int ip = blockIdx.x * blockDim.x + threadIdx.x;
   const Geo& g = a.g;
@@ -462,7 +576,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
         // keep the failing conserved value for the diagnostic message
         a.dt[ip] = m > 0.0 ? p : m;
         a.which[ip] = m > 0.0 ? 1.0 : 0.0;
-        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0));
+        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0), sub_update(a.ctl));
       } else {
         if (g.kind[ip] == KIND_WALL) {
           const double2 nv = g.nrm[ip];
@@ -492,8 +606,8 @@ struct PeerTab {
 };
 
 __global__ void k_halo(D4* dst, int recs, int n_own, int n_halo, const int* hdom, const int* hidx,
-                       PeerTab src, const Shared* sh) {
-  if (ld_volatile(&sh->err_key) != kNoErr) return;  // keep the failing iteration's halo intact
+                       PeerTab src, const Ctl* ctl, int sub) {
+  if (skip_stage(ctl, sub)) return;  // keep the failing stage's buffers intact
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_halo * recs; t += gridDim.x * blockDim.x) {
     const int h = t / recs, r = t - h * recs;
     const D4* s = src.base[hdom[h]] + static_cast<size_t>(hidx[h]) * recs + r;
@@ -522,7 +636,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (i >= g.n || g.kind[i] == KIND_OUTER) return;
   const D4 s = ld4_rw(prim + i);
   if (!(s.a > 0.0) || !(s.d > 0.0)) {  // conserved_from_primitives require_valid
-    raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0));
+    raise_err(ctl, err_key(PH_QVAR, g.part[i], gidx(g, i), 0, 0), 0);
     return;
   }
   const D4 r = ld4(res + i);
@@ -537,7 +651,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (!(m > 0.0)) {
     dt[i] = m;
     which[i] = 0.0;
-    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0));
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0), 0);
     return;
   }
   double u1 = mx / m, u2 = my_ / m;
@@ -545,7 +659,7 @@ __global__ void k_op_update(Geo g, D4* prim, const D4* res, double* dt, Gas gas,
   if (!(p > 0.0)) {
     dt[i] = p;
     which[i] = 1.0;
-    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0));
+    raise_err(ctl, err_key(PH_UPDATE, g.part[i], gidx(g, i), 0, 0), 0);
     return;
   }
   if (g.kind[i] == KIND_WALL) {
@@ -625,7 +739,7 @@ __global__ void __launch_bounds__(kTreeThreads)
   __shared__ long long ss[2][kTreeThreads];
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_RESIDUE);
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl));
   __syncthreads();
   if (!s_skip) {
     long long lo, hi, tlo, thi;
@@ -654,7 +768,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
   __shared__ int s_skip;
-  if (threadIdx.x == 0) s_skip = ld_volatile(&ctl->sh->err_key) != kNoErr;
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl));
   __syncthreads();
   if (s_skip) return;
   const int m = 1 << d1;
@@ -668,7 +782,7 @@ __global__ void __launch_bounds__(1024)
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
     const int it = ctl->sh->iter;
     if (!isfinite(res)) {
-      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0));
+      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0), sub_residue(ctl));
     } else {
       if (history) history[it] = res;
       if (iter_t1) iter_t1[it] = globaltimer();

@@ -84,7 +84,8 @@ void rank_download(RankRun* r);
 void rank_flush_l2(RankRun* r);
 void rank_event_ms(const RankRun* r, double* sweep_ms, double* flux_ms);
 int rank_launches_per_iter(const RankRun* r);
-int rank_fault_owner(const RankRun* r);
+// This rank's failure record (stage, key; ~0 = none) and whether it owns the failing point.
+void rank_error(const RankRun* r, unsigned long long* stage, unsigned long long* key, int* owns);
 void rank_close(RankRun* r);
 
 // Per-phase operators on the whole cloud (reference kernels.hpp:25-63).

@@ -593,11 +593,17 @@ int lskum_b200_rank_residues(const lskum_b200_rank* r, double* out, int cap, int
   });
 }
 
-int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, int* fault_owner) {
+int lskum_b200_rank_info(const lskum_b200_rank* r, int* launches_per_iter, uint64_t* err_stage, uint64_t* err_key,
+                         int* owns_failure) {
   NONNULL(r);
   return guard([&] {
     if (launches_per_iter) *launches_per_iter = lskb::rank_launches_per_iter(r->run);
-    if (fault_owner) *fault_owner = lskb::rank_fault_owner(r->run);
+    unsigned long long st = 0, key = 0;
+    int owns = 0;
+    lskb::rank_error(r->run, &st, &key, &owns);
+    if (err_stage) *err_stage = st;
+    if (err_key) *err_key = key;
+    if (owns_failure) *owns_failure = owns;
   });
 }
 

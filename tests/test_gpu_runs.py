@@ -199,7 +199,7 @@ def test_multi_domain_halo_engine_is_bitwise_single_domain(bump_cloud_arrays, gp
         assert other.fields_equal(base), (gpus, order)
 
 
-@pytest.mark.parametrize("gpus,parts", [(4, 1), (8, 8)])
+@pytest.mark.parametrize("gpus,parts", [(4, 1), (8, 8), (4, 8), (3, 2)])
 def test_multi_domain_abort_matches_reference(bump_cloud_arrays, golden, gpus, parts):
     c, prim0 = bump_cloud_arrays
     _, meta = golden

@@ -43,24 +43,22 @@ def test_rank_setup_failure_is_agreed(bump_cloud_arrays):
     assert out[0][1:] == out[1][1:]
 
 
-def test_agree_picks_owner_message():
-    """The error every rank raises is the owning rank's (reference wording)."""
+def test_first_failure_is_min_stage_then_key_owner_message():
+    """The error every rank raises is the smallest (stage, key) record, in the
+    words of the rank owning the failing point (reference wording)."""
     from paper_2403_13287_b200 import lskum as L
 
-    class Fake(L.RankSession):
-        def __init__(self, gathered):
-            self._x = lambda obj: gathered
-            self._h = None
-
-    msgs = [(5, "iteration 3: failure at point 7 owned by another rank", 1),
-            (5, "iteration 3: q-derivative solve singular at point 7", 1)]
-    with pytest.raises(L.LskumError) as e:
-        Fake(msgs)._agree(0)
-    assert e.value.message == msgs[1][1]
-    with pytest.raises(L.LskumError) as e:
-        Fake([(0, "", -1), (6, "solver diverged", -1)])._agree(0)
-    assert e.value.message == "solver diverged"
-    Fake([(0, "", -1), (0, "", -1)])._agree(0)  # no error anywhere: returns
+    N = L.NO_ERROR
+    owner_msg = "iteration 3: flux reconstruction failed on edge (7, 9): q-state with q3 >= 0 (q3=0.1)"
+    recs = [(6, "iteration 3: failure at point 7 owned by another rank", 40, 5, 0),
+            (6, owner_msg, 40, 5, 1),
+            (5, "iteration 3: later-stage failure", 41, 1, 1),
+            (6, "the run failed on another rank", N, N, 0)]
+    assert L.first_failure(recs) == (6, owner_msg)
+    # a lower stage wins over a lower key
+    assert L.first_failure([(5, "a", 38, 9, 1), (6, "b", 39, 0, 1)]) == (5, "a")
+    assert L.first_failure([(0, "", N, N, 0), (0, "", N, N, 0)]) is None
+    assert L.first_failure([(0, "", N, N, 0), (1, "setup", N, N, 0)]) == (1, "setup")
 
 
 def _single(c, prim0, iters, **cfg):
