@@ -336,6 +336,7 @@ __global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, 
   ctl->sh = sh;
   ctl->diag_iter = diag_iter;
   ctl->spi = spi;
+  ctl->it = 0;
   ctl->err_stage = kNoErr;
   ctl->err_key = kNoErr;
   if (own_shared) {
@@ -878,7 +879,7 @@ class Domain {
     ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "EventElapsed");
     total_ms_ += ms;
     refresh_ctl();
-    done_ = hsh_.get()->iter;
+    done_ = completed();
     return ms;
   }
 
@@ -917,6 +918,15 @@ class Domain {
     return (st == kNoErr || spi <= 0) ? 0 : static_cast<int>(st / static_cast<unsigned>(spi));
   }
   const Shared& shared_host() const { return *hsh_.get(); }
+  // Iterations completed without failure (valid after refresh_ctl): the
+  // shared counter also advances past failed iterations, so it is capped at
+  // the iteration of the run's first failing stage.
+  int completed() const {
+    const Shared& s = *hsh_.get();
+    const int spi = hctl_.get()->spi;
+    if (s.err_stage == kNoErr || spi <= 0) return s.iter;
+    return std::min<long long>(s.iter, static_cast<long long>(s.err_stage / static_cast<unsigned>(spi)));
+  }
 
   // CUDA-event times of the first sweep and the flux kernel of the last
   // iteration of the last graph replay (valid after iterate()).
@@ -1329,7 +1339,7 @@ class MultiRun {
     float ms = 0.0f;
     ck(cudaEventElapsedTime(&ms, t0_, t1_), "EventElapsed");
     r.refresh_ctl();
-    const int done = r.shared_host().iter;
+    const int done = r.completed();
     for (int d = 0; d < P_; ++d) dom_[d]->set_done(done);
     r.add_ms(ms);
     return ms;
@@ -1647,7 +1657,7 @@ class RankRun {
     float ms = 0.0f;
     ck(cudaEventElapsedTime(&ms, t0_, t1_), "EventElapsed");
     d.refresh_ctl();
-    d.set_done(d.shared_host().iter);
+    d.set_done(d.completed());
     d.add_ms(ms);
     return ms;
   }

@@ -73,6 +73,10 @@ struct Ctl {
   Shared* sh;
   int diag_iter;  // iteration whose res/dt are kept for copy-back (this domain)
   int spi;        // stages per iteration
+  int it;         // 0-based iteration this domain's stream is in: advanced by
+                  // the last block of every k_update, so each kernel of an
+                  // iteration sees that iteration's index (failed or not)
+  int pad_;
   unsigned long long err_stage;  // this domain's failing stage (kNoErr = none)
   unsigned long long err_key;    // min key at that stage
   KTimer kt[KT_COUNT];
@@ -107,9 +111,13 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__device__ __forceinline__ unsigned long long stage_of(const Ctl* ctl, int sub) {
-  const int it = *reinterpret_cast<const volatile int*>(&ctl->sh->iter);
-  return static_cast<unsigned long long>(it) * static_cast<unsigned>(ctl->spi) + static_cast<unsigned>(sub);
+// The residue kernels run after k_update advanced `it`, hence `back`.
+__device__ __forceinline__ int iter_of(const Ctl* ctl, int back = 0) {
+  return *reinterpret_cast<const volatile int*>(&ctl->it) - back;
+}
+__device__ __forceinline__ unsigned long long stage_of(const Ctl* ctl, int sub, int back = 0) {
+  return static_cast<unsigned long long>(iter_of(ctl, back)) * static_cast<unsigned>(ctl->spi) +
+         static_cast<unsigned>(sub);
 }
 // Stage subs of the per-iteration kernels after the sweeps.
 __device__ __forceinline__ int sub_flux(const Ctl* ctl) { return ctl->spi - 3; }
@@ -117,14 +125,14 @@ __device__ __forceinline__ int sub_update(const Ctl* ctl) { return ctl->spi - 2;
 __device__ __forceinline__ int sub_residue(const Ctl* ctl) { return ctl->spi - 1; }
 
 // True when a failure at a stage before `sub` of this iteration is recorded.
-__device__ __forceinline__ bool skip_stage(const Ctl* ctl, int sub) {
+__device__ __forceinline__ bool skip_stage(const Ctl* ctl, int sub, int back = 0) {
   const unsigned long long first =
       min(ld_volatile(&ctl->sh->err_stage), ld_volatile(&ctl->err_stage));
-  return first != kNoErr && first < stage_of(ctl, sub);
+  return first != kNoErr && first < stage_of(ctl, sub, back);
 }
 
-__device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int sub) {
-  const unsigned long long st = stage_of(ctl, sub);
+__device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int sub, int back = 0) {
+  const unsigned long long st = stage_of(ctl, sub, back);
   atomicMin(&ctl->err_stage, st);
   atomicMin(&ctl->err_key, key);
   atomicMin(&ctl->sh->err_stage, st);
@@ -135,7 +143,8 @@ __device__ __forceinline__ void ktimer_begin(Ctl* ctl, int k) {
   if (threadIdx.x == 0) atomicMin(&ctl->kt[k].t0, globaltimer());
 }
 // Call after a __syncthreads() that every thread of the block reaches.
-__device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* iter_t0) {
+__device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* iter_t0,
+                                           bool advance = false) {
   if (threadIdx.x == 0) {
     atomicMax(&ctl->kt[k].t1, globaltimer());
     __threadfence();
@@ -147,7 +156,8 @@ __device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* 
       ctl->kt[k].done = 0;
       ctl->kt[k].total_ns += t1 - t0;
       ctl->kt[k].launches += 1;
-      if (iter_t0) iter_t0[ctl->sh->iter] = t0;
+      if (iter_t0) iter_t0[ctl->it] = t0;
+      if (advance) ctl->it += 1;
     }
   }
 }
@@ -546,7 +556,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   const int ip = blockIdx.x * blockDim.x + threadIdx.x;
   const Geo& g = a.g;
   if (!s_skip && ip < g.n) {
-    const bool diag = a.ctl->sh->iter == a.ctl->diag_iter;
+    const bool diag = iter_of(a.ctl) == a.ctl->diag_iter;
     if (g.kind[ip] == KIND_OUTER) {
       st4(a.q_next + ip, ld4(a.q + ip));
       a.mag[gidx(g, ip)] = 0.0;
@@ -593,7 +603,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
     }
   }
   __syncthreads();
-  ktimer_end(a.ctl, KT_UPDATE, nullptr);
+  ktimer_end(a.ctl, KT_UPDATE, nullptr, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -739,7 +749,7 @@ __global__ void __launch_bounds__(kTreeThreads)
   __shared__ long long ss[2][kTreeThreads];
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_RESIDUE);
-  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl));
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl), 1);
   __syncthreads();
   if (!s_skip) {
     long long lo, hi, tlo, thi;
@@ -768,7 +778,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
   __shared__ int s_skip;
-  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl));
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl), 1);
   __syncthreads();
   if (s_skip) return;
   const int m = 1 << d1;
@@ -780,13 +790,13 @@ __global__ void __launch_bounds__(1024)
   tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
   if (threadIdx.x == 0) {
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
-    const int it = ctl->sh->iter;
+    const int it = iter_of(ctl, 1);
     if (!isfinite(res)) {
-      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0), sub_residue(ctl));
+      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0), sub_residue(ctl), 1);
     } else {
       if (history) history[it] = res;
       if (iter_t1) iter_t1[it] = globaltimer();
-      ctl->sh->iter = it + 1;
+      ctl->sh->iter = it + 1;  // iterations completed (residue recorded)
     }
   }
 }
