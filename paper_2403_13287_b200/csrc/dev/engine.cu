@@ -247,6 +247,23 @@ void flux_launch(int W, bool strict, const FluxArgs& a, std::size_t smem, cudaSt
   else flux_launch_s<false>(W, a, smem, st);
 }
 
+// Fast-mode flux: the weighted kernel (LSKUM_FLUX_W=0 selects the per-iteration
+// solve kernel k_flux instead).
+bool flux_weighted() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_FLUX_W");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+void flux_w_launch(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                   cudaStream_t st) {
+  const int groups = (a.g.n + 3) / 4;
+  const int blocks = std::max(1, std::min((groups + 7) / 8, resident_blocks(k_flux_w<2>, 7)));
+  k_flux_w<2><<<blocks, 256, 0, st>>>(a, w1, w2, sing);
+}
+
 // Depth of the per-block nodes of the residue tree: at most ~8 values per
 // thread (256 threads per block), at most 1024 blocks (one block folds the
 // partials).
@@ -477,6 +494,7 @@ class Domain {
     kfix_ = kmax_;
     for (int i = 0; i < n_ && kfix_ > 0; ++i)
       if (gv.off[i + 1] - gv.off[i] != kmax_ || gv.off[i] != static_cast<std::int64_t>(i) * kmax_) kfix_ = 0;
+    nnz_ = gv.nnz;
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
     stride_ = flux_stride(kmax_);
@@ -715,6 +733,7 @@ class Domain {
     inner_ = inner;
     strict_ = fp_mode == 1;
     chunk_ = std::max(1, chunk);
+    if (!strict_ && flux_weighted()) ensure_weights();
     const std::size_t n = static_cast<std::size_t>(n_), nl = static_cast<std::size_t>(n_loc_);
     ck(cudaMemsetAsync(dq_[0].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
@@ -742,6 +761,28 @@ class Domain {
   }
 
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
+
+  // Geometry-only split-stencil weights for the fast flux kernel (once per
+  // domain); the zero-offset table w2 only exists when such pairs do.
+  void ensure_weights() {
+    if (weights_) return;
+    const int blocks = (n_ + 255) / 256;
+    DBuf<unsigned long long> zc(1, st_);
+    ck(cudaMemsetAsync(zc.get(), 0, sizeof(unsigned long long), st_), "memset");
+    k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, nullptr, nullptr, nullptr, zc.get());
+    unsigned long long zeros = 0;
+    ck(cudaMemcpyAsync(&zeros, zc.get(), sizeof zeros, cudaMemcpyDeviceToHost, st_), "D2H zero pairs");
+    ck(cudaStreamSynchronize(st_), "weights count");
+    const std::size_t nnz = static_cast<std::size_t>(std::max<std::int64_t>(1, nnz_));
+    w1_.alloc(nnz, st_);
+    if (zeros) w2_.alloc(nnz, st_);
+    sing_.alloc(static_cast<std::size_t>(std::max(1, n_)), st_);
+    k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, w1_.get(), w2_.get(), sing_.get(),
+                                                          zc.get());
+    ck(cudaGetLastError(), "k_flux_weights");
+    ck(cudaStreamSynchronize(st_), "weights");
+    weights_ = true;
+  }
 
   // Event record that also fires when captured into a graph (an external
   // event-record node); a plain captured cudaEventRecord only orders work.
@@ -773,7 +814,8 @@ class Domain {
     fa.stride = stride_;
     fa.mask = 0xF;
     fa.first = 1;
-    flux_launch(W_, strict_, fa, smem_, st_);
+    if (!strict_ && weights_) flux_w_launch(fa, w1_.get(), w2_.get(), sing_.get(), st_);
+    else flux_launch(W_, strict_, fa, smem_, st_);
   }
   void launch_update(int a) {
     UpdateArgs ua;
@@ -1094,6 +1136,10 @@ class Domain {
   double* mag_out_ = nullptr;
   DBuf<long long> psz_;
   DBuf<D4> prim_, q_[2], dq_[2], res_;
+  std::int64_t nnz_ = 0;
+  DBuf<double2> w1_, w2_;       // least-squares weights of the split stencils (fast mode)
+  DBuf<std::uint8_t> sing_;     // first singular split direction per point
+  bool weights_ = false;
   DBuf<Ctl> ctl_;
   DBuf<Shared> sh_;
   Shared* shared_ = nullptr;

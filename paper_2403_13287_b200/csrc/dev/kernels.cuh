@@ -533,6 +533,174 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
 }
 
+// ---------------------------------------------------------------------------
+// Flux residual, fp_mode fast: least-squares weights instead of per-iteration
+// solves.  Each direction's derivative (kernels.cpp:37-64)
+//   D_d = (syy_d bx_d - sxy_d by_d) / det_d,   bx_d = sum_{j in d} dx_j dG_j, ...
+// (y directions: (sxx_d by_d - sxy_d bx_d) / det_d) is linear in the pair
+// differences dG_j, so D_d = sum_{j in d} w_dj dG_j with geometry-only weights
+//   w_dj = (syy_d dx_j - sxy_d dy_j) / det_d   (x)   (sxx_d dy_j - sxy_d dx_j) / det_d   (y).
+// k_flux_weights computes them once per run; the residual sum_d D_d becomes
+// one dot product per pair and a shuffle reduction over the pair lanes — no
+// shared-memory transpose, no block barriers, no divisions per iteration.
+// Per pair e: w1[e] = (weight in the pair's x direction: Gx+ if dx <= 0 else
+// Gx-, weight in its y direction: Gy+ if dy <= 0 else Gy-); w2[e] = (weight in
+// Gx- when dx == 0, in Gy- when dy == 0) — a zero offset belongs to both
+// halves (only allocated when such pairs exist).  det is formed with the
+// reference's exact operation sequence, so the singular-stencil decision
+// `!(det > det_tol)` is bitwise the reference's; sing[i] holds the first
+// singular direction of point i (0xFF: none), raised by the flux kernel.
+__global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, std::uint8_t* sing,
+                               unsigned long long* zero_pairs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  int e0, k;
+  stencil_of(g, i, e0, k);
+  if (g.kind[i] == KIND_OUTER) {
+    if (w1)
+      for (int j = 0; j < k; ++j) w1[e0 + j] = make_double2(0.0, 0.0);
+    if (sing) sing[i] = 0xFF;
+    return;
+  }
+  const double2 pi = g.xy[i];
+  if (!w1) {  // counting pass
+    unsigned long long z = 0;
+    for (int j = 0; j < k; ++j) {
+      const double2 pn = g.xy[g.nbr[e0 + j]];
+      z += (X::sub(pn.x, pi.x) == 0.0 || X::sub(pn.y, pi.y) == 0.0) ? 1 : 0;
+    }
+    if (z) atomicAdd(zero_pairs, z);
+    return;
+  }
+  double sxx[4] = {0.0, 0.0, 0.0, 0.0}, sxy[4] = {0.0, 0.0, 0.0, 0.0}, syy[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int j = 0; j < k; ++j) {
+    const double2 pn = g.xy[g.nbr[e0 + j]];
+    const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const double dd = d < 2 ? dx : dy;
+      if (!((d & 1) ? dd >= 0.0 : dd <= 0.0)) continue;
+      sxx[d] = X::add(sxx[d], X::mul(dx, dx));
+      sxy[d] = X::add(sxy[d], X::mul(dx, dy));
+      syy[d] = X::add(syy[d], X::mul(dy, dy));
+    }
+  }
+  double rdet[4];
+  int first_sing = 0xFF;
+#pragma unroll
+  for (int d = 3; d >= 0; --d) {
+    const double det = X::sub(X::mul(sxx[d], syy[d]), X::mul(sxy[d], sxy[d]));
+    const bool ok = det > det_tol;
+    if (!ok) first_sing = d;
+    rdet[d] = ok ? 1.0 / det : 0.0;
+  }
+  sing[i] = static_cast<std::uint8_t>(first_sing);
+  auto wt = [&](int d, double dx, double dy) {
+    return d < 2 ? (syy[d] * dx - sxy[d] * dy) * rdet[d] : (sxx[d] * dy - sxy[d] * dx) * rdet[d];
+  };
+  for (int j = 0; j < k; ++j) {
+    const double2 pn = g.xy[g.nbr[e0 + j]];
+    const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+    w1[e0 + j] = make_double2(wt(dx <= 0.0 ? 0 : 1, dx, dy), wt(dy <= 0.0 ? 2 : 3, dx, dy));
+    if (w2) w2[e0 + j] = make_double2(dx == 0.0 ? wt(1, dx, dy) : 0.0, dy == 0.0 ? wt(3, dx, dy) : 0.0);
+  }
+}
+
+// Eight lanes per point (one per stencil neighbour, looping for k > 8), four
+// points per warp, warps independent (persistent grid-stride over groups of
+// 4 points).  Phase A is the same convergent pair evaluation as k_flux; the
+// pair's contribution sum_c w dG is reduced across the 8 lanes with shuffles.
+template <int MB>
+__global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* __restrict__ w1,
+                                                    const double2* __restrict__ w2,
+                                                    const std::uint8_t* __restrict__ sing) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  using A = Ar<false>;
+  __shared__ int s_skip;
+  ktimer_begin(a.ctl, KT_FLUX);
+  if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_flux(a.ctl));
+  __syncthreads();
+  const int lane = threadIdx.x & 7;
+  const int sub = (threadIdx.x >> 3) & 3;
+  const Geo& g = a.g;
+  const int groups = (g.n + 3) >> 2;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; !s_skip && grp < groups; grp += nwarps) {
+    const int i = grp * 4 + sub;
+    const int ic = i < g.n ? i : g.n - 1;  // clamped for loads
+    const bool live = i < g.n && g.kind[ic] != KIND_OUTER;
+    int k = 0, e0 = 0;
+    if (live) stencil_of(g, i, e0, k);
+    const int kwarp = __reduce_max_sync(kFull, k);
+    if (live && lane == 0) {
+      const unsigned sd = sing[i];
+      if (sd != 0xFFu) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
+    }
+    const double2 pi = g.xy[ic];
+    const D4 qi = ld4(a.q + ic), qxi = ld4(a.dq + 2 * ic), qyi = ld4(a.dq + 2 * ic + 1);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int jb = 0; jb < kwarp; jb += 8) {
+      const int j = jb + lane;
+      const bool act = live && j < k;
+      const int nb = act ? g.nbr[e0 + j] : ic;
+      const double2 w = act ? w1[e0 + j] : make_double2(0.0, 0.0);
+      const double2 pn = g.xy[nb];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+      double ti[4], tn[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        ti[c] = corrected<false>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
+        tn[c] = corrected<false>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
+      }
+      bool ok = ti[3] < 0.0 && tn[3] < 0.0;
+      if (!ok) {  // q3 >= 0 has no state: evaluate a dummy one, add nothing
+        ti[3] = -1.0;
+        tn[3] = -1.0;
+      }
+      FluxState fi, fn;
+      ok = reconstruct2<false>(ti, tn, a.gas, fi, fn) && ok;
+      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
+      AxisTerms at[4];
+      axis_terms4<false>(fi, fn, at);
+      const bool store = act && ok;
+      const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
+      // dG = gn - gi is an explicitly rounded subtraction: a contracted
+      // fma(rho_n, x_n, -gi) would leave ~1 ulp where the states are equal
+      // (the free stream must stay an exact fixed point).
+      double gi[4], gn[4];
+      split_flux<false>(fi, at[0], 0, !(dx <= 0.0), gi);
+      split_flux<false>(fn, at[1], 0, !(dx <= 0.0), gn);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = fma(wx, X::sub(gn[c], gi[c]), acc[c]);
+      split_flux<false>(fi, at[2], 1, !(dy <= 0.0), gi);
+      split_flux<false>(fn, at[3], 1, !(dy <= 0.0), gn);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
+      // a zero offset belongs to both half stencils: add the minus direction
+      if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
+        const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? w2[e0 + j] : make_double2(0.0, 0.0);
+        split_flux<false>(fi, at[0], 0, true, gi);
+        split_flux<false>(fn, at[1], 0, true, gn);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = fma(v.x, X::sub(gn[c], gi[c]), acc[c]);
+        split_flux<false>(fi, at[2], 1, true, gi);
+        split_flux<false>(fn, at[3], 1, true, gn);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = fma(v.y, X::sub(gn[c], gi[c]), acc[c]);
+      }
+    }
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = A::add(acc[c], __shfl_xor_sync(kFull, acc[c], o));
+    }
+    if (live && lane == 0) st4(a.res + i, D4{acc[0], acc[1], acc[2], acc[3]});
+  }
+  __syncthreads();
+  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+}
+
 // Local time step + forward-Euler update + wall slip + next q-variables +
 // residue summand, one thread per point (kernels.cpp:68-80, 160-223).
 struct UpdateArgs {

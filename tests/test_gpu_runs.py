@@ -220,3 +220,32 @@ def test_multi_domain_session_pieces_equal_single_run(bump_cloud_arrays):
         assert np.array_equal(s.residues(), rw.residues())
         s.download()
     assert pc.fields_equal(whole)
+
+
+def _grid_cloud():
+    """20x20 unjittered rectangle: many pairs with a zero x or y offset, which
+    belong to both half stencils of that axis (kernels.cpp:32-35)."""
+    return P.orc_generate_rect(20, 20, 0.0, 11, 8)
+
+
+@pytest.mark.parametrize("fp_mode", ["strict", "fast"])
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("cloud", ["bump", "grid"])
+def test_solver_flux_residual_matches_oracle(bump_cloud_arrays, cloud, order, fp_mode):
+    """The solver loop's flux kernel (fast mode: geometry-only split-stencil
+    weights, k_flux_w) against the oracle after one iteration: residual slot
+    and updated primitives within the reference's 1e-12 oracle tolerance."""
+    if cloud == "bump":
+        c, prim0 = bump_cloud_arrays
+    else:
+        c = _grid_cloud()
+        prim0 = P.center_bump(c)
+    want = P.orc_run(c, iters=1, order=order, prim0=prim0)
+    assert want.code == 0, want.msg
+    pc, res = bump_run(c, prim0, 1, order=order, fp_mode=fp_mode)
+    f = pc.fields()
+    live = c.kind != 2
+    assert np.abs(want.store[live, 16:20]).max() > 1e-4
+    assert rel_err(f[live, 16:20], want.store[live, 16:20]) <= 1e-12
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-12
+    assert rel_seq(res.residues(), want.residue) <= 1e-10
