@@ -158,13 +158,15 @@ void flux_launch_t(const FluxArgs& a, std::size_t smem, cudaStream_t st) {
 
 // Derivative sweep launch: strict (bitwise) or FMA variant, resident blocks per
 // SM from LSKUM_SWEEP_MINB (2 | 3 | 4, default 3), persistent grid.
-int sweep_min_blocks() {
+// Default: 2 for the unrolled 8-point kernel (128 registers keep all eight
+// gathers in flight), 3 for the generic loop.
+int sweep_min_blocks(bool unrolled) {
   static int mb = [] {
     const char* e = std::getenv("LSKUM_SWEEP_MINB");
-    const int v = e ? std::atoi(e) : 3;
-    return (v >= 2 && v <= 4) ? v : 3;
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 2 && v <= 4) ? v : 0;
   }();
-  return mb;
+  return mb ? mb : (unrolled ? 2 : 3);
 }
 
 // Sweep variant: LSKUM_SWEEP_LANES = 2 (default, k_sweep2) | 1 (k_sweep).
@@ -174,6 +176,15 @@ int sweep_lanes() {
     return (e && std::atoi(e) == 1) ? 1 : 2;
   }();
   return v;
+}
+
+// Unrolled sweep for uniform 8-point stencils (LSKUM_SWEEP_UNROLL=0 disables).
+bool sweep_unrolled() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_SWEEP_UNROLL");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
 }
 
 template <class K>
@@ -195,7 +206,19 @@ template <bool S, int MB>
 void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
                     unsigned long long* it0, int sweep, cudaStream_t st) {
   const int slot = (S ? 4 : 0) + MB - 2;
-  if (sweep_lanes() == 2) {
+  if (sweep_lanes() == 2 && g.kfix == 8 && sweep_unrolled()) {
+    static int resident[64] = {};  // per (S, MB) instantiation and device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!resident[dev & 63]) {
+      int per_sm = 0, sms = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep2<S, MB, 8>, 256, 0), "occupancy");
+      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+      resident[dev & 63] = std::max(1, per_sm) * sms;
+    }
+    const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident[dev & 63]));
+    k_sweep2<S, MB, 8><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0, sweep);
+  } else if (sweep_lanes() == 2) {
     const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
     k_sweep2<S, MB><<<grid, 256, 0, st>>>(g, q, dq_in, dq_out, gas, ctl, it0, sweep);
   } else {
@@ -206,7 +229,7 @@ void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, cons
 
 void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
                   unsigned long long* it0, int sweep, cudaStream_t st) {
-  const int mb = sweep_min_blocks();
+  const int mb = sweep_min_blocks(sweep_lanes() == 2 && g.kfix == 8 && sweep_unrolled());
   if (strict) {
     if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
     else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
@@ -257,9 +280,35 @@ bool flux_weighted() {
   return v != 0;
 }
 
-void flux_w_launch(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+// Staged variant for stencils of at most 8 (LSKUM_FLUX_STAGE=0 disables it).
+bool flux_staged() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_FLUX_STAGE");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+void flux_w_launch(const FluxArgs& a, int kmax, const double2* w1, const double2* w2, const std::uint8_t* sing,
                    cudaStream_t st) {
   const int groups = (a.g.n + 3) / 4;
+  if (kmax <= 8 && flux_staged()) {
+    constexpr std::size_t smem = static_cast<std::size_t>(2 * kFluxWarps) * kFluxStageBytes;
+    static int resident[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!resident[dev & 63]) {
+      ck(cudaFuncSetAttribute(k_flux_ws<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+         "cudaFuncSetAttribute(k_flux_ws)");
+      int per_sm = 0, sms = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_ws<2>, 256, smem), "occupancy");
+      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+      resident[dev & 63] = std::max(1, per_sm) * sms;
+    }
+    const int blocks = std::max(1, std::min((groups + kFluxWarps - 1) / kFluxWarps, resident[dev & 63]));
+    k_flux_ws<2><<<blocks, 256, smem, st>>>(a, w1, w2, sing);
+    return;
+  }
   const int blocks = std::max(1, std::min((groups + 7) / 8, resident_blocks(k_flux_w<2>, 7)));
   k_flux_w<2><<<blocks, 256, 0, st>>>(a, w1, w2, sing);
 }
@@ -814,7 +863,7 @@ class Domain {
     fa.stride = stride_;
     fa.mask = 0xF;
     fa.first = 1;
-    if (!strict_ && weights_) flux_w_launch(fa, w1_.get(), w2_.get(), sing_.get(), st_);
+    if (!strict_ && weights_) flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), st_);
     else flux_launch(W_, strict_, fa, smem_, st_);
   }
   void launch_update(int a) {

@@ -269,7 +269,16 @@ __device__ __forceinline__ void st2(double* p, double2 v) {
   asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-template <bool S, int MB>
+// K = 8: uniform 8-point stencils (offsets i*8): the eight neighbour ids come
+// in two 16-byte loads and the neighbour loop is unrolled, so all gathers of a
+// point are in flight together instead of one neighbour at a time.
+__device__ __forceinline__ int4 ld_i4(const int* p) {
+  int4 v;
+  asm("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+template <bool S, int MB, int K = 0>
 __global__ void __launch_bounds__(256, MB) k_sweep2(Geo g, const D4* __restrict__ q,
                                                     const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
                                                     Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
@@ -290,9 +299,19 @@ __global__ void __launch_bounds__(256, MB) k_sweep2(Geo g, const D4* __restrict_
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
     int e0, k;
-    stencil_of(g, i, e0, k);
-    for (int e = e0; e < e0 + k; ++e) {
-      const int nb = g.nbr[e];
+    int nbk[K > 0 ? K : 1];
+    if constexpr (K == 8) {
+      e0 = 8 * i;
+      k = 8;
+      const int4 a0 = ld_i4(g.nbr + e0), a1 = ld_i4(g.nbr + e0 + 4);
+      nbk[0] = a0.x, nbk[1] = a0.y, nbk[2] = a0.z, nbk[3] = a0.w;
+      nbk[4] = a1.x, nbk[5] = a1.y, nbk[6] = a1.z, nbk[7] = a1.w;
+    } else {
+      stencil_of(g, i, e0, k);
+    }
+#pragma unroll
+    for (int j = 0; j < (K > 0 ? K : k); ++j) {
+      const int nb = K > 0 ? nbk[j] : g.nbr[e0 + j];
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
       const double2 qn = ld2(qd + 4 * nb), qxn = ld2(dd + 8 * nb), qyn = ld2(dd + 8 * nb + 4);
@@ -606,16 +625,78 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
   }
 }
 
+// One (point i, neighbour position j) pair of the fast flux residual: both
+// reconstructions, the x and y split fluxes of each side (the pair's half
+// stencils), acc += w . dG.  Warp-convergent (inactive lanes evaluate their
+// own point with zero offsets and add nothing).
+__device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, bool act, double2 pi,
+                                               const D4& qi, const D4& qxi, const D4& qyi, double2 pn,
+                                               const D4& qn, const D4& qxn, const D4& qyn, double2 w,
+                                               const double2* w2e, double (&acc)[4]) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  const Geo& g = a.g;
+  const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+  double ti[4], tn[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    ti[c] = corrected<false>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
+    tn[c] = corrected<false>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
+  }
+  bool ok = ti[3] < 0.0 && tn[3] < 0.0;
+  if (!ok) {  // q3 >= 0 has no state: evaluate a dummy one, add nothing
+    ti[3] = -1.0;
+    tn[3] = -1.0;
+  }
+  FluxState fi, fn;
+  ok = reconstruct2<false>(ti, tn, a.gas, fi, fn) && ok;
+  if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
+  AxisTerms at[4];
+  axis_terms4<false>(fi, fn, at);
+  const bool store = act && ok;
+  const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
+  // dG = gn - gi is an explicitly rounded subtraction: a contracted
+  // fma(rho_n, x_n, -gi) would leave ~1 ulp where the states are equal
+  // (the free stream must stay an exact fixed point).
+  double gi[4], gn[4];
+  split_flux<false>(fi, at[0], 0, !(dx <= 0.0), gi);
+  split_flux<false>(fn, at[1], 0, !(dx <= 0.0), gn);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c] = fma(wx, X::sub(gn[c], gi[c]), acc[c]);
+  split_flux<false>(fi, at[2], 1, !(dy <= 0.0), gi);
+  split_flux<false>(fn, at[3], 1, !(dy <= 0.0), gn);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
+  // a zero offset belongs to both half stencils: add the minus direction
+  if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
+    const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? *w2e : make_double2(0.0, 0.0);
+    split_flux<false>(fi, at[0], 0, true, gi);
+    split_flux<false>(fn, at[1], 0, true, gn);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = fma(v.x, X::sub(gn[c], gi[c]), acc[c]);
+    split_flux<false>(fi, at[2], 1, true, gi);
+    split_flux<false>(fn, at[3], 1, true, gn);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = fma(v.y, X::sub(gn[c], gi[c]), acc[c]);
+  }
+}
+
+// Sum over the 8 pair lanes of a point (xor shuffles stay inside the group).
+__device__ __forceinline__ void reduce8(double (&acc)[4]) {
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = X::add(acc[c], __shfl_xor_sync(0xFFFFFFFFu, acc[c], o));
+  }
+}
+
 // Eight lanes per point (one per stencil neighbour, looping for k > 8), four
 // points per warp, warps independent (persistent grid-stride over groups of
-// 4 points).  Phase A is the same convergent pair evaluation as k_flux; the
-// pair's contribution sum_c w dG is reduced across the 8 lanes with shuffles.
+// 4 points).  Any stencil size.
 template <int MB>
 __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* __restrict__ w1,
                                                     const double2* __restrict__ w2,
                                                     const std::uint8_t* __restrict__ sing) {
   constexpr unsigned kFull = 0xFFFFFFFFu;
-  using A = Ar<false>;
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_FLUX);
   if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_flux(a.ctl));
@@ -644,58 +725,153 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       const bool act = live && j < k;
       const int nb = act ? g.nbr[e0 + j] : ic;
       const double2 w = act ? w1[e0 + j] : make_double2(0.0, 0.0);
-      const double2 pn = g.xy[nb];
-      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
       const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
-      double ti[4], tn[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        ti[c] = corrected<false>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
-        tn[c] = corrected<false>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
-      }
-      bool ok = ti[3] < 0.0 && tn[3] < 0.0;
-      if (!ok) {  // q3 >= 0 has no state: evaluate a dummy one, add nothing
-        ti[3] = -1.0;
-        tn[3] = -1.0;
-      }
-      FluxState fi, fn;
-      ok = reconstruct2<false>(ti, tn, a.gas, fi, fn) && ok;
-      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
-      AxisTerms at[4];
-      axis_terms4<false>(fi, fn, at);
-      const bool store = act && ok;
-      const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
-      // dG = gn - gi is an explicitly rounded subtraction: a contracted
-      // fma(rho_n, x_n, -gi) would leave ~1 ulp where the states are equal
-      // (the free stream must stay an exact fixed point).
-      double gi[4], gn[4];
-      split_flux<false>(fi, at[0], 0, !(dx <= 0.0), gi);
-      split_flux<false>(fn, at[1], 0, !(dx <= 0.0), gn);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] = fma(wx, X::sub(gn[c], gi[c]), acc[c]);
-      split_flux<false>(fi, at[2], 1, !(dy <= 0.0), gi);
-      split_flux<false>(fn, at[3], 1, !(dy <= 0.0), gn);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
-      // a zero offset belongs to both half stencils: add the minus direction
-      if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
-        const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? w2[e0 + j] : make_double2(0.0, 0.0);
-        split_flux<false>(fi, at[0], 0, true, gi);
-        split_flux<false>(fn, at[1], 0, true, gn);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[c] = fma(v.x, X::sub(gn[c], gi[c]), acc[c]);
-        split_flux<false>(fi, at[2], 1, true, gi);
-        split_flux<false>(fn, at[3], 1, true, gn);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[c] = fma(v.y, X::sub(gn[c], gi[c]), acc[c]);
-      }
+      flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 + (e0 + j), acc);
     }
-#pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] = A::add(acc[c], __shfl_xor_sync(kFull, acc[c], o));
-    }
+    reduce8(acc);
     if (live && lane == 0) st4(a.res + i, D4{acc[0], acc[1], acc[2], acc[3]});
+  }
+  __syncthreads();
+  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+}
+
+// ---- staged variant (stencils of at most 8): each warp copies the NEXT group's
+// gathers (neighbour xy, q, qx, qy, weights; own point records) into its
+// shared-memory stage with cp.async while it computes the current group, and
+// loads the stencil indices two groups ahead, so no global-memory latency is
+// exposed inside the loop.  Stage layout is field-major (16-byte chunks per
+// lane) so each LDS.128 of a warp is conflict-free.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kFluxStageChunks = 8;                                  // per lane: xy, w, q(2), qx(2), qy(2)
+constexpr int kFluxStageBytes = kFluxStageChunks * 32 * 16 + 4 * 7 * 16;  // + 4 own records of 7 chunks
+constexpr int kFluxWarps = 8;                                       // 256 threads
+
+struct StageIdx {  // per lane, one group
+  int i, ic, nb, e;
+  bool live, act;
+};
+// Raw loads of a group's indices, issued two groups ahead; the predicates are
+// formed only when the group is staged (stage_index), so nothing waits on them.
+struct StageRaw {
+  int i, kind, nbr, e, k;
+};
+
+__device__ __forceinline__ StageRaw stage_load(const Geo& g, int grp, int lane, int sub) {
+  StageRaw r;
+  r.i = grp * 4 + sub;
+  const int ic = r.i < g.n ? r.i : g.n - 1;
+  r.kind = g.kind[ic];
+  int e0 = 0, k = 0;
+  stencil_of(g, ic, e0, k);
+  r.e = e0 + lane;
+  r.k = k;
+  r.nbr = (r.i < g.n && lane < k) ? g.nbr[r.e] : ic;
+  return r;
+}
+
+__device__ __forceinline__ StageIdx stage_index(const Geo& g, const StageRaw& r, int lane) {
+  StageIdx x;
+  x.i = r.i;
+  x.ic = r.i < g.n ? r.i : g.n - 1;
+  x.live = r.i < g.n && r.kind != KIND_OUTER;
+  x.act = x.live && lane < r.k;
+  x.e = r.e;
+  x.nb = x.act ? r.nbr : x.ic;
+  return x;
+}
+
+__device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1, const StageIdx& x,
+                                            char* st, int lane32, int lane, int sub) {
+  const Geo& g = a.g;
+  char* f = st + lane32 * 16;
+  cp_async16(f + 0 * 512, g.xy + x.nb, true);
+  cp_async16(f + 1 * 512, w1 + x.e, x.act);  // zero-filled for inactive lanes
+  const char* qn = reinterpret_cast<const char*>(a.q + x.nb);
+  const char* dn = reinterpret_cast<const char*>(a.dq + 2 * x.nb);
+  cp_async16(f + 2 * 512, qn, true);
+  cp_async16(f + 3 * 512, qn + 16, true);
+  cp_async16(f + 4 * 512, dn, true);
+  cp_async16(f + 5 * 512, dn + 16, true);
+  cp_async16(f + 6 * 512, dn + 32, true);
+  cp_async16(f + 7 * 512, dn + 48, true);
+  if (lane < 7) {  // own record of the lane group's point: xy, q (2), qx (2), qy (2)
+    char* o = st + kFluxStageChunks * 512 + (sub * 7 + lane) * 16;
+    const char* src = lane == 0 ? reinterpret_cast<const char*>(g.xy + x.ic)
+                      : lane < 3 ? reinterpret_cast<const char*>(a.q + x.ic) + (lane - 1) * 16
+                                 : reinterpret_cast<const char*>(a.dq + 2 * x.ic) + (lane - 3) * 16;
+    cp_async16(o, src, true);
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(256, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
+                                                     const double2* __restrict__ w2,
+                                                     const std::uint8_t* __restrict__ sing) {
+  extern __shared__ __align__(16) char fsm[];
+  __shared__ int s_skip;
+  ktimer_begin(a.ctl, KT_FLUX);
+  if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_flux(a.ctl));
+  __syncthreads();
+  const int lane32 = threadIdx.x & 31;
+  const int lane = threadIdx.x & 7;
+  const int sub = lane32 >> 3;
+  const int warp = threadIdx.x >> 5;
+  char* const stage0 = fsm + (2 * warp) * kFluxStageBytes;  // stage b at stage0 + b * kFluxStageBytes
+  const Geo& g = a.g;
+  const int groups = (g.n + 3) >> 2;
+  const int nwarps = gridDim.x * kFluxWarps;
+  int grp = blockIdx.x * kFluxWarps + warp;
+  if (!s_skip && grp < groups) {
+    StageIdx cur = stage_index(g, stage_load(g, grp, lane, sub), lane);
+    stage_issue(a, w1, cur, stage0, lane32, lane, sub);
+    cp_async_commit();
+    StageRaw nxt = stage_load(g, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
+    int buf = 0;
+    for (; grp < groups; grp += nwarps, buf ^= 1) {
+      const bool more = grp + nwarps < groups;
+      const StageIdx nx = stage_index(g, nxt, lane);
+      if (more) stage_issue(a, w1, nx, stage0 + (buf ^ 1) * kFluxStageBytes, lane32, lane, sub);
+      cp_async_commit();
+      const StageRaw nxt2 = stage_load(g, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
+      cp_async_wait<1>();
+      __syncwarp();
+      const char* st = stage0 + buf * kFluxStageBytes;
+      const char* f = st + lane32 * 16;
+      const char* o = st + kFluxStageChunks * 512 + sub * 7 * 16;
+      const double2 pn = *reinterpret_cast<const double2*>(f);
+      const double2 w = *reinterpret_cast<const double2*>(f + 512);
+      const double2 q01 = *reinterpret_cast<const double2*>(f + 2 * 512), q23 = *reinterpret_cast<const double2*>(f + 3 * 512);
+      const double2 x01 = *reinterpret_cast<const double2*>(f + 4 * 512), x23 = *reinterpret_cast<const double2*>(f + 5 * 512);
+      const double2 y01 = *reinterpret_cast<const double2*>(f + 6 * 512), y23 = *reinterpret_cast<const double2*>(f + 7 * 512);
+      const double2 pi = *reinterpret_cast<const double2*>(o);
+      const double2 oq01 = *reinterpret_cast<const double2*>(o + 16), oq23 = *reinterpret_cast<const double2*>(o + 32);
+      const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), ox23 = *reinterpret_cast<const double2*>(o + 64);
+      const double2 oy01 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
+      if (cur.live && lane == 0) {
+        const unsigned sd = sing[cur.i];
+        if (sd != 0xFFu)
+          raise_err(a.ctl, err_key(PH_FLUX, g.part[cur.i], gidx(g, cur.i), sd, kSolveSlot), sub_flux(a.ctl));
+      }
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      flux_pair_fast(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
+                     D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
+                     D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
+                     D4{y01.x, y01.y, y23.x, y23.y}, w, w2 + cur.e, acc);
+      reduce8(acc);
+      if (cur.live && lane == 0) st4(a.res + cur.i, D4{acc[0], acc[1], acc[2], acc[3]});
+      __syncwarp();  // the stage is refilled two groups on
+      cur = nx;
+      nxt = nxt2;
+    }
+    cp_async_wait<0>();
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
