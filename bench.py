@@ -29,6 +29,8 @@ import tempfile
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -68,6 +70,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-steady", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample target")
+    ap.add_argument("--large-side", type=int, default=3163,
+                    help="side of the >=10M-point cloud measured alongside (configs[3]); 0 = skip")
+    ap.add_argument("--large-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -232,6 +237,65 @@ def cpu_baseline(cloud, a, target_s):
             "sample": f"{iters} iterations of the {n}-point cloud, oracle/lskum_oracle.c (1 thread)"}
 
 
+def rooflines(L, counts, n, n_flux, k, order, inner, step_ms, sweep_ms, flux_ms, device=0, domains=1):
+    """Flux kernel against the measured DFMA peak (dynamic FP64 flops per point
+    from ncu), sweep and whole iteration against the measured HBM copy peak."""
+    fp64_peak = L.fp64_peak_tflops(device)
+    flops_pt = counts.get("flux_fp64_flops_per_point")
+    n_flux_dom = n_flux / domains
+    achieved = flops_pt * n_flux_dom / (flux_ms * 1e-3) / 1e12 if (flops_pt and flux_ms > 0) else None
+    traffic = counts.get("flux_dram_bytes_per_point")
+    hbm, hbm_kind = hbm_peak()
+    sweep_gbs = sweep_bytes(k) * (n / domains) / (sweep_ms * 1e-3) / 1e9 if sweep_ms else None
+    iter_gbs = iteration_bytes(k, order, inner) * n / (step_ms * 1e-3) / 1e9 / domains
+    flux = {"bound": "fp64", "kernel": "k_flux_ws (fast flux residual: split-stencil weights, cp.async staged)",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak if achieved else None,
+            "traffic": traffic * n_flux_dom if traffic else None,
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+            "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
+            "flops_source": f"ncu dynamic 2*DFMA+DADD+DMUL = {flops_pt:.0f} per point "
+                            "(profiles/flux_ncu_counts.json)" if flops_pt else None,
+            "launch_ms": flux_ms}
+    hbmr = {"bound": "hbm", "kernel": "k_sweep2 (derivative sweep)", "achieved": sweep_gbs, "peak": hbm,
+            "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
+            "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_ms, "peak_source": hbm_kind,
+            "iteration_achieved_gbs_per_gpu": iter_gbs, "iteration_frac": iter_gbs / hbm,
+            "iteration_bytes_per_point": iteration_bytes(k, order, inner)}
+    return flux, hbmr
+
+
+def large_run(L, a, counts):
+    """The >=10M-point cloud (BASELINE configs[3] size; roofline
+    fractions are quoted there), same session machinery, L2 flushed per step."""
+    side = a.large_side
+    cloud = L.Cloud.generate_rect(side, side, 0.1, 7, 8)
+    n = cloud.n
+    k = cloud.nnz // n
+    n_flux = int(np.count_nonzero(cloud.geometry()["kind"] != 2))
+    cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
+                   iters=a.large_steps, device=0)
+    step_ms, sweep_ms, flux_ms = [], [], []
+    with ClockSampler(0) as clocks, L.Session(cloud, cfg, capacity=a.large_steps + 3) as sess:
+        for _ in range(3):
+            sess.flush_l2()
+            sess.iterate(1)
+        for _ in range(a.large_steps):
+            sess.flush_l2()
+            step_ms.append(sess.iterate(1))
+            sw, fl = sess.event_ms()
+            sweep_ms.append(sw)
+            flux_ms.append(fl)
+    total = sum(step_ms)
+    flux, hbmr = rooflines(L, counts, n, n_flux, k, a.order, a.inner, total / a.large_steps,
+                           statistics.mean(sweep_ms) if a.order == 2 else None, statistics.mean(flux_ms))
+    return {"workload": f"rect {side}x{side} (BASELINE configs[3] size, ~10M points), same physics",
+            "n_points": n, "value": n * a.large_steps / (total * 1e-3), "unit": UNIT,
+            "ms_per_step": total / a.large_steps, "steps": a.large_steps, "warmup": 3,
+            "roofline": flux, "roofline_hbm": hbmr, "clocks": clocks.summary(),
+            "l2": "flushed before every timed step (384 MB overwrite); working set ~3 GB > L2"}
+
+
 def config_block(a, n, extra=None):
     c = {"workload": f"rect {a.side}x{a.side} stand-in for BASELINE configs[1] "
                      f"(NACA 0012 transonic ~160K, M={a.mach}, AoA={a.aoa}, order {a.order}, "
@@ -334,16 +398,9 @@ def run_b200_arm(a):
 
     # rooflines
     counts = load_counts()
-    fp64_peak = L.fp64_peak_tflops(0)
-    flux_avg = statistics.mean(flux_ms)
-    flops_pt = counts.get("flux_fp64_flops_per_point")
-    n_flux_dom = n_flux / gpus
-    achieved = flops_pt * n_flux_dom / (flux_avg * 1e-3) / 1e12 if (flops_pt and flux_avg > 0) else None
-    traffic = counts.get("flux_dram_bytes_per_point")
-    hbm, hbm_kind = hbm_peak()
     sweep_avg = statistics.mean(sweep_ms) if a.order == 2 else None
-    sweep_gbs = sweep_bytes(k) * (n / gpus) / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
-    iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9 / gpus
+    flux_roof, hbm_roof = rooflines(L, counts, n, n_flux, k, a.order, a.inner, total_ms / a.steps, sweep_avg,
+                                    statistics.mean(flux_ms), 0, gpus)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": total_ms / a.steps, "higher_is_better": True,
@@ -358,24 +415,15 @@ def run_b200_arm(a):
         "gpu_launches": launches * a.steps,
         "gpu_launches_note": f"{launches} kernels per iteration (all domains) x {a.steps}; "
                              f"plus {a.steps * gpus} L2-flush kernels between steps",
-        "roofline": {"bound": "fp64", "kernel": "k_flux (flux residual, W=8 lanes per point)",
-                     "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak if achieved else None,
-                     "traffic": traffic * n_flux_dom if traffic else None,
-                     "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
-                     "flops_source": "ncu dynamic 2*DFMA+DADD+DMUL per point, profiles/flux_ncu_counts.json",
-                     "launch_ms": flux_avg},
-        "roofline_hbm": {"bound": "hbm", "kernel": "k_sweep", "achieved": sweep_gbs, "peak": hbm,
-                         "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
-                         "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_avg,
-                         "peak_source": hbm_kind,
-                         "iteration_achieved_gbs_per_gpu": iter_gbs, "iteration_frac": iter_gbs / hbm,
-                         "iteration_bytes_per_point": iteration_bytes(k, a.order, a.inner)},
+        "roofline": flux_roof,
+        "roofline_hbm": hbm_roof,
         "steady_state": {"value": steady, "iterations": steady_iters,
                          "what": "same session, back-to-back iterations, no L2 flush"},
         "clocks": clk,
         "final_residue": float(residues[-1]) if len(residues) else None,
     }
+    if a.large_side > 0 and gpus == 1:
+        out["large"] = large_run(L, a, counts)
     if not a.no_cpu_baseline and gpus == 1:
         out["cpu_baseline"] = cpu_baseline(cloud, a, a.cpu_seconds)
     print(json.dumps(out), flush=True)
@@ -440,15 +488,9 @@ def run_b200_ranks(a, L, world, rank, local):
         e2e_wall = max(e["e2e_wall"] for e in everyone)
         flux_avg = max(e["flux_ms"] for e in everyone)
         counts = load_counts()
-        fp64_peak = L.fp64_peak_tflops(device)
-        flops_pt = counts.get("flux_fp64_flops_per_point")
-        n_flux_dom = n_flux / world
-        achieved = flops_pt * n_flux_dom / (flux_avg * 1e-3) / 1e12 if (flops_pt and flux_avg > 0) else None
-        traffic = counts.get("flux_dram_bytes_per_point")
-        hbm, hbm_kind = hbm_peak()
         sweep_avg = max(e["sweep_ms"] for e in everyone) if a.order == 2 else None
-        sweep_gbs = sweep_bytes(k) * (n / world) / (sweep_avg * 1e-3) / 1e9 if sweep_avg else None
-        iter_gbs = iteration_bytes(k, a.order, a.inner) * n / (total_ms / a.steps * 1e-3) / 1e9 / world
+        flux_roof, hbm_roof = rooflines(L, counts, n, n_flux, k, a.order, a.inner, total_ms / a.steps, sweep_avg,
+                                        flux_avg, device, world)
         nnz = e2e_cloud.nnz
         h2d = n * (16 + 16 + 1 + 1 + 32) + 4 * (n + 1) + 4 * nnz
         d2h = n * 21 * 8 + 8 * a.steps
@@ -469,19 +511,8 @@ def run_b200_ranks(a, L, world, rank, local):
             "gpu_launches": launches * a.steps,
             "gpu_launches_note": f"{launches} kernels per iteration summed over ranks (compute, halo, "
                                  f"signal, wait) x {a.steps}; plus {a.steps * world} L2-flush kernels",
-            "roofline": {"bound": "fp64", "kernel": "k_flux (flux residual, W=8 lanes per point)",
-                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak if achieved else None,
-                         "traffic": traffic * n_flux_dom if traffic else None,
-                         "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
-                         "flops_source": "ncu dynamic 2*DFMA+DADD+DMUL per point, profiles/flux_ncu_counts.json",
-                         "launch_ms": flux_avg},
-            "roofline_hbm": {"bound": "hbm", "kernel": "k_sweep", "achieved": sweep_gbs, "peak": hbm,
-                             "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
-                             "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_avg,
-                             "peak_source": hbm_kind, "iteration_achieved_gbs_per_gpu": iter_gbs,
-                             "iteration_frac": iter_gbs / hbm,
-                             "iteration_bytes_per_point": iteration_bytes(k, a.order, a.inner)},
+            "roofline": flux_roof,
+            "roofline_hbm": hbm_roof,
             "clocks": clk,
             "final_residue": float(residues[-1]) if len(residues) else None,
         }

@@ -69,7 +69,7 @@ def main():
                    "flux_fp64_flops_per_point": flops, "flux_dram_bytes_per_point": dram / n,
                    "flux_fp64_thread_inst_per_point": fp,
                    "note": "dynamic counts of k_flux from one ncu --set full capture "
-                           "(2000x2000 rect cloud, order 2); flops = 2*DFMA + DADD + DMUL"},
+                           "(rect cloud, order 2; n_points above); flops = 2*DFMA + DADD + DMUL"},
                   open(path, "w"), indent=1)
         print("wrote", path)
 
