@@ -680,13 +680,25 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   }
 }
 
-// Sum over the 8 pair lanes of a point (xor shuffles stay inside the group).
-__device__ __forceinline__ void reduce8(double (&acc)[4]) {
-#pragma unroll
-  for (int o = 4; o >= 1; o >>= 1) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c] = X::add(acc[c], __shfl_xor_sync(0xFFFFFFFFu, acc[c], o));
-  }
+// Sum over the 8 pair lanes of a point (xor shuffles stay inside the group),
+// as a transposing reduction: after it, lanes 2c and 2c+1 of the group hold
+// component c of the sum (4 double shuffles instead of 12).
+__device__ __forceinline__ double reduce8(const double (&acc)[4], int lane) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  const bool hi2 = lane & 4, hi1 = lane & 2;
+  // xor 4: keep components {0,1} (lanes 0-3) or {2,3} (lanes 4-7)
+  const double s0 = hi2 ? acc[0] : acc[2], s1 = hi2 ? acc[1] : acc[3];
+  const double k0 = hi2 ? acc[2] : acc[0], k1 = hi2 ? acc[3] : acc[1];
+  const double a0 = X::add(k0, __shfl_xor_sync(kFull, s0, 4));
+  const double a1 = X::add(k1, __shfl_xor_sync(kFull, s1, 4));
+  // xor 2: keep the first (lanes x0x) or second (lanes x1x) of the pair
+  const double b = X::add(hi1 ? a1 : a0, __shfl_xor_sync(kFull, hi1 ? a0 : a1, 2));
+  return X::add(b, __shfl_xor_sync(kFull, b, 1));
+}
+
+// Residual of point i from the transposed reduction: lane 2c writes component c.
+__device__ __forceinline__ void store_res8(D4* res, int i, double v, int lane) {
+  if (!(lane & 1)) reinterpret_cast<double*>(res + i)[lane >> 1] = v;
 }
 
 // Eight lanes per point (one per stencil neighbour, looping for k > 8), four
@@ -728,8 +740,8 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
       flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 + (e0 + j), acc);
     }
-    reduce8(acc);
-    if (live && lane == 0) st4(a.res + i, D4{acc[0], acc[1], acc[2], acc[3]});
+    const double r = reduce8(acc, lane);
+    if (live) store_res8(a.res, i, r, lane);
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
@@ -865,8 +877,8 @@ __global__ void __launch_bounds__(256, MB) k_flux_ws(FluxArgs a, const double2* 
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
                      D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
                      D4{y01.x, y01.y, y23.x, y23.y}, w, w2 + cur.e, acc);
-      reduce8(acc);
-      if (cur.live && lane == 0) st4(a.res + cur.i, D4{acc[0], acc[1], acc[2], acc[3]});
+      const double r = reduce8(acc, lane);
+      if (cur.live) store_res8(a.res, cur.i, r, lane);
       __syncwarp();  // the stage is refilled two groups on
       cur = nx;
       nxt = nxt2;
