@@ -37,6 +37,14 @@ int lskum_b200_cloud_from_arrays(int32_t n, const double* x, const double* y,
                                  const int64_t* offsets, const int32_t* nbrs,
                                  lskum_cloud** out);
 int lskum_b200_cloud_nnz(const lskum_cloud* cloud, int64_t* out);
+/* Synthetic NACA 0012 O-cloud (no reference counterpart, the
+ * reference's generators are cloud.cpp:323-425): n_wall surface points (even),
+ * n_rings rings out to a far-field circle of radius outer_radius chords about
+ * (0.5, 0); kNN stencils as lskum_cloud_generate_rect.  frozen_wall != 0 marks
+ * the surface ring outer (held state) instead of wall.  Config spec:
+ * generate=naca0012:<n_wall>x<n_rings>[:frozen]. */
+int lskum_b200_cloud_generate_naca0012(int n_wall, int n_rings, double outer_radius, double jitter,
+                                       uint64_t seed, int knn, int frozen_wall, lskum_cloud** out);
 /* Any output pointer may be NULL. */
 int lskum_b200_cloud_geometry(const lskum_cloud* cloud, double* x, double* y, uint8_t* kind,
                               double* nx, double* ny, int64_t* offsets, int32_t* nbrs);

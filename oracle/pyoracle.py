@@ -321,6 +321,8 @@ def _setup_ref(L):
     L.refshim_generate_annulus.restype = C.c_void_p
     L.refshim_generate_annulus.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double,
                                            C.c_uint64, C.c_int]
+    L.refshim_knn.restype = C.c_void_p
+    L.refshim_knn.argtypes = [C.c_int32, _dp, _dp, C.c_int]
     L.refshim_cloud_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
     L.refshim_cloud_get.argtypes = [C.c_void_p, _dp, _dp, _u8p, _dp, _dp, _i64p, _i32p]
     L.refshim_cloud_free.argtypes = [C.c_void_p]
@@ -344,6 +346,13 @@ def _ref_take(h) -> Cloud:
 
 def ref_generate_rect(nx, ny, jitter, seed, k, bounds=(0.0, 1.0, 0.0, 1.0)) -> Cloud:
     return _ref_take(ref_lib().refshim_generate_rect(nx, ny, *bounds, jitter, seed, k))
+
+
+def ref_knn(x, y, k) -> Cloud:
+    """The reference's build_stencils on the given points (kinds/normals zero)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return _ref_take(ref_lib().refshim_knn(len(x), x, y, k))
 
 
 def ref_generate_annulus(nt, nr, r_outer, jitter, seed, k) -> Cloud:

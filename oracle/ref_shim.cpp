@@ -232,6 +232,24 @@ void* refshim_generate_annulus(int nt, int nr, double r_outer, double jitter, ui
   }
 }
 
+// The reference's kNN (build_stencils, cloud.cpp:137-237) on arbitrary points
+// (kind interior, zero normals), e.g. the NACA 0012 clouds it cannot generate.
+void* refshim_knn(int32_t n, const double* x, const double* y, int k) {
+  try {
+    std::vector<PointRecord> recs(n);
+    for (int32_t i = 0; i < n; ++i) {
+      recs[i].id = i;
+      recs[i].x = x[i];
+      recs[i].y = y[i];
+    }
+    PointCloud c(std::move(recs));
+    build_stencils(c, k);
+    return new Generated{std::move(c)};
+  } catch (...) {
+    return nullptr;
+  }
+}
+
 void refshim_cloud_sizes(void* h, int32_t* n, int64_t* nnz) {
   const PointCloud& c = static_cast<Generated*>(h)->cloud;
   *n = c.n_points();

@@ -107,6 +107,14 @@ int lskum_cloud_generate_annulus(int n_theta, int n_rings, double outer_radius, 
   });
 }
 
+int lskum_b200_cloud_generate_naca0012(int n_wall, int n_rings, double outer_radius, double jitter,
+                                       uint64_t seed, int knn, int frozen_wall, lskum_cloud** out) {
+  NONNULL(out);
+  return guard([&] {
+    *out = new lskum_cloud{lskb::make_naca0012(n_wall, n_rings, outer_radius, jitter, seed, knn, frozen_wall != 0)};
+  });
+}
+
 int lskum_cloud_from_config(const lskum_config* cfg, lskum_cloud** out) {
   NONNULL(cfg, out);
   return guard([&] { *out = new lskum_cloud{lskb::acquire_points(cfg->s)}; });

@@ -133,6 +133,8 @@ struct Box {
 PointSet make_rect(int nx, int ny, const Box& box, double jitter, std::uint64_t seed, int k);
 PointSet make_annulus(int n_theta, int n_rings, double r_outer, double jitter,
                       std::uint64_t seed, int k);
+PointSet make_naca0012(int n_wall, int n_rings, double r_outer, double jitter, std::uint64_t seed, int k,
+                       bool frozen_wall);
 void attach_knn(PointSet& ps, int k);
 
 // ---- stencil screening (reference cloud.cpp:252-321) ----

@@ -169,6 +169,20 @@ PointSet acquire_points(const Settings& s) {
   const bool file = !s.grid.empty(), gen = !s.generate.empty();
   if (file == gen) raise(Status::config, "exactly one of grid path or generator spec required");
   if (file) return read_grid_file(s.grid);
+  // extension: naca0012:<n_wall>x<n_rings>[:frozen] (the reference
+  // rejects the spec as a malformed rect size)
+  const std::string naca = "naca0012:";
+  if (s.generate.rfind(naca, 0) == 0) {
+    std::string rest = s.generate.substr(naca.size());
+    bool frozen = false;
+    const std::string fz = ":frozen";
+    if (rest.size() > fz.size() && rest.compare(rest.size() - fz.size(), fz.size(), fz) == 0) {
+      frozen = true;
+      rest.resize(rest.size() - fz.size());
+    }
+    const auto [nw, nr] = dims_value("generate", rest);
+    return make_naca0012(nw, nr, s.outer_radius, s.jitter, s.seed, s.knn, frozen);
+  }
   const std::string ring = "annulus:";
   if (s.generate.rfind(ring, 0) == 0) {
     const auto [nt, nr] = dims_value("generate", s.generate.substr(ring.size()));
