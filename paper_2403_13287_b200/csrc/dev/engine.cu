@@ -514,6 +514,19 @@ GeomView view_of(const PointSet& ps, const std::vector<std::uint8_t>& part) {
   return v;
 }
 
+Gas make_gas(double gamma, double cfl, double det_tol) {
+  Gas g{};
+  g.gamma = gamma;
+  g.gm1 = gamma - 1.0;
+  g.inv_gm1 = 1.0 / (gamma - 1.0);
+  g.cfl = cfl;
+  g.det_tol = det_tol;
+  const double m = 2.0 / (gamma - 1.0);
+  const double mr = std::nearbyint(m);
+  g.half_pow = (std::fabs(m - mr) < 1e-9 && mr >= 1.0 && mr <= 40.0) ? static_cast<int>(mr) : -1;
+  return g;
+}
+
 class Domain {
  public:
   // ipc: buffers that peers read (q, dq, the shared word, the residue array)
@@ -527,16 +540,7 @@ class Domain {
     for (auto& e : kev_) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : poll_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     if (gv.nnz >= (1ll << 31)) raise(Status::argument, "stencil table exceeds 2^31 entries");
-    gas_.gamma = gamma;
-    gas_.gm1 = gamma - 1.0;
-    gas_.inv_gm1 = 1.0 / (gamma - 1.0);
-    gas_.cfl = cfl;
-    gas_.det_tol = det_tol;
-    {
-      const double m = 2.0 / (gamma - 1.0);
-      const double mr = std::nearbyint(m);
-      gas_.half_pow = (std::fabs(m - mr) < 1e-9 && mr >= 1.0 && mr <= 40.0) ? static_cast<int>(mr) : -1;
-    }
+    gas_ = make_gas(gamma, cfl, det_tol);
     std::int64_t km = 1;
     for (int i = 0; i < n_; ++i) km = std::max(km, gv.off[i + 1] - gv.off[i]);
     kmax_ = static_cast<int>(km);
@@ -587,6 +591,7 @@ class Domain {
     ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
     ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
     ck(cudaMemcpyAsync(part_.get(), hpart, nl, cudaMemcpyHostToDevice, st_), "H2D part");
+    part_host_.assign(hpart, hpart + nl);
     ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
     if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
     if (gv.gid) {
@@ -627,7 +632,7 @@ class Domain {
   ~Domain() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(st_);  // nothing in flight before the buffers go back to the pool
-    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    clear_graphs();
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     for (auto& e : kev_) cudaEventDestroy(e);
@@ -778,6 +783,9 @@ class Domain {
   // Zeroes the once-per-run fields (runtime.cpp:216-224) and the control
   // block; with `own_shared` this domain also resets the run's shared word.
   void reset_run(int order, int inner, int fp_mode, int chunk, bool own_shared) {
+    // captured graphs bake in the iteration's kernel sequence
+    if (order != order_ || inner != inner_ || (fp_mode == 1) != strict_ || std::max(1, chunk) != chunk_)
+      clear_graphs();
     order_ = order;
     inner_ = inner;
     strict_ = fp_mode == 1;
@@ -804,12 +812,47 @@ class Domain {
   }
   void begin_run(int order, int inner, int fp_mode, int chunk) {
     reset_run(order, inner, fp_mode, chunk, true);
+    trace("engine: run reset (weights)");
     first_q();
     ck(cudaStreamSynchronize(st_), "begin_run");
     refresh_ctl();
   }
 
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
+
+  void clear_graphs() {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    graphs_.clear();
+  }
+
+  // Reuse by a later run on the same geometry (the per-cloud engine cache):
+  // gas constants, the error tie-break partition ids and the history
+  // capacity may change; kernels captured with the old values are dropped.
+  void reconfigure(double gamma, double cfl, double det_tol, const std::uint8_t* part, int capacity) {
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    const Gas g = make_gas(gamma, cfl, det_tol);
+    if (g.gamma != gas_.gamma || g.cfl != gas_.cfl || g.det_tol != gas_.det_tol) {
+      if (g.det_tol != gas_.det_tol) weights_ = false;
+      gas_ = g;
+      clear_graphs();
+    }
+    if (capacity > capacity_) {
+      capacity_ = capacity;
+      hist_.alloc(capacity_, st_);
+      it0_.alloc(capacity_, st_);
+      it1_.alloc(capacity_, st_);
+      clear_graphs();
+    }
+    const std::size_t nl = static_cast<std::size_t>(n_loc_);
+    std::vector<std::uint8_t> hp(nl, 0);
+    if (part)
+      for (std::size_t i = 0; i < nl; ++i) hp[i] = part[gid_host_.empty() ? i : static_cast<std::size_t>(gid_host_[i])];
+    if (hp != part_host_) {
+      part_host_ = hp;
+      ck(cudaMemcpyAsync(part_.get(), part_host_.data(), nl, cudaMemcpyHostToDevice, st_), "H2D part");
+      ck(cudaStreamSynchronize(st_), "part");
+    }
+  }
 
   // Geometry-only split-stencil weights for the fast flux kernel (once per
   // domain); the zero-offset table w2 only exists when such pairs do.
@@ -953,6 +996,7 @@ class Domain {
         left -= c;
       }
     }
+    trace("engine: graphs ready");
     ck(cudaEventRecord(ev0_, st_), "EventRecord");
     int left = n, issued = 0, waited = 0;
     bool failed = false;
@@ -1178,6 +1222,7 @@ class Domain {
   std::size_t smem_ = 0;
   int stride_ = 0;
   std::vector<int> gid_host_;
+  std::vector<std::uint8_t> part_host_;
   DBuf<double2> xy_, nrm_;
   DBuf<std::uint8_t> kind_, part_;
   DBuf<int> off_, nbr_, gid_;
@@ -1217,6 +1262,38 @@ std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int ca
   return d;
 }
 
+// The cloud's cached single-device domain (PointSet::engine_cache), created on
+// first use and reconfigured for later runs: repeated lskum_run calls on one
+// cloud keep geometry, split-stencil weights, buffers and captured graphs
+// resident instead of re-uploading and re-capturing them.
+struct EngineCache {
+  std::unique_ptr<Domain> dom;
+  int device = -1;
+};
+
+Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
+  auto* c = static_cast<EngineCache*>(ps.engine_cache.get());
+  if (c && c->device == spec.device && c->dom) {
+    c->dom->reconfigure(spec.gamma, spec.cfl, spec.det_tol, spec.part_of.empty() ? nullptr : spec.part_of.data(),
+                        capacity);
+    trace("engine: cached domain reconfigured");
+  } else {
+    ps.engine_cache.reset();  // release the old device's buffers first
+    auto fresh = std::make_shared<EngineCache>();
+    fresh->device = spec.device;
+    fresh->dom = std::make_unique<Domain>(view_of(ps, spec.part_of), spec.device, spec.gamma, spec.cfl,
+                                          spec.det_tol, capacity);
+    trace("engine: geometry uploaded");
+    ps.engine_cache = fresh;
+    c = fresh.get();
+  }
+  Domain& d = *c->dom;
+  d.upload(ps.fields, false);
+  trace("engine: state uploaded");
+  d.begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
+  return d;
+}
+
 // Copy-back of the reference's end-of-run store: prim (final), q of the last
 // iteration, published qx/qy, flux_res and delta_t of the last iteration.
 void copy_back(Domain& d, PointSet& ps) {
@@ -1240,7 +1317,15 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
     }
     return rec;
   }
-  auto d = open_domain(ps, spec, spec.iters);
+  Domain* d = nullptr;
+  try {
+    d = &cached_domain(ps, spec, spec.iters);
+  } catch (const Fault&) {
+    throw;
+  } catch (...) {
+    ps.engine_cache.reset();  // a device-side failure leaves the cached domain unusable
+    throw;
+  }
   trace("engine: domain open");
   if (d->failed()) {  // first q_variables
     copy_back(*d, ps);

@@ -105,6 +105,10 @@ struct PointSet {
   }
   // Screening report of this (immutable) geometry, computed on first use.
   mutable std::shared_ptr<const Screening> screening;
+  // Device-resident copy of this geometry kept between lskum_run calls (the
+  // engine's single-device domain: geometry, weights, state buffers, CUDA
+  // graphs); released with the cloud.
+  mutable std::shared_ptr<void> engine_cache;
 
   bool has_wall() const;
   int max_degree() const;

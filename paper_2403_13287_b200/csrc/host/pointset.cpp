@@ -72,7 +72,9 @@ bool fields_identical(const FieldBlock& a, const FieldBlock& b) {
 
 void PointSet::reset_fields(Layout layout) {
   if (fields.size() == n() && fields.layout() == layout) {
-    std::fill(fields.raw(), fields.raw() + static_cast<std::size_t>(n()) * slot::count, 0.0);
+    double* d = fields.raw();
+    const std::int64_t total = static_cast<std::int64_t>(n()) * slot::count;
+    parallel_slices(total, [d](std::int64_t lo, std::int64_t hi) { std::fill(d + lo, d + hi, 0.0); }, 1 << 18);
   } else {
     fields = FieldBlock(layout, n());
   }

@@ -11,6 +11,7 @@
 #include <filesystem>
 
 #include "core.hpp"
+#include "par.hpp"
 
 namespace lskb {
 
@@ -53,12 +54,15 @@ class OutFile {
 void freestream(PointSet& ps, double mach, double aoa_deg, double gamma) {
   const double a = aoa_deg * M_PI / 180.0;
   const double u1 = mach * std::cos(a), u2 = mach * std::sin(a), p = 1.0 / gamma;
-  for (std::int32_t i = 0; i < ps.n(); ++i) {
-    ps.fields.at(i, slot::prim) = 1.0;
-    ps.fields.at(i, slot::prim + 1) = u1;
-    ps.fields.at(i, slot::prim + 2) = u2;
-    ps.fields.at(i, slot::prim + 3) = p;
-  }
+  parallel_slices(ps.n(), [&](std::int64_t lo, std::int64_t hi) {
+    for (std::int64_t i = lo; i < hi; ++i) {
+      const std::int32_t k = static_cast<std::int32_t>(i);
+      ps.fields.at(k, slot::prim) = 1.0;
+      ps.fields.at(k, slot::prim + 1) = u1;
+      ps.fields.at(k, slot::prim + 2) = u2;
+      ps.fields.at(k, slot::prim + 3) = p;
+    }
+  }, 1 << 16);
 }
 
 double rate_of_data_processing(double seconds, std::int64_t iters, std::int64_t n) {

@@ -470,8 +470,9 @@ PointSet make_naca0012(int n_wall, int n_rings, double r_outer, double jitter, s
     for (std::int32_t p : scr.defective) {
       if (ps.kind[p] == Kind::outer) continue;
       ps.kind[p] = Kind::outer;
-      ps.nx[p] = 0.0;
-      ps.ny[p] = 0.0;
+      const double h = std::hypot(ps.x[p] - cx, ps.y[p]);  // boundary points carry a unit normal
+      ps.nx[p] = h > 0.0 ? (ps.x[p] - cx) / h : 1.0;
+      ps.ny[p] = h > 0.0 ? ps.y[p] / h : 0.0;
     }
   }
   return ps;

@@ -249,3 +249,29 @@ def test_solver_flux_residual_matches_oracle(bump_cloud_arrays, cloud, order, fp
     assert rel_err(f[live, 16:20], want.store[live, 16:20]) <= 1e-12
     assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-12
     assert rel_seq(res.residues(), want.residue) <= 1e-10
+
+
+def test_cached_domain_reruns_match_fresh_clouds(bump_cloud_arrays):
+    """lskum_run keeps the cloud's device domain between calls (geometry,
+    weights, buffers, graphs).  A sequence of runs with changing order, fp
+    mode, CFL, partition count, chunking and iteration count on ONE cloud must
+    give bitwise the results of the same runs on fresh clouds."""
+    c, prim0 = bump_cloud_arrays
+    cached = product_cloud(c)
+    seq = [dict(order=2, iters=12), dict(order=1, iters=30), dict(order=2, iters=12, fp_mode="strict"),
+           dict(order=2, iters=7, cfl=0.4, parts=8), dict(order=2, iters=30, chunk=5),
+           dict(order=2, iters=60), dict(order=2, iters=12)]  # 60: aborts at 35 like the reference
+    for cfg in seq:
+        iters = cfg.pop("iters")
+        conf = L.Config(mach=0.63, aoa=2.0, iters=iters, inner=3, **dict(dict(cfl=0.5), **cfg))
+        out = []
+        for cloud in (cached, product_cloud(c)):
+            cloud.reset_store(0)
+            cloud.set_primitives(prim0)
+            try:
+                out.append((L.run_fixed_point(cloud, conf).residues(), cloud.fields()))
+            except L.LskumError as e:
+                out.append((e.message, cloud.fields()))
+        (r1, f1), (r2, f2) = out
+        assert (r1 == r2) if isinstance(r1, str) else np.array_equal(r1, r2), cfg
+        assert np.array_equal(f1, f2), cfg

@@ -122,3 +122,18 @@ def test_frozen_naca_run_matches_oracle(naca, order, iters):
     got = res.residues()
     assert float(np.max(np.abs(got - want.residue) / np.abs(want.residue))) <= 1e-10
     assert rel_err(pc.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-12
+
+
+def test_frozen_trailing_edge_points_are_valid_boundary_points(tmp_path):
+    """Interior points behind the sharp trailing edge whose split stencils fail
+    validation are held (kind outer) and carry a unit normal, as the grid
+    format requires of boundary points (reference cloud.cpp:470-477)."""
+    nw, nr = 520, 308
+    c = L.Cloud.generate_naca0012(nw, nr, 20.0, 0.0, 7, 8, frozen_wall=True)
+    g = c.geometry()
+    held = np.nonzero(g["kind"][nw:-nw] == 2)[0] + nw
+    assert len(held) > 0 and np.all(g["x"][held] > 0.99)  # all just behind the trailing edge
+    np.testing.assert_allclose(np.hypot(g["nx"][held], g["ny"][held]), 1.0, rtol=1e-14)
+    path = str(tmp_path / "naca.grid")
+    c.write_file(path)
+    assert L.Cloud.read_file(path).validate()["n_defective"] == 0
