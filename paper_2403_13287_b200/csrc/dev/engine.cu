@@ -22,6 +22,7 @@
 
 #include "../engine.hpp"
 #include "kernels.cuh"
+#include "../host/par.hpp"
 
 namespace lskb {
 
@@ -446,6 +447,10 @@ __global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const
 }
 
 // Scatters the primitives (slots 0-3 of a FieldBlock in either layout) into D4 records.
+__global__ void k_fill_d4(D4* out, int n, D4 v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
+}
+
 __global__ void k_unpack_prim(int n, int soa, const double* in, D4* prim) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (soa)
@@ -677,6 +682,13 @@ class Domain {
   int global_of(int local) const { return gid_host_.empty() ? local : gid_host_[local]; }
 
   // ---- state transfer (FieldBlock <-> device records) ----
+  // Uniform primitive state on owned and halo points (lskum_run's free stream).
+  void fill_prim(const double (&v)[4]) {
+    k_fill_d4<<<std::min<int>((n_loc_ + 255) / 256, 4096), 256, 0, st_>>>(prim_.get(), n_loc_,
+                                                                          D4{v[0], v[1], v[2], v[3]});
+    ck(cudaGetLastError(), "k_fill_d4");
+  }
+
   void upload(const FieldBlock& f, bool full) {
     const std::size_t n = static_cast<std::size_t>(n_);
     if (!full && gid_host_.empty()) {
@@ -739,9 +751,15 @@ class Domain {
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
           n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
-      ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
-         "D2H fields");
+      // through pinned staging (full-rate D2H), then a parallel host copy
+      const std::size_t bytes = 21 * n * sizeof(double);
+      char* h = static_cast<char*>(t_staging.get(bytes));
+      ck(cudaMemcpyAsync(h, packed.get(), bytes, cudaMemcpyDeviceToHost, st_), "D2H fields");
       ck(cudaStreamSynchronize(st_), "download");
+      char* dst = reinterpret_cast<char*>(f.raw());
+      parallel_slices(static_cast<std::int64_t>(bytes), [&](std::int64_t lo, std::int64_t hi) {
+        std::memcpy(dst + lo, h + lo, static_cast<std::size_t>(hi - lo));
+      }, 1 << 21);
       return;
     }
     std::vector<D4> h(6 * n);
@@ -1288,7 +1306,8 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
     c = fresh.get();
   }
   Domain& d = *c->dom;
-  d.upload(ps.fields, false);
+  if (spec.fs_device) d.fill_prim(spec.fs_prim);
+  else d.upload(ps.fields, false);
   trace("engine: state uploaded");
   d.begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
   return d;
@@ -1296,9 +1315,10 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
 
 // Copy-back of the reference's end-of-run store: prim (final), q of the last
 // iteration, published qx/qy, flux_res and delta_t of the last iteration.
-void copy_back(Domain& d, PointSet& ps) {
+void copy_back(Domain& d, PointSet& ps, bool* written = nullptr) {
   const bool with_q = d.done() > 0;
   d.download(ps.fields, with_q, d.q_read_last(), d.dq_cur());
+  if (written) *written = true;
 }
 
 }  // namespace
@@ -1328,18 +1348,18 @@ RunRecord engine_run(PointSet& ps, const EngineSpec& spec) {
   }
   trace("engine: domain open");
   if (d->failed()) {  // first q_variables
-    copy_back(*d, ps);
+    copy_back(*d, ps, spec.store_written);
     throw d->fault_in_run();
   }
   d->iterate(spec.iters);
   trace("engine: iterated");
   if (d->failed()) {
     Fault f = d->fault_in_run();
-    copy_back(*d, ps);
+    copy_back(*d, ps, spec.store_written);
     rec.abort_iteration = d->err_iter() + 1;
     throw f;
   }
-  copy_back(*d, ps);
+  copy_back(*d, ps, spec.store_written);
   trace("engine: copied back");
   rec.iterations = d->done();
   rec.residue = d->residues();

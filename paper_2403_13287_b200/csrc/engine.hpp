@@ -23,6 +23,13 @@ struct EngineSpec {
   int gpus = 1;     // device domains (sessions; lskum_run decides in solve.cpp)
   // Partition of each point (reference error tie-break, runtime.cpp:115-118).
   std::vector<std::uint8_t> part_of;
+  // lskum_run's free-stream initialisation done on the device (single-domain
+  // runs): the host store is only written by the copy-back; store_written
+  // reports whether that happened, so the caller can apply the host-side
+  // initialisation the reference leaves behind when a run fails earlier.
+  bool fs_device = false;
+  double fs_prim[4] = {0.0, 0.0, 0.0, 0.0};
+  bool* store_written = nullptr;
 };
 
 // Config check + stencil screening gate + bisection (host side of a run).

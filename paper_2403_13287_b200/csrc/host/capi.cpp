@@ -197,13 +197,8 @@ static int run_impl(lskum_cloud* cloud, const lskum_config* cfg, lskum_result** 
   NONNULL(cloud, cfg, out);
   return guard([&] {
     lskb::trace("run: enter");
-    if (reinit) {
-      cfg->s.check();
-      cloud->ps.reset_fields(cfg->s.layout);
-      lskb::freestream(cloud->ps, cfg->s.mach, cfg->s.aoa, cfg->s.gamma);
-    }
-    lskb::trace("run: store initialised");
-    lskb::RunRecord run = lskb::solve_on_device(cloud->ps, cfg->s);
+    lskb::RunRecord run = reinit ? lskb::solve_from_freestream(cloud->ps, cfg->s)
+                                 : lskb::solve_on_device(cloud->ps, cfg->s);
     lskb::Report rep = lskb::summarize(run, cloud->ps.n());
     lskb::trace("run: done");
     *out = new lskum_result{std::move(run), std::move(rep), cfg->s};

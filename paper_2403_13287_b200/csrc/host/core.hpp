@@ -220,5 +220,10 @@ void write_run_outputs(const std::string& prefix, const PointSet& ps, const RunR
 // (reference run_fixed_point, runtime.cpp:195-275).  Throws Fault on failure
 // with the reference's code and "iteration N: ..." message.
 RunRecord solve_on_device(PointSet& ps, const Settings& s);
+// lskum_run: reset the store to the configured layout + free stream + solve.
+// Single-domain runs initialise the state on the device and leave the host
+// store to the copy-back; on an early failure the host store gets the same
+// reset + free stream the reference leaves (lskum_capi.cpp:209-220).
+RunRecord solve_from_freestream(PointSet& ps, const Settings& s);
 
 }  // namespace lskb

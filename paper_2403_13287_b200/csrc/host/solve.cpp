@@ -2,6 +2,7 @@
 // runtime.cpp:195-275): config check, stencil screening gate, bisection into
 // `parts` pieces (the pieces fix the error tie-break order and, with gpus > 1,
 // the device domains), then the device loop.
+#include <cmath>
 #include <algorithm>
 
 #include "../engine.hpp"
@@ -51,6 +52,34 @@ EngineSpec prepare_run(const PointSet& ps, const Settings& s) {
   EngineSpec spec = spec_from(ps, s, scr.det_tol);
   trace("prepare: partitioned");
   return spec;
+}
+
+RunRecord solve_from_freestream(PointSet& ps, const Settings& s) {
+  s.check();
+  if (s.gpus > 1 || s.iters <= 0) {
+    ps.reset_fields(s.layout);
+    freestream(ps, s.mach, s.aoa, s.gamma);
+    return solve_on_device(ps, s);
+  }
+  bool written = false;
+  try {
+    EngineSpec spec = prepare_run(ps, s);
+    if (!(ps.fields.size() == ps.n() && ps.fields.layout() == s.layout)) ps.fields = FieldBlock(s.layout, ps.n());
+    const double a = s.aoa * M_PI / 180.0;  // freestream_init, bench.cpp:43-56
+    spec.fs_device = true;
+    spec.fs_prim[0] = 1.0;
+    spec.fs_prim[1] = s.mach * std::cos(a);
+    spec.fs_prim[2] = s.mach * std::sin(a);
+    spec.fs_prim[3] = 1.0 / s.gamma;
+    spec.store_written = &written;
+    return engine_run(ps, spec);
+  } catch (...) {
+    if (!written) {
+      ps.reset_fields(s.layout);
+      freestream(ps, s.mach, s.aoa, s.gamma);
+    }
+    throw;
+  }
 }
 
 RunRecord solve_on_device(PointSet& ps, const Settings& s) {
