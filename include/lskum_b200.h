@@ -37,6 +37,11 @@ int lskum_b200_cloud_from_arrays(int32_t n, const double* x, const double* y,
                                  const int64_t* offsets, const int32_t* nbrs,
                                  lskum_cloud** out);
 int lskum_b200_cloud_nnz(const lskum_cloud* cloud, int64_t* out);
+/* validate_cloud (reference cloud.cpp:252-321) computed on `device` — the
+ * screening lskum_run performs there; same report and
+ * defective ids (ascending) as lskum_cloud_validate / _defective_ids. */
+int lskum_b200_cloud_validate_device(lskum_cloud* cloud, int device, lskum_validation* out, int32_t* ids,
+                                     int32_t cap, int32_t* n_out);
 /* Synthetic NACA 0012 O-cloud (no reference counterpart, the
  * reference's generators are cloud.cpp:323-425): n_wall surface points (even),
  * n_rings rings out to a far-field circle of radius outer_radius chords about

@@ -9,6 +9,8 @@
 // globaltimer-stamped device durations.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -447,6 +449,64 @@ __global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const
 }
 
 // Scatters the primitives (slots 0-3 of a FieldBlock in either layout) into D4 records.
+// ---- stencil screening on the device (reference validate_cloud,
+// cloud.cpp:252-321; host twin: host/screen.cpp).  Same sums in the same
+// order with separately rounded products and sums, so determinants, the
+// defective set and the report are bitwise the reference's.
+struct ScreenOut {
+  unsigned long long n_finite;
+  int n_defective, n_wall_isolated, min_size, pad;
+};
+
+// Nearest-neighbour distances as sortable keys (non-negative doubles order
+// like their bit patterns; non-finite values sort last) + the finite count.
+__global__ void k_screen_keys(int n, const double* mind, unsigned long long* keys, ScreenOut* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double d = mind[i];
+  keys[i] = static_cast<unsigned long long>(__double_as_longlong(d));
+  if (isfinite(d)) atomicAdd(&out->n_finite, 1ull);
+}
+
+__global__ void k_screen(Geo g, double tol, ScreenOut* out, int* defective, int cap) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.n) return;
+  double fxx = 0.0, fxy = 0.0, fyy = 0.0, hxx[4] = {0, 0, 0, 0}, hxy[4] = {0, 0, 0, 0}, hyy[4] = {0, 0, 0, 0};
+  int fc = 0, hc[4] = {0, 0, 0, 0}, walls = 0;
+  const double2 pp = g.xy[p];
+  for (int e = g.off[p]; e < g.off[p + 1]; ++e) {
+    const int nb = g.nbr[e];
+    const double2 pn = g.xy[nb];
+    const double dx = X::sub(pn.x, pp.x), dy = X::sub(pn.y, pp.y);
+    const double xx = X::mul(dx, dx), xy = X::mul(dx, dy), yy = X::mul(dy, dy);
+    fxx = X::add(fxx, xx);
+    fxy = X::add(fxy, xy);
+    fyy = X::add(fyy, yy);
+    ++fc;
+    const bool in[4] = {dx >= 0.0, dx <= 0.0, dy >= 0.0, dy <= 0.0};
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      if (in[h]) {
+        hxx[h] = X::add(hxx[h], xx);
+        hxy[h] = X::add(hxy[h], xy);
+        hyy[h] = X::add(hyy[h], yy);
+        ++hc[h];
+      }
+    if (g.kind[nb] == KIND_WALL) ++walls;
+  }
+  bool bad = X::sub(X::mul(fxx, fyy), X::mul(fxy, fxy)) < tol || fc < 3;
+  if (g.kind[p] != KIND_OUTER)
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      bad = bad || hc[h] == 0 || X::sub(X::mul(hxx[h], hyy[h]), X::mul(hxy[h], hxy[h])) < tol;
+  if (bad) {
+    const int slot = atomicAdd(&out->n_defective, 1);
+    if (slot < cap) defective[slot] = p;
+  }
+  if (g.kind[p] == KIND_WALL && walls < 2) atomicAdd(&out->n_wall_isolated, 1);
+  atomicMin(&out->min_size, fc);
+}
+
 __global__ void k_fill_d4(D4* out, int n, D4 v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
 }
@@ -680,6 +740,48 @@ class Domain {
   int n_loc() const { return n_loc_; }
   int device() const { return device_; }
   int global_of(int local) const { return gid_host_.empty() ? local : gid_host_[local]; }
+
+  // ---- stencil screening (validate_cloud) on the device-resident geometry ----
+  Screening screen() {
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    Screening out;
+    const int n = n_;
+    if (n <= 0) return out;
+    DBuf<ScreenOut> so(1, st_);
+    ScreenOut init{0, 0, 0, 0x7FFFFFFF, 0};
+    ck(cudaMemcpyAsync(so.get(), &init, sizeof init, cudaMemcpyHostToDevice, st_), "H2D screen");
+    DBuf<unsigned long long> keys(static_cast<std::size_t>(n), st_), sorted(static_cast<std::size_t>(n), st_);
+    k_screen_keys<<<(n + 255) / 256, 256, 0, st_>>>(n, mind_.get(), keys.get(), so.get());
+    std::size_t tmp_bytes = 0;
+    ck(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort size");
+    DBuf<char> tmp(std::max<std::size_t>(1, tmp_bytes), st_);
+    ck(cub::DeviceRadixSort::SortKeys(tmp.get(), tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort");
+    ScreenOut head{};
+    ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
+    ck(cudaStreamSynchronize(st_), "screen keys");
+    if (head.n_finite > 0) {
+      unsigned long long bits = 0;
+      ck(cudaMemcpy(&bits, sorted.get() + (head.n_finite - 1) / 2, sizeof bits, cudaMemcpyDeviceToHost), "D2H h_ref");
+      std::memcpy(&out.h_ref, &bits, sizeof bits);
+    }
+    out.det_tol = 1e-12 * out.h_ref * out.h_ref * out.h_ref * out.h_ref;  // cloud.cpp:274
+    const int cap = n;
+    DBuf<int> bad(static_cast<std::size_t>(cap), st_);
+    k_screen<<<(n + 255) / 256, 256, 0, st_>>>(geo(), out.det_tol, so.get(), bad.get(), cap);
+    ck(cudaGetLastError(), "k_screen");
+    ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
+    ck(cudaStreamSynchronize(st_), "screen");
+    out.n_defective = head.n_defective;
+    out.n_wall_isolated = head.n_wall_isolated;
+    out.min_stencil = head.min_size;
+    out.defective.resize(static_cast<std::size_t>(head.n_defective));
+    if (head.n_defective > 0) {
+      ck(cudaMemcpy(out.defective.data(), bad.get(), sizeof(int) * head.n_defective, cudaMemcpyDeviceToHost),
+         "D2H defective");
+      std::sort(out.defective.begin(), out.defective.end());
+    }
+    return out;
+  }
 
   // ---- state transfer (FieldBlock <-> device records) ----
   // Uniform primitive state on owned and halo points (lskum_run's free stream).
@@ -1312,6 +1414,34 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
   d.begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
   return d;
 }
+
+}  // namespace
+
+// lskum_run's stencil screening on the device: uploads the
+// geometry into the cloud's resident domain (which the run then reuses) and
+// screens it there.  The report is cached on the cloud like the host one.
+Screening engine_screen(PointSet& ps, int device, double gamma, double cfl, int capacity) {
+  auto* c = static_cast<EngineCache*>(ps.engine_cache.get());
+  if (!(c && c->device == device && c->dom)) {
+    ps.engine_cache.reset();
+    auto fresh = std::make_shared<EngineCache>();
+    fresh->device = device;
+    fresh->dom = std::make_unique<Domain>(view_of(ps, {}), device, gamma, cfl, 0.0, std::max(1, capacity));
+    trace("engine: geometry uploaded");
+    ps.engine_cache = fresh;
+    c = fresh.get();
+  }
+  Screening scr = c->dom->screen();
+  trace("engine: screened on device");
+  return scr;
+}
+
+void engine_prescreen(PointSet& ps, const Settings& s) {
+  if (ps.screening || s.gpus > 1) return;
+  ps.screening = std::make_shared<const Screening>(engine_screen(ps, s.device, s.gamma, s.cfl, s.iters));
+}
+
+namespace {
 
 // Copy-back of the reference's end-of-run store: prim (final), q of the last
 // iteration, published qx/qy, flux_res and delta_t of the last iteration.

@@ -32,6 +32,12 @@ struct EngineSpec {
   bool* store_written = nullptr;
 };
 
+// Stencil screening on the device into ps.screening (single-device runs; no-op
+// when the report is cached or gpus > 1).
+void engine_prescreen(PointSet& ps, const Settings& s);
+// The same report computed on `device` (kept resident in the cloud's cache).
+Screening engine_screen(PointSet& ps, int device, double gamma = 1.4, double cfl = 0.5, int capacity = 1);
+
 // Config check + stencil screening gate + bisection (host side of a run).
 EngineSpec prepare_run(const PointSet& ps, const Settings& s);
 

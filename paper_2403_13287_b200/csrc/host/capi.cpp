@@ -135,6 +135,23 @@ int lskum_cloud_validate(const lskum_cloud* cloud, lskum_validation* out) {
   });
 }
 
+int lskum_b200_cloud_validate_device(lskum_cloud* cloud, int device, lskum_validation* out, int32_t* ids,
+                                     int32_t cap, int32_t* n_out) {
+  if (!cloud || !out || !n_out || (cap > 0 && !ids)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
+  return guard([&] {
+    const lskb::Screening s = lskb::engine_screen(cloud->ps, device);
+    out->n_points = cloud->ps.n();
+    out->n_defective = s.n_defective;
+    out->n_wall_isolated = s.n_wall_isolated;
+    out->min_stencil_size = s.min_stencil;
+    out->h_ref = s.h_ref;
+    out->det_tol = s.det_tol;
+    *n_out = s.n_defective;
+    const int32_t m = std::min<int32_t>(cap, static_cast<int32_t>(s.defective.size()));
+    for (int32_t i = 0; i < m; ++i) ids[i] = s.defective[i];
+  });
+}
+
 int lskum_cloud_defective_ids(const lskum_cloud* cloud, int32_t* ids, int32_t cap, int32_t* n_out) {
   if (!cloud || !n_out || (cap > 0 && !ids)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
   return guard([&] {

@@ -3,6 +3,7 @@
 // `parts` pieces (the pieces fix the error tie-break order and, with gpus > 1,
 // the device domains), then the device loop.
 #include <cmath>
+#include <cstdlib>
 #include <algorithm>
 
 #include "../engine.hpp"
@@ -11,6 +12,15 @@
 namespace lskb {
 
 namespace {
+
+// lskum_run screens on the device (LSKUM_DEVICE_SCREEN=0: on the host).
+bool device_screening() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSKUM_DEVICE_SCREEN");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
 
 EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
   EngineSpec spec;
@@ -63,6 +73,14 @@ RunRecord solve_from_freestream(PointSet& ps, const Settings& s) {
   }
   bool written = false;
   try {
+    if (!ps.screening && device_screening()) {
+      try {
+        engine_prescreen(ps, s);
+      } catch (const Fault&) {
+        // no usable device: screen on the host, so a defective cloud still
+        // reports LSKUM_ERR_VALIDATION before any device error
+      }
+    }
     EngineSpec spec = prepare_run(ps, s);
     if (!(ps.fields.size() == ps.n() && ps.fields.layout() == s.layout)) ps.fields = FieldBlock(s.layout, ps.n());
     const double a = s.aoa * M_PI / 180.0;  // freestream_init, bench.cpp:43-56

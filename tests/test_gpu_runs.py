@@ -275,3 +275,26 @@ def test_cached_domain_reruns_match_fresh_clouds(bump_cloud_arrays):
         (r1, f1), (r2, f2) = out
         assert (r1 == r2) if isinstance(r1, str) else np.array_equal(r1, r2), cfg
         assert np.array_equal(f1, f2), cfg
+
+
+@pytest.mark.parametrize("which", ["rect", "annulus", "naca_wall", "naca_frozen", "grid"])
+def test_device_screening_equals_host(which):
+    """validate_cloud on the device (lskum_run's screening) == the host
+    screening, itself pinned to the reference: report and defective ids."""
+    if which == "rect":
+        c = L.Cloud.generate_rect(60, 50, 0.1, 3, 8)
+    elif which == "annulus":
+        c = L.Cloud.generate_annulus(64, 12, 6.0, 0.1, 5, 8)
+    elif which == "naca_wall":
+        c = L.Cloud.generate_naca0012(160, 60, 20.0, 0.05, 5, 8)
+    elif which == "naca_frozen":
+        c = L.Cloud.generate_naca0012(160, 60, 20.0, 0.0, 5, 8, frozen_wall=True)
+    else:
+        c = L.Cloud.generate_rect(30, 30, 0.0, 1, 8)
+    want = c.validate()
+    got, ids = c.validate_device(0)
+    for key in ("n_points", "n_defective", "n_wall_isolated", "min_stencil_size", "h_ref", "det_tol"):
+        assert got[key] == want[key], key
+    assert np.array_equal(ids, c.defective_ids())
+    if which in ("naca_wall", "annulus"):
+        assert want["n_defective"] + want["n_wall_isolated"] > 0  # the check is not vacuous
