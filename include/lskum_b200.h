@@ -37,6 +37,13 @@ int lskum_b200_cloud_from_arrays(int32_t n, const double* x, const double* y,
                                  const int64_t* offsets, const int32_t* nbrs,
                                  lskum_cloud** out);
 int lskum_b200_cloud_nnz(const lskum_cloud* cloud, int64_t* out);
+/* Surface force coefficients from the cloud's current pressures (SURVEY
+ * 8(f)-4; the reference has Cp only, bench.cpp:101-105): out = {Cl, Cd, Cm
+ * about the quarter chord, chord}.  loop = surface point ids around the body
+ * in order (n = 0: the wall points in id order); panels carry the mean Cp of
+ * their end points; M and AoA from cfg. */
+int lskum_b200_surface_forces(const lskum_cloud* cloud, const lskum_config* cfg, const int32_t* loop, int32_t n,
+                              double out[4]);
 /* validate_cloud (reference cloud.cpp:252-321) computed on `device` — the
  * screening lskum_run performs there; same report and
  * defective ids (ascending) as lskum_cloud_validate / _defective_ids. */

@@ -286,6 +286,19 @@ int lskum_result_write_outputs(const lskum_result* r, const lskum_cloud* cloud, 
 
 void lskum_result_destroy(lskum_result* r) { delete r; }
 
+int lskum_b200_surface_forces(const lskum_cloud* cloud, const lskum_config* cfg, const int32_t* loop, int32_t n,
+                              double out[4]) {
+  if (!cloud || !cfg || !out || (n > 0 && !loop)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
+  return guard([&] {
+    const std::vector<std::int32_t> ids(loop, loop + std::max<int32_t>(n, 0));
+    const lskb::Forces f = lskb::surface_forces(cloud->ps, ids, cfg->s.mach, cfg->s.aoa, cfg->s.gamma);
+    out[0] = f.cl;
+    out[1] = f.cd;
+    out[2] = f.cm;
+    out[3] = f.chord;
+  });
+}
+
 // ---------------------------------------------------------------- metrics / diagnostics
 int lskum_rdp(double wall_seconds, int64_t iterations, int64_t n_points, double* out) {
   NONNULL(out);

@@ -201,6 +201,12 @@ void freestream(PointSet& ps, double mach, double aoa_deg, double gamma);
 double rate_of_data_processing(double seconds, std::int64_t iters, std::int64_t n);
 double relative_rate(double rdp_test, double rdp_ref);
 double pressure_coeff(double p, double mach, double gamma);
+struct Forces {
+  double cl = 0.0, cd = 0.0, cm = 0.0, chord = 0.0;
+  std::int32_t points = 0;
+};
+Forces surface_forces(const PointSet& ps, const std::vector<std::int32_t>& loop, double mach, double aoa_deg,
+                      double gamma);
 
 struct KernelRow {
   std::string name;

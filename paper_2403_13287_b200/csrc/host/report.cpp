@@ -102,6 +102,61 @@ Report summarize(const RunRecord& run, std::int32_t n) {
   return rep;
 }
 
+// Surface force coefficients (new: the reference has Cp only,
+// bench.cpp:101-105).  The surface is the closed polygon through `loop`
+// (point ids in order; empty = the wall points in id order, the generators'
+// boundary order).  Each panel carries the mean Cp of its end points; the
+// force on the body is -sum Cp n ds over panels, n the panel normal pointing
+// out of the enclosed body region; coefficients are per unit chord (the
+// loop's x extent) in the free-stream frame: Cl normal to it, Cd along it,
+// Cm about the quarter chord (positive nose up).
+Forces surface_forces(const PointSet& ps, const std::vector<std::int32_t>& loop_in, double mach, double aoa_deg,
+                      double gamma) {
+  std::vector<std::int32_t> loop = loop_in;
+  if (loop.empty())
+    for (std::int32_t i = 0; i < ps.n(); ++i)
+      if (ps.kind[i] == Kind::wall) loop.push_back(i);
+  if (loop.size() < 3) raise(Status::argument, "surface forces need a closed loop of >= 3 surface points");
+  for (std::int32_t p : loop)
+    if (p < 0 || p >= ps.n()) raise(Status::argument, "surface point id out of range");
+  if (mach == 0.0) raise(Status::argument, "force coefficients need a nonzero Mach number");
+  const std::size_t m = loop.size();
+  double area2 = 0.0, xmin = ps.x[loop[0]], xmax = xmin, ylead = ps.y[loop[0]];
+  for (std::size_t k = 0; k < m; ++k) {
+    const std::int32_t a = loop[k], b = loop[(k + 1) % m];
+    area2 += ps.x[a] * ps.y[b] - ps.x[b] * ps.y[a];
+    if (ps.x[a] < xmin) {
+      xmin = ps.x[a];
+      ylead = ps.y[a];
+    }
+    xmax = std::max(xmax, ps.x[a]);
+  }
+  const double chord = xmax - xmin;
+  if (!(chord > 0.0)) raise(Status::argument, "degenerate surface loop (zero chord)");
+  const double orient = area2 > 0.0 ? 1.0 : -1.0;  // counter-clockwise: outward normal (dy, -dx)
+  const double xr = xmin + 0.25 * chord, yr = ylead;
+  double fx = 0.0, fy = 0.0, mz = 0.0;
+  for (std::size_t k = 0; k < m; ++k) {
+    const std::int32_t a = loop[k], b = loop[(k + 1) % m];
+    const double cp = 0.5 * (pressure_coeff(ps.fields.at(a, slot::prim + 3), mach, gamma) +
+                             pressure_coeff(ps.fields.at(b, slot::prim + 3), mach, gamma));
+    const double dx = ps.x[b] - ps.x[a], dy = ps.y[b] - ps.y[a];
+    const double px = -cp * orient * dy, py = cp * orient * dx;  // -cp * n ds
+    fx += px;
+    fy += py;
+    const double cx = 0.5 * (ps.x[a] + ps.x[b]) - xr, cy = 0.5 * (ps.y[a] + ps.y[b]) - yr;
+    mz += cx * py - cy * px;
+  }
+  const double a = aoa_deg * M_PI / 180.0;
+  Forces f;
+  f.cl = (fy * std::cos(a) - fx * std::sin(a)) / chord;
+  f.cd = (fx * std::cos(a) + fy * std::sin(a)) / chord;
+  f.cm = -mz / (chord * chord);
+  f.chord = chord;
+  f.points = static_cast<std::int32_t>(m);
+  return f;
+}
+
 void write_run_outputs(const std::string& prefix, const PointSet& ps, const RunRecord& run,
                        const Report& rep, const Settings& s) {
   {
