@@ -56,6 +56,23 @@ inline constexpr int prim = 0, q = 4, qx = 8, qy = 12, res = 16, dt = 20, count 
 // Per-point solver fields in one buffer; AoS or SoA differ only in strides
 // (reference layout.hpp:24-48).  The GPU never sees this block directly: it
 // is the staging/copy-back format behind lskum_cloud_primitive/fields_equal.
+// std::allocator without value-initialisation of default-constructed elements.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) > 0) ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    else ::new (static_cast<void*>(p)) U;
+  }
+};
+
 class FieldBlock {
  public:
   FieldBlock() = default;
@@ -82,7 +99,9 @@ class FieldBlock {
   }
   Layout layout_ = Layout::aos;
   std::int32_t n_ = 0;
-  std::vector<double> data_;
+  // Allocated without value-initialisation; the constructor zero-fills it in
+  // parallel (first touch spread over threads: hundreds of MB at 10M+ points).
+  std::vector<double, NoInitAlloc<double>> data_;
 };
 
 // Bitwise comparison over every (point, slot) (reference layout.cpp:29-45).
