@@ -107,6 +107,16 @@ __device__ __forceinline__ void stencil_of(const Geo& g, int i, int& e0, int& k)
   }
 }
 
+// Programmatic dependent launch: the iteration's kernels are launched with
+// programmatic stream serialisation, so each can be scheduled while its
+// predecessor drains; it waits here for the predecessor's completion (and
+// memory) before touching anything, then lets its own successor launch.
+// Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
@@ -203,6 +213,7 @@ template <bool S, int MB>
 __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__ q,
                                                    const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
                                                    Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
+  pdl_enter();
   using A = Ar<S>;
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_SWEEP);
@@ -282,6 +293,7 @@ template <bool S, int MB, int K = 0>
 __global__ void __launch_bounds__(256, MB) k_sweep2(Geo g, const D4* __restrict__ q,
                                                     const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
                                                     Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
+  pdl_enter();
   using A = Ar<S>;
   __shared__ int s_skip;
   ktimer_begin(ctl, KT_SWEEP);
@@ -405,6 +417,7 @@ __host__ __device__ inline int flux_stride(int kcap) {
 // warp-uniform branch.
 template <int W, bool S, int MB>
 __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxArgs a) {
+  pdl_enter();
   constexpr int P = flux_points_per_block(W);
   constexpr int NOWN = W >= 16 ? 16 : W;        // lanes owning accumulators
   constexpr int NC = 16 / NOWN;                 // components per owning lane
@@ -708,6 +721,7 @@ template <int MB>
 __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* __restrict__ w1,
                                                     const double2* __restrict__ w2,
                                                     const std::uint8_t* __restrict__ sing) {
+  pdl_enter();
   constexpr unsigned kFull = 0xFFFFFFFFu;
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_FLUX);
@@ -827,6 +841,7 @@ template <int MB>
 __global__ void __launch_bounds__(256, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
                                                      const double2* __restrict__ w2,
                                                      const std::uint8_t* __restrict__ sing) {
+  pdl_enter();
   extern __shared__ __align__(16) char fsm[];
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_FLUX);
@@ -905,6 +920,7 @@ struct UpdateArgs {
 };
 
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
+  pdl_enter();
   __shared__ int s_skip;
   ktimer_begin(a.ctl, KT_UPDATE);
   if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_update(a.ctl));
@@ -1101,6 +1117,7 @@ constexpr int kTreeThreadLevels = 8;
 __global__ void __launch_bounds__(kTreeThreads)
     k_tree_partial(const double* v, long long n, int d1, double* part_val, long long* part_sz,
                    Ctl* ctl) {
+  pdl_enter();
   __shared__ double sv[2][kTreeThreads];
   __shared__ long long ss[2][kTreeThreads];
   __shared__ int s_skip;
@@ -1131,6 +1148,7 @@ __global__ void __launch_bounds__(kTreeThreads)
 __global__ void __launch_bounds__(1024)
     k_tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
                  double* history, unsigned long long* iter_t1, Ctl* ctl) {
+  pdl_enter();
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
   __shared__ int s_skip;
