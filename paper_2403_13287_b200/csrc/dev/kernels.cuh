@@ -671,23 +671,25 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   // fma(rho_n, x_n, -gi) would leave ~1 ulp where the states are equal
   // (the free stream must stay an exact fixed point).
   double gi[4], gn[4];
-  split_flux<false>(fi, at[0], 0, !(dx <= 0.0), gi);
-  split_flux<false>(fn, at[1], 0, !(dx <= 0.0), gn);
+  const double epi = fi.e + fi.p, kki = fma(0.5, fi.p, fi.e);
+  const double epn = fn.e + fn.p, kkn = fma(0.5, fn.p, fn.e);
+  split_flux_fast<0>(fi, at[0], !(dx <= 0.0), epi, kki, gi);
+  split_flux_fast<0>(fn, at[1], !(dx <= 0.0), epn, kkn, gn);
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = fma(wx, X::sub(gn[c], gi[c]), acc[c]);
-  split_flux<false>(fi, at[2], 1, !(dy <= 0.0), gi);
-  split_flux<false>(fn, at[3], 1, !(dy <= 0.0), gn);
+  split_flux_fast<1>(fi, at[2], !(dy <= 0.0), epi, kki, gi);
+  split_flux_fast<1>(fn, at[3], !(dy <= 0.0), epn, kkn, gn);
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
   // a zero offset belongs to both half stencils: add the minus direction
   if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
     const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? *w2e : make_double2(0.0, 0.0);
-    split_flux<false>(fi, at[0], 0, true, gi);
-    split_flux<false>(fn, at[1], 0, true, gn);
+    split_flux_fast<0>(fi, at[0], true, epi, kki, gi);
+    split_flux_fast<0>(fn, at[1], true, epn, kkn, gn);
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[c] = fma(v.x, X::sub(gn[c], gi[c]), acc[c]);
-    split_flux<false>(fi, at[2], 1, true, gi);
-    split_flux<false>(fn, at[3], 1, true, gn);
+    split_flux_fast<1>(fi, at[2], true, epi, kki, gi);
+    split_flux_fast<1>(fn, at[3], true, epn, kkn, gn);
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[c] = fma(v.y, X::sub(gn[c], gi[c]), acc[c]);
   }

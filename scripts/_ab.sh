@@ -1,4 +1,4 @@
-for v in "LSKUM_PDL=0" "LSKUM_PDL=1"; do
+for v in "LSKUM_PDL=0"; do
   echo "== $v"; env $v PROBE_ORDERS=2 timeout 300 python scripts/probe_perf.py 400 3163 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
