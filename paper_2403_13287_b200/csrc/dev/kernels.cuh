@@ -839,8 +839,8 @@ __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1
   }
 }
 
-template <int MB>
-__global__ void __launch_bounds__(256, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
+template <int MB, int NW = kFluxWarps>
+__global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
                                                      const double2* __restrict__ w2,
                                                      const std::uint8_t* __restrict__ sing) {
   pdl_enter();
@@ -856,8 +856,8 @@ __global__ void __launch_bounds__(256, MB) k_flux_ws(FluxArgs a, const double2* 
   char* const stage0 = fsm + (2 * warp) * kFluxStageBytes;  // stage b at stage0 + b * kFluxStageBytes
   const Geo& g = a.g;
   const int groups = (g.n + 3) >> 2;
-  const int nwarps = gridDim.x * kFluxWarps;
-  int grp = blockIdx.x * kFluxWarps + warp;
+  const int nwarps = gridDim.x * NW;
+  int grp = blockIdx.x * NW + warp;
   if (!s_skip && grp < groups) {
     StageIdx cur = stage_index(g, stage_load(g, grp, lane, sub), lane);
     stage_issue(a, w1, cur, stage0, lane32, lane, sub);
