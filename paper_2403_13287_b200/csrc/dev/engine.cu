@@ -232,22 +232,39 @@ int resident_blocks(K kern, int slot) {
   return r;
 }
 
+// The unrolled 8-point sweep in blocks of NT threads (MB resident per SM).
+template <bool S, int MB, int NT>
+void sweep8_launch(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                   unsigned long long* it0, int sweep, cudaStream_t st) {
+  static int resident[64] = {};  // per instantiation and device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!resident[dev & 63]) {
+    int per_sm = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep2<S, MB, 8, NT>, NT, 0), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    resident[dev & 63] = std::max(1, per_sm) * sms;
+  }
+  const int grid = std::max(1, std::min((2 * g.n + NT - 1) / NT, resident[dev & 63]));
+  launch_pdl(k_sweep2<S, MB, 8, NT>, grid, NT, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
+}
+
+// 128-thread blocks for the unrolled sweep (LSKUM_SWEEP_BLOCK=128).
+bool sweep_small_blocks() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSKUM_SWEEP_BLOCK");
+    return e && std::atoi(e) == 128;
+  }();
+  return on;
+}
+
 template <bool S, int MB>
 void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
                     unsigned long long* it0, int sweep, cudaStream_t st) {
   const int slot = (S ? 4 : 0) + MB - 2;
   if (sweep_lanes() == 2 && g.kfix == 8 && sweep_unrolled()) {
-    static int resident[64] = {};  // per (S, MB) instantiation and device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!resident[dev & 63]) {
-      int per_sm = 0, sms = 0;
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep2<S, MB, 8>, 256, 0), "occupancy");
-      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-      resident[dev & 63] = std::max(1, per_sm) * sms;
-    }
-    const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident[dev & 63]));
-    launch_pdl(k_sweep2<S, MB, 8>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
+    if (sweep_small_blocks()) sweep8_launch<S, 2 * MB, 128>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep8_launch<S, MB, 256>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   } else if (sweep_lanes() == 2) {
     const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
     launch_pdl(k_sweep2<S, MB, 0>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);

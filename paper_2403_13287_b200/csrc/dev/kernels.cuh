@@ -289,8 +289,8 @@ __device__ __forceinline__ int4 ld_i4(const int* p) {
   return v;
 }
 
-template <bool S, int MB, int K = 0>
-__global__ void __launch_bounds__(256, MB) k_sweep2(Geo g, const D4* __restrict__ q,
+template <bool S, int MB, int K = 0, int NT = 256>
+__global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__ q,
                                                     const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
                                                     Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
   pdl_enter();

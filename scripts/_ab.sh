@@ -1,4 +1,4 @@
-for v in "LSKUM_FLUX_WS=8x2" "LSKUM_FLUX_WS=4x4" "LSKUM_FLUX_WS=4x5" "LSKUM_FLUX_WS=6x3"; do
+for v in "LSKUM_SWEEP_BLOCK=256" "LSKUM_SWEEP_BLOCK=128"; do
   echo "== $v"; env $v PROBE_ORDERS=2 timeout 300 python scripts/probe_perf.py 400 3163 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
