@@ -443,8 +443,10 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
   const int nb = g.nbr[g.off[i] + j];
   const double2 pn = g.xy[nb];
   const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-  const D4 qi = q[i], qxi = dq[2 * i], qyi = dq[2 * i + 1];
-  const D4 qn = q[nb], qxn = dq[2 * nb], qyn = dq[2 * nb + 1];
+  const D4 qi = q[i], qn = q[nb];
+  D4 qxi, qyi, qxn, qyn;
+  dq_load(dq, i, qxi, qyi);
+  dq_load(dq, nb, qxn, qyn);
   double ti[4], tn[4];
   for (int c = 0; c < 4; ++c) {
     ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
@@ -503,7 +505,9 @@ __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter
 __global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, const D4* res,
                               const double* dt, double* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const D4 v[5] = {prim[i], q[i], dq[2 * i], dq[2 * i + 1], res[i]};
+    D4 qx, qy;
+    dq_load(dq, i, qx, qy);
+    const D4 v[5] = {prim[i], q[i], qx, qy, res[i]};
     double r[21];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -580,6 +584,21 @@ __global__ void k_screen(Geo g, double tol, ScreenOut* out, int* defective, int 
   }
   if (g.kind[p] == KIND_WALL && walls < 2) atomicAdd(&out->n_wall_isolated, 1);
   atomicMin(&out->min_size, fc);
+}
+
+// Derivative records <-> the reference's scratch layout [qx0..3, qy0..3]:
+// to_records = 1: plain -> records, 0: records -> plain.
+__global__ void k_dq_layout(const D4* in, D4* out, long long n, int to_records) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  if (to_records) {
+    dq_store(out, i, ld4(in + 2 * i), ld4(in + 2 * i + 1));
+  } else {
+    D4 qx, qy;
+    dq_load(in, i, qx, qy);
+    st4(out + 2 * i, qx);
+    st4(out + 2 * i + 1, qy);
+  }
 }
 
 __global__ void k_fill_d4(D4* out, int n, D4 v) {
@@ -905,9 +924,10 @@ class Domain {
       const int p = static_cast<int>(i);
       hp[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2), f.at(p, slot::prim + 3)};
       hp[n + i] = D4{f.at(p, slot::q), f.at(p, slot::q + 1), f.at(p, slot::q + 2), f.at(p, slot::q + 3)};
-      hp[2 * n + 2 * i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qx + 2), f.at(p, slot::qx + 3)};
+      // derivative records per component pair (dq_load/dq_store layout)
+      hp[2 * n + 2 * i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qy), f.at(p, slot::qy + 1)};
       hp[2 * n + 2 * i + 1] =
-          D4{f.at(p, slot::qy), f.at(p, slot::qy + 1), f.at(p, slot::qy + 2), f.at(p, slot::qy + 3)};
+          D4{f.at(p, slot::qx + 2), f.at(p, slot::qx + 3), f.at(p, slot::qy + 2), f.at(p, slot::qy + 3)};
       hp[4 * n + i] =
           D4{f.at(p, slot::res), f.at(p, slot::res + 1), f.at(p, slot::res + 2), f.at(p, slot::res + 3)};
       reinterpret_cast<double*>(hp + 5 * n)[i] = f.at(p, slot::dt);
@@ -962,8 +982,9 @@ class Domain {
         f.at(p, slot::q + 2) = q.c;
         f.at(p, slot::q + 3) = q.d;
       }
-      const D4& qx = hp[2 * n + 2 * i];
-      const D4& qy = hp[2 * n + 2 * i + 1];
+      const D4& r0 = hp[2 * n + 2 * i];
+      const D4& r1 = hp[2 * n + 2 * i + 1];
+      const D4 qx{r0.a, r0.b, r1.a, r1.b}, qy{r0.c, r0.d, r1.c, r1.d};
       const D4& r = hp[4 * n + i];
       for (int c = 0; c < 4; ++c) {
         f.at(p, slot::qx + c) = comp(qx, c);
@@ -2380,10 +2401,10 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
     case Op::q_derivatives:
       sweep_launch(spec.fp_mode == 1, g, d.q_buf(0), d.dq_buf(0), d.dq_buf(1), d.gas(), d.dctl(), nullptr, 0, st);
       break;
-    case Op::publish:
+    case Op::publish:  // scratch is the reference's [qx0..3, qy0..3] per point
       ck(cudaMemcpyAsync(d.dq_buf(1), scratch, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D scratch");
-      k_copy_d4<<<static_cast<int>((2 * nn + 255) / 256), 256, 0, st>>>(d.dq_buf(1), d.dq_buf(0),
-                                                                       static_cast<long long>(2 * nn));
+      k_dq_layout<<<static_cast<int>((nn + 255) / 256), 256, 0, st>>>(d.dq_buf(1), d.dq_buf(0),
+                                                                     static_cast<long long>(nn), 1);
       break;
     case Op::flux_fused:
     case Op::flux_direction: {
@@ -2413,7 +2434,11 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
   d.refresh_ctl();
   if (d.failed()) throw d.fault(false, d.q_buf(0), d.dq_buf(0));
   if (op == Op::q_derivatives) {
-    ck(cudaMemcpy(scratch, d.dq_buf(1), nn * 8 * sizeof(double), cudaMemcpyDeviceToHost), "D2H scratch");
+    DBuf<D4> plain(2 * nn, st);
+    k_dq_layout<<<static_cast<int>((nn + 255) / 256), 256, 0, st>>>(d.dq_buf(1), plain.get(),
+                                                                   static_cast<long long>(nn), 0);
+    ck(cudaMemcpyAsync(scratch, plain.get(), nn * 8 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H scratch");
+    ck(cudaStreamSynchronize(st), "scratch");
     return;  // the store itself is untouched (reference kernels.hpp:30-35)
   }
   d.download(ps.fields, true, d.q_buf(0), d.dq_buf(0));

@@ -14,7 +14,7 @@
 // Data layout in HBM (structure of arrays of 32-byte records):
 //   xy  double2[n]        nrm double2[n]     kind u8[n]     part u8[n]
 //   off int32[n+1]        nbr int32[nnz]     mind double[n] (geometry, per run)
-//   prim D4[n]            q[2] D4[n]         dq[2] D4[2n]  ({qx}, {qy} per point)
+//   prim D4[n]            q[2] D4[n]         dq[2] D4[2n]  ({qx0,qx1,qy0,qy1}, {qx2,qx3,qy2,qy3})
 //   res D4[n] (every iteration), dt double[n] (copy-back iteration only), mag double[n]
 // Every D4 gather is one 256-bit LDG (one 32-byte sector).
 #pragma once
@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n; i += gridDim.x * blockDim.x) {
     const double2 pi = g.xy[i];
-    const D4 qi = ld4(q + i), qxi = ld4(dq_in + 2 * i), qyi = ld4(dq_in + 2 * i + 1);
+    const D4 qi = ld4(q + i);
+    D4 qxi, qyi;
+    dq_load(dq_in, i, qxi, qyi);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
     int e0, k;
@@ -230,7 +232,9 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
       const int nb = g.nbr[e];
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const D4 qn = ld4(q + nb), qxn = ld4(dq_in + 2 * nb), qyn = ld4(dq_in + 2 * nb + 1);
+      const D4 qn = ld4(q + nb);
+      D4 qxn, qyn;
+      dq_load(dq_in, nb, qxn, qyn);
       sxx = A::add(sxx, A::mul(dx, dx));
       sxy = A::add(sxy, A::mul(dx, dy));
       syy = A::add(syy, A::mul(dy, dy));
@@ -255,8 +259,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
       fy.b = A::sub(A::mul(sxx, by[1]), A::mul(sxy, bx[1])) / det;
       fy.c = A::sub(A::mul(sxx, by[2]), A::mul(sxy, bx[2])) / det;
       fy.d = A::sub(A::mul(sxx, by[3]), A::mul(sxy, bx[3])) / det;
-      st4(dq_out + 2 * i, fx);
-      st4(dq_out + 2 * i + 1, fy);
+      dq_store(dq_out, i, fx, fy);
     }
   }
   __syncthreads();
@@ -275,6 +278,10 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   double2 v;
   asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
+}
+// One 32-byte load split into its two 16-byte halves.
+__device__ __forceinline__ void ld4d(const double* p, double2& lo, double2& hi) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y) : "l"(p));
 }
 __device__ __forceinline__ void st2(double* p, double2 v) {
   asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
@@ -301,13 +308,15 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
   __syncthreads();
   const int h = threadIdx.x & 1;
   const double* qd = reinterpret_cast<const double*>(q) + 2 * h;
-  const double* dd = reinterpret_cast<const double*>(dq_in) + 2 * h;
+  const double* dd = reinterpret_cast<const double*>(dq_in) + 4 * h;  // {qx, qy} of this lane's pair
   const long long n2 = 2ll * g.n;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; !s_skip && t < n2;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(t >> 1);
     const double2 pi = g.xy[i];
-    const double2 qi = ld2(qd + 4 * i), qxi = ld2(dd + 8 * i), qyi = ld2(dd + 8 * i + 4);
+    const double2 qi = ld2(qd + 4 * i);
+    double2 qxi, qyi;
+    ld4d(dd + 8 * i, qxi, qyi);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
     int e0, k;
@@ -326,7 +335,9 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
       const int nb = K > 0 ? nbk[j] : g.nbr[e0 + j];
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const double2 qn = ld2(qd + 4 * nb), qxn = ld2(dd + 8 * nb), qyn = ld2(dd + 8 * nb + 4);
+      const double2 qn = ld2(qd + 4 * nb);
+      double2 qxn, qyn;
+      ld4d(dd + 8 * nb, qxn, qyn);
       sxx = A::add(sxx, A::mul(dx, dx));
       sxy = A::add(sxy, A::mul(dx, dy));
       syy = A::add(syy, A::mul(dy, dy));
@@ -360,9 +371,8 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
         fy.x = (sxx * by0 - sxy * bx0) * r;
         fy.y = (sxx * by1 - sxy * bx1) * r;
       }
-      double* o = reinterpret_cast<double*>(dq_out) + 8 * static_cast<long long>(i) + 2 * h;
-      st2(o, fx);
-      st2(o + 4, fy);
+      double* o = reinterpret_cast<double*>(dq_out) + 8 * static_cast<long long>(i) + 4 * h;
+      st4(reinterpret_cast<D4*>(o), D4{fx.x, fx.y, fy.x, fy.y});
     }
   }
   __syncthreads();
@@ -447,14 +457,18 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
 
     // ---- phase A: one lane per (point, neighbour) pair ----
     const double2 pi = g.xy[ic];
-    const D4 qi = ld4(a.q + ic), qxi = ld4(a.dq + 2 * ic), qyi = ld4(a.dq + 2 * ic + 1);
+    const D4 qi = ld4(a.q + ic);
+    D4 qxi, qyi;
+    dq_load(a.dq, ic, qxi, qyi);
     for (int jb = 0; jb < kwarp; jb += W) {
       const int j = jb + lane;
       const bool act = live && j < k;
       const int nb = act ? g.nbr[e0 + j] : ic;
       const double2 pn = g.xy[nb];
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+      const D4 qn = ld4(a.q + nb);
+      D4 qxn, qyn;
+      dq_load(a.dq, nb, qxn, qyn);
       double ti[4], tn[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -746,14 +760,18 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       if (sd != 0xFFu) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
     }
     const double2 pi = g.xy[ic];
-    const D4 qi = ld4(a.q + ic), qxi = ld4(a.dq + 2 * ic), qyi = ld4(a.dq + 2 * ic + 1);
+    const D4 qi = ld4(a.q + ic);
+    D4 qxi, qyi;
+    dq_load(a.dq, ic, qxi, qyi);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int jb = 0; jb < kwarp; jb += 8) {
       const int j = jb + lane;
       const bool act = live && j < k;
       const int nb = act ? g.nbr[e0 + j] : ic;
       const double2 w = act ? w1[e0 + j] : make_double2(0.0, 0.0);
-      const D4 qn = ld4(a.q + nb), qxn = ld4(a.dq + 2 * nb), qyn = ld4(a.dq + 2 * nb + 1);
+      const D4 qn = ld4(a.q + nb);
+      D4 qxn, qyn;
+      dq_load(a.dq, nb, qxn, qyn);
       flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 + (e0 + j), acc);
     }
     const double r = reduce8(acc, lane);
@@ -878,12 +896,12 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 pn = *reinterpret_cast<const double2*>(f);
       const double2 w = *reinterpret_cast<const double2*>(f + 512);
       const double2 q01 = *reinterpret_cast<const double2*>(f + 2 * 512), q23 = *reinterpret_cast<const double2*>(f + 3 * 512);
-      const double2 x01 = *reinterpret_cast<const double2*>(f + 4 * 512), x23 = *reinterpret_cast<const double2*>(f + 5 * 512);
-      const double2 y01 = *reinterpret_cast<const double2*>(f + 6 * 512), y23 = *reinterpret_cast<const double2*>(f + 7 * 512);
+      const double2 x01 = *reinterpret_cast<const double2*>(f + 4 * 512), y01 = *reinterpret_cast<const double2*>(f + 5 * 512);
+      const double2 x23 = *reinterpret_cast<const double2*>(f + 6 * 512), y23 = *reinterpret_cast<const double2*>(f + 7 * 512);
       const double2 pi = *reinterpret_cast<const double2*>(o);
       const double2 oq01 = *reinterpret_cast<const double2*>(o + 16), oq23 = *reinterpret_cast<const double2*>(o + 32);
-      const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), ox23 = *reinterpret_cast<const double2*>(o + 64);
-      const double2 oy01 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
+      const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), oy01 = *reinterpret_cast<const double2*>(o + 64);
+      const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
       if (cur.live && lane == 0) {
         const unsigned sd = sing[cur.i];
         if (sd != 0xFFu)
