@@ -801,20 +801,22 @@ constexpr int kFluxStageBytes = kFluxStageChunks * 32 * 16 + 4 * 7 * 16;  // + 4
 constexpr int kFluxWarps = 8;                                       // 256 threads
 
 struct StageIdx {  // per lane, one group
-  int i, ic, nb, e;
+  int i, ic, nb, e, sing;
   bool live, act;
 };
 // Raw loads of a group's indices, issued two groups ahead; the predicates are
 // formed only when the group is staged (stage_index), so nothing waits on them.
 struct StageRaw {
-  int i, kind, nbr, e, k;
+  int i, kind, nbr, e, k, sing;
 };
 
-__device__ __forceinline__ StageRaw stage_load(const Geo& g, int grp, int lane, int sub) {
+__device__ __forceinline__ StageRaw stage_load(const Geo& g, const std::uint8_t* sing, int grp, int lane,
+                                               int sub) {
   StageRaw r;
   r.i = grp * 4 + sub;
   const int ic = r.i < g.n ? r.i : g.n - 1;
   r.kind = g.kind[ic];
+  r.sing = lane == 0 ? sing[ic] : 0xFF;  // first singular split direction (k_flux_weights)
   int e0 = 0, k = 0;
   stencil_of(g, ic, e0, k);
   r.e = e0 + lane;
@@ -831,6 +833,7 @@ __device__ __forceinline__ StageIdx stage_index(const Geo& g, const StageRaw& r,
   x.act = x.live && lane < r.k;
   x.e = r.e;
   x.nb = x.act ? r.nbr : x.ic;
+  x.sing = r.sing;
   return x;
 }
 
@@ -877,17 +880,17 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
   const int nwarps = gridDim.x * NW;
   int grp = blockIdx.x * NW + warp;
   if (!s_skip && grp < groups) {
-    StageIdx cur = stage_index(g, stage_load(g, grp, lane, sub), lane);
+    StageIdx cur = stage_index(g, stage_load(g, sing, grp, lane, sub), lane);
     stage_issue(a, w1, cur, stage0, lane32, lane, sub);
     cp_async_commit();
-    StageRaw nxt = stage_load(g, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
+    StageRaw nxt = stage_load(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
     int buf = 0;
     for (; grp < groups; grp += nwarps, buf ^= 1) {
       const bool more = grp + nwarps < groups;
       const StageIdx nx = stage_index(g, nxt, lane);
       if (more) stage_issue(a, w1, nx, stage0 + (buf ^ 1) * kFluxStageBytes, lane32, lane, sub);
       cp_async_commit();
-      const StageRaw nxt2 = stage_load(g, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
+      const StageRaw nxt2 = stage_load(g, sing, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
       cp_async_wait<1>();
       __syncwarp();
       const char* st = stage0 + buf * kFluxStageBytes;
@@ -902,11 +905,8 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 oq01 = *reinterpret_cast<const double2*>(o + 16), oq23 = *reinterpret_cast<const double2*>(o + 32);
       const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), oy01 = *reinterpret_cast<const double2*>(o + 64);
       const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
-      if (cur.live && lane == 0) {
-        const unsigned sd = sing[cur.i];
-        if (sd != 0xFFu)
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[cur.i], gidx(g, cur.i), sd, kSolveSlot), sub_flux(a.ctl));
-      }
+      if (cur.live && lane == 0 && cur.sing != 0xFF)
+        raise_err(a.ctl, err_key(PH_FLUX, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       flux_pair_fast(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
