@@ -1137,7 +1137,8 @@ class Domain {
     ua.mag = mag_out_;
     ua.which = which_.get();
     ua.ctl = ctl_.get();
-    launch_pdl(k_update, (n_ + 255) / 256, 256, 0, st_, ua);
+    // persistent grid: one block-completion record per resident block, not per 256 points
+    launch_pdl(k_update, std::max(1, std::min((n_ + 255) / 256, resident_blocks(k_update, 3))), 256, 0, st_, ua);
   }
   void launch_residue() {
     launch_pdl(k_tree_partial, 1 << d1_, kTreeThreads, 0, st_, static_cast<const double*>(mag_.get()), n_res_, d1_,

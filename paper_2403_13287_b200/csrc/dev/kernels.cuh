@@ -310,8 +310,17 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
   const double* qd = reinterpret_cast<const double*>(q) + 2 * h;
   const double* dd = reinterpret_cast<const double*>(dq_in) + 4 * h;  // {qx, qy} of this lane's pair
   const long long n2 = 2ll * g.n;
-  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; !s_skip && t < n2;
-       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  // K = 8: the next point's neighbour ids are loaded one point ahead
+  int4 na0 = make_int4(0, 0, 0, 0), na1 = na0;
+  if constexpr (K == 8) {
+    if (t < n2) {
+      na0 = ld_i4(g.nbr + 8 * (t >> 1));
+      na1 = ld_i4(g.nbr + 8 * (t >> 1) + 4);
+    }
+  }
+  for (; !s_skip && t < n2; t += stride) {
     const int i = static_cast<int>(t >> 1);
     const double2 pi = g.xy[i];
     const double2 qi = ld2(qd + 4 * i);
@@ -324,9 +333,12 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
     if constexpr (K == 8) {
       e0 = 8 * i;
       k = 8;
-      const int4 a0 = ld_i4(g.nbr + e0), a1 = ld_i4(g.nbr + e0 + 4);
-      nbk[0] = a0.x, nbk[1] = a0.y, nbk[2] = a0.z, nbk[3] = a0.w;
-      nbk[4] = a1.x, nbk[5] = a1.y, nbk[6] = a1.z, nbk[7] = a1.w;
+      nbk[0] = na0.x, nbk[1] = na0.y, nbk[2] = na0.z, nbk[3] = na0.w;
+      nbk[4] = na1.x, nbk[5] = na1.y, nbk[6] = na1.z, nbk[7] = na1.w;
+      if (t + stride < n2) {
+        na0 = ld_i4(g.nbr + 8 * ((t + stride) >> 1));
+        na1 = ld_i4(g.nbr + 8 * ((t + stride) >> 1) + 4);
+      }
     } else {
       stencil_of(g, i, e0, k);
     }
@@ -945,10 +957,9 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   ktimer_begin(a.ctl, KT_UPDATE);
   if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_update(a.ctl));
   __syncthreads();
-  const int ip = blockIdx.x * blockDim.x + threadIdx.x;
   const Geo& g = a.g;
-  if (!s_skip && ip < g.n) {
-    const bool diag = iter_of(a.ctl) == a.ctl->diag_iter;
+  const bool diag = iter_of(a.ctl) == a.ctl->diag_iter;
+  for (int ip = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && ip < g.n; ip += gridDim.x * blockDim.x) {
     if (g.kind[ip] == KIND_OUTER) {
       st4(a.q_next + ip, ld4(a.q + ip));
       a.mag[gidx(g, ip)] = 0.0;
