@@ -478,11 +478,12 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
 
 // Resets this domain's timers, points it at the run's shared word and (for
 // the domain that owns it) resets that word.
-__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, int spi) {
+__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, int spi, int upd_blocks) {
   ctl->sh = sh;
   ctl->diag_iter = diag_iter;
   ctl->spi = spi;
-  ctl->it = 0;
+  ctl->upd_blocks = upd_blocks > 0 ? upd_blocks : 1;
+  ctl->upd_done = 0;
   ctl->err_stage = kNoErr;
   ctl->err_key = kNoErr;
   if (own_shared) {
@@ -784,7 +785,7 @@ class Domain {
     hsh_.alloc(1);
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
     ck(cudaGetLastError(), "k_min_dist");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0, update_blocks());
     ck(cudaStreamSynchronize(st_), "geometry upload");
   }
 
@@ -1012,7 +1013,8 @@ class Domain {
     ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(res_.get(), 0, n * sizeof(D4), st_), "zero res");
     ck(cudaMemsetAsync(dt_.get(), 0, n * sizeof(double), st_), "zero dt");
-    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1, (order == 2 ? inner : 0) + 4);
+    k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1, (order == 2 ? inner : 0) + 4,
+                                 update_blocks());
     a_ = 0;
     b_ = 0;
     done_ = 0;
@@ -1035,6 +1037,12 @@ class Domain {
   }
 
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
+
+  // Grid of k_update (persistent: at most the resident blocks); fixed per
+  // domain, since the iteration index is derived from its completed blocks.
+  int update_blocks() const {
+    return std::max(1, std::min((n_ + 255) / 256, resident_blocks(k_update, 3)));
+  }
 
   void clear_graphs() {
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
@@ -1137,15 +1145,15 @@ class Domain {
     ua.mag = mag_out_;
     ua.which = which_.get();
     ua.ctl = ctl_.get();
-    // persistent grid: one block-completion record per resident block, not per 256 points
-    launch_pdl(k_update, std::max(1, std::min((n_ + 255) / 256, resident_blocks(k_update, 3))), 256, 0, st_, ua);
+    launch_pdl(k_update, update_blocks(), 256, 0, st_, ua);
   }
   void launch_residue() {
     launch_pdl(k_tree_partial, 1 << d1_, kTreeThreads, 0, st_, static_cast<const double*>(mag_.get()), n_res_, d1_,
                pval_.get(), psz_.get(),
                                                       ctl_.get());
     launch_pdl(k_tree_final, 1, 1024, 0, st_, static_cast<const double*>(pval_.get()),
-               static_cast<const long long*>(psz_.get()), d1_, n_res_, hist_.get(), it1_.get(), ctl_.get());
+               static_cast<const long long*>(psz_.get()), d1_, n_res_, hist_.get(), it0_.get(), it1_.get(),
+               ctl_.get());
   }
   // Halo gather of `recs` records per point from the owners' buffers, as
   // part of stage `sub` of the iteration (0: q; 1+s: derivatives of sweep s).
@@ -1401,14 +1409,19 @@ class Domain {
     return out;
   }
   std::vector<KernelTime> kernel_times() const {
-    static const char* names[KT_COUNT] = {"q_variables", "q_derivatives", "flux_residual", "state_update",
-                                          "residue"};
-    std::vector<KernelTime> out;
+    // slot -> reported kernel (the sweeps' slots add up to q_derivatives)
+    static const char* names[] = {"q_variables", "q_derivatives", "flux_residual", "state_update", "residue"};
+    double secs[5] = {0, 0, 0, 0, 0};
+    std::int64_t cnt[5] = {0, 0, 0, 0, 0};
     for (int k = 0; k < KT_COUNT; ++k) {
       const KTimer& t = hctl_.get()->kt[k];
-      if (t.launches == 0) continue;
-      out.push_back({names[k], t.total_ns * 1e-9, static_cast<std::int64_t>(t.launches)});
+      const int r = k == KT_QVAR ? 0 : (k < KT_FLUX ? 1 : (k == KT_FLUX ? 2 : (k == KT_UPDATE ? 3 : 4)));
+      secs[r] += t.total_ns * 1e-9;
+      cnt[r] += static_cast<std::int64_t>(t.launches);
     }
+    std::vector<KernelTime> out;
+    for (int r = 0; r < 5; ++r)
+      if (cnt[r] > 0) out.push_back({names[r], secs[r], cnt[r]});
     return out;
   }
 
@@ -2388,7 +2401,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
   Domain d(view_of(ps, {}), spec.device, spec.gamma, spec.cfl, spec.det_tol, 1);
   d.set_strict(spec.fp_mode == 1);
   d.upload(ps.fields, true);
-  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), d.shared(), 1, -1, 0);
+  k_ctl_init<<<1, 1, 0, d.stream()>>>(d.dctl(), d.shared(), 1, -1, 0, d.update_blocks());
   const Geo g = d.geo();
   const int n = ps.n();
   const int blocks = (n + 255) / 256;
@@ -2453,7 +2466,7 @@ double engine_reduce(const double* v, std::int64_t n, int device) {
   DBuf<Ctl> ctl(1);
   ck(cudaMemcpy(dv.get(), v, n * sizeof(double), cudaMemcpyHostToDevice), "H2D reduce");
   DBuf<Shared> sh(1);
-  k_ctl_init<<<1, 1>>>(ctl.get(), sh.get(), 1, -1, 0);
+  k_ctl_init<<<1, 1>>>(ctl.get(), sh.get(), 1, -1, 0, 1);
   const int d1 = tree_depth(n);
   k_tree_partial<<<1 << d1, kTreeThreads>>>(dv.get(), n, d1, pv.get(), ps.get(), ctl.get());
   k_tree_result<<<1, 1024>>>(pv.get(), ps.get(), d1, out.get());

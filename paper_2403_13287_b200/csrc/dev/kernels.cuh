@@ -49,7 +49,10 @@ struct KTimer {
   unsigned long long total_ns, launches;
 };
 
-enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 2, KT_UPDATE = 3, KT_RESIDUE = 4, KT_COUNT = 5 };
+// Timer slots: one per kernel launch of an iteration (sweep s -> KT_SWEEP + s,
+// the 8th and later sweeps share the last sweep slot).
+enum : int { KT_QVAR = 0, KT_SWEEP = 1, KT_FLUX = 9, KT_UPDATE = 10, KT_RESIDUE = 11, KT_COUNT = 12 };
+__host__ __device__ constexpr int kt_sweep(int s) { return KT_SWEEP + (s < 7 ? s : 7); }
 
 // Failures are ordered by STAGE first: stage = iteration * spi + sub, with
 // sub 0 = q_variables, 1+s = derivative sweep s, then flux, update, residue
@@ -73,10 +76,13 @@ struct Ctl {
   Shared* sh;
   int diag_iter;  // iteration whose res/dt are kept for copy-back (this domain)
   int spi;        // stages per iteration
-  int it;         // 0-based iteration this domain's stream is in: advanced by
-                  // the last block of every k_update, so each kernel of an
-                  // iteration sees that iteration's index (failed or not)
-  int pad_;
+  int upd_blocks; // grid size of this domain's k_update
+  // Blocks of k_update completed on this domain's stream.  The iteration a
+  // kernel belongs to is upd_done / upd_blocks (failed or not): every block
+  // of k_update adds one at its end, so k_update's own blocks still see their
+  // iteration (fewer than upd_blocks of them have finished) and every later
+  // kernel sees the next one.
+  unsigned long long upd_done;
   unsigned long long err_stage;  // this domain's failing stage (kNoErr = none)
   unsigned long long err_key;    // min key at that stage
   KTimer kt[KT_COUNT];
@@ -123,7 +129,8 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 
 // The residue kernels run after k_update advanced `it`, hence `back`.
 __device__ __forceinline__ int iter_of(const Ctl* ctl, int back = 0) {
-  return *reinterpret_cast<const volatile int*>(&ctl->it) - back;
+  const unsigned long long done = *reinterpret_cast<const volatile unsigned long long*>(&ctl->upd_done);
+  return static_cast<int>(done / static_cast<unsigned>(ctl->upd_blocks)) - back;
 }
 __device__ __forceinline__ unsigned long long stage_of(const Ctl* ctl, int sub, int back = 0) {
   return static_cast<unsigned long long>(iter_of(ctl, back)) * static_cast<unsigned>(ctl->spi) +
@@ -148,28 +155,32 @@ __device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int 
   atomicMin(&ctl->sh->err_stage, st);
 }
 
-// ---- per-kernel device timing (globaltimer; one record per kernel class) ----
+// ---- per-kernel device timing (globaltimer) ----
+// Each launch marks its slot with fire-and-forget atomics: first block start
+// (min) and last block end (max).  k_tree_final, the iteration's last kernel,
+// folds the slots into totals and resets them (ktimer_fold) — no fences or
+// completion counters in the kernels' tails.
 __device__ __forceinline__ void ktimer_begin(Ctl* ctl, int k) {
   if (threadIdx.x == 0) atomicMin(&ctl->kt[k].t0, globaltimer());
 }
 // Call after a __syncthreads() that every thread of the block reaches.
-__device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* iter_t0,
-                                           bool advance = false) {
-  if (threadIdx.x == 0) {
-    atomicMax(&ctl->kt[k].t1, globaltimer());
-    __threadfence();
-    const unsigned nblocks = gridDim.x * gridDim.y;
-    if (atomicAdd(&ctl->kt[k].done, 1u) == nblocks - 1) {
-      __threadfence();
-      const unsigned long long t0 = atomicExch(&ctl->kt[k].t0, ~0ull);
-      const unsigned long long t1 = atomicExch(&ctl->kt[k].t1, 0ull);
-      ctl->kt[k].done = 0;
-      ctl->kt[k].total_ns += t1 - t0;
-      ctl->kt[k].launches += 1;
-      if (iter_t0) iter_t0[ctl->it] = t0;
-      if (advance) ctl->it += 1;
-    }
+__device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* = nullptr) {
+  if (threadIdx.x == 0) atomicMax(&ctl->kt[k].t1, globaltimer());
+}
+// Folds every marked slot (single thread); returns the earliest start of the
+// iteration's kernels (slots other than q_variables).
+__device__ __forceinline__ unsigned long long ktimer_fold(Ctl* ctl) {
+  unsigned long long first = ~0ull;
+  for (int k = 0; k < KT_COUNT; ++k) {
+    KTimer& t = ctl->kt[k];
+    if (t.t1 == 0 || t.t0 == ~0ull) continue;
+    if (k != KT_QVAR && t.t0 < first) first = t.t0;
+    t.total_ns += t.t1 > t.t0 ? t.t1 - t.t0 : 0;
+    t.launches += 1;
+    t.t0 = ~0ull;
+    t.t1 = 0;
   }
+  return first;
 }
 
 // ---------------------------------------------------------------------------
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
   pdl_enter();
   using A = Ar<S>;
   __shared__ int s_skip;
-  ktimer_begin(ctl, KT_SWEEP);
+  ktimer_begin(ctl, kt_sweep(sweep));
   if (threadIdx.x == 0) s_skip = skip_stage(ctl, 1 + sweep);
   __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && i < g.n; i += gridDim.x * blockDim.x) {
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
     }
   }
   __syncthreads();
-  ktimer_end(ctl, KT_SWEEP, iter_t0);
+  ktimer_end(ctl, kt_sweep(sweep));
 }
 
 // Two lanes per point: lane h owns components {2h, 2h+1} of q, qx, qy and
@@ -303,7 +314,7 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
   pdl_enter();
   using A = Ar<S>;
   __shared__ int s_skip;
-  ktimer_begin(ctl, KT_SWEEP);
+  ktimer_begin(ctl, kt_sweep(sweep));
   if (threadIdx.x == 0) s_skip = skip_stage(ctl, 1 + sweep);
   __syncthreads();
   const int h = threadIdx.x & 1;
@@ -388,7 +399,7 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
     }
   }
   __syncthreads();
-  ktimer_end(ctl, KT_SWEEP, iter_t0);
+  ktimer_end(ctl, kt_sweep(sweep));
 }
 
 // ---------------------------------------------------------------------------
@@ -588,7 +599,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
     __syncthreads();  // terms/records are reused by the next group
   }
   __syncthreads();
-  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+  ktimer_end(a.ctl, KT_FLUX);
 }
 
 // ---------------------------------------------------------------------------
@@ -790,7 +801,7 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
     if (live) store_res8(a.res, i, r, lane);
   }
   __syncthreads();
-  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+  ktimer_end(a.ctl, KT_FLUX);
 }
 
 // ---- staged variant (stencils of at most 8): each warp copies the NEXT group's
@@ -933,7 +944,7 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
     cp_async_wait<0>();
   }
   __syncthreads();
-  ktimer_end(a.ctl, KT_FLUX, a.iter_t0);
+  ktimer_end(a.ctl, KT_FLUX);
 }
 
 // Local time step + forward-Euler update + wall slip + next q-variables +
@@ -1006,7 +1017,8 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
     }
   }
   __syncthreads();
-  ktimer_end(a.ctl, KT_UPDATE, nullptr, true);
+  ktimer_end(a.ctl, KT_UPDATE);
+  if (threadIdx.x == 0) atomicAdd(&a.ctl->upd_done, 1ull);  // read by later kernels (stream order)
 }
 
 // ---------------------------------------------------------------------------
@@ -1178,14 +1190,17 @@ __global__ void __launch_bounds__(kTreeThreads)
 // the history entry (runtime.cpp:251-269); non-finite -> positivity error.
 __global__ void __launch_bounds__(1024)
     k_tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
-                 double* history, unsigned long long* iter_t1, Ctl* ctl) {
+                 double* history, unsigned long long* iter_t0, unsigned long long* iter_t1, Ctl* ctl) {
   pdl_enter();
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
   __shared__ int s_skip;
   if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl), 1);
   __syncthreads();
-  if (s_skip) return;
+  if (s_skip) {
+    if (threadIdx.x == 0) ktimer_fold(ctl);
+    return;
+  }
   const int m = 1 << d1;
   for (int t = threadIdx.x; t < m; t += blockDim.x) {
     sv[0][t] = part_val[t];
@@ -1203,6 +1218,9 @@ __global__ void __launch_bounds__(1024)
       if (iter_t1) iter_t1[it] = globaltimer();
       ctl->sh->iter = it + 1;  // iterations completed (residue recorded)
     }
+    atomicMax(&ctl->kt[KT_RESIDUE].t1, globaltimer());
+    const unsigned long long t0 = ktimer_fold(ctl);
+    if (iter_t0 && !(res != res) && isfinite(res)) iter_t0[it] = t0;
   }
 }
 

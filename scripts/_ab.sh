@@ -1,8 +1,10 @@
-for v in "LSKUM_SWEEP_BLOCK=256" "LSKUM_SWEEP_BLOCK=128"; do
-  echo "== $v"; env $v PROBE_ORDERS=2 timeout 300 python scripts/probe_perf.py 400 3163 2>&1 | python -c "
+export PROBE_NACA=520x308,4000x2500 PROBE_ORDERS=2
+echo "== with ktimer"; python scripts/probe_perf.py 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
-  try: d=json.loads(l)
-  except Exception: print(l.strip()); continue
-  k={a:b for a,b,c in d['kernels']}; print(d['n'], round(d['ms_per_it'],4), 'sweep', k.get('q_derivatives'), 'flux', k['flux_residual'])"
-done
+  d=json.loads(l); print(d['n'], round(d['ms_per_it'],4))"
+cp paper_2403_13287_b200/nokt/liblskum_b200.so paper_2403_13287_b200/liblskum_b200.so
+echo "== no ktimer"; python scripts/probe_perf.py 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+  d=json.loads(l); print(d['n'], round(d['ms_per_it'],4))"
