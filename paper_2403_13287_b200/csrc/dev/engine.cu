@@ -18,6 +18,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -85,24 +86,71 @@ class DBuf {
   cudaStream_t st_ = nullptr;
 };
 
+// Small pinned host blocks (control words, poll slots) are recycled through a
+// process-wide free list: cudaHostAlloc costs about a millisecond per call,
+// which a fresh domain would otherwise pay several times.
+class PinnedPool {
+ public:
+  static constexpr std::size_t kBlock = 4096;
+  static void* take() {
+    {
+      std::lock_guard<std::mutex> g(mu());
+      auto& f = free_list();
+      if (!f.empty()) {
+        void* p = f.back();
+        f.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    ck(cudaHostAlloc(&p, kBlock, 0), "cudaHostAlloc");
+    return p;
+  }
+  static void give(void* p) {
+    std::lock_guard<std::mutex> g(mu());
+    free_list().push_back(p);
+  }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<void*>& free_list() {
+    static std::vector<void*> f;
+    return f;
+  }
+};
+
 template <class T>
 class HBuf {  // pinned host staging
  public:
   HBuf() = default;
   HBuf(const HBuf&) = delete;
   HBuf& operator=(const HBuf&) = delete;
-  ~HBuf() {
-    if (p_) cudaFreeHost(p_);
-  }
+  ~HBuf() { release(); }
   void alloc(std::size_t count) {
-    if (p_) cudaFreeHost(p_);
-    p_ = nullptr;
-    if (count) ck(cudaHostAlloc(reinterpret_cast<void**>(&p_), count * sizeof(T), 0), "cudaHostAlloc");
+    release();
+    if (!count) return;
+    if (count * sizeof(T) <= PinnedPool::kBlock) {
+      p_ = static_cast<T*>(PinnedPool::take());
+      pooled_ = true;
+    } else {
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&p_), count * sizeof(T), 0), "cudaHostAlloc");
+    }
   }
   T* get() const { return p_; }
 
  private:
+  void release() {
+    if (!p_) return;
+    if (pooled_) PinnedPool::give(p_);
+    else cudaFreeHost(p_);
+    p_ = nullptr;
+    pooled_ = false;
+  }
   T* p_ = nullptr;
+  bool pooled_ = false;
 };
 
 // Grow-only pinned host staging, one per host thread (runs on different
@@ -728,18 +776,27 @@ class Domain {
     int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * nl + 15) & ~std::size_t{15}));
     int* hnbr = hoff + n + 1;
     int* hgid = hnbr + nnz;
-    for (std::size_t i = 0; i < nl; ++i) {
-      hxy[i] = make_double2(gv.x[i], gv.y[i]);
-      hnrm[i] = make_double2(gv.nx[i], gv.ny[i]);
-      hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
-      hpart[i] = gv.part ? gv.part[i] : 0;
-    }
-    for (std::size_t i = 0; i <= n; ++i) hoff[i] = static_cast<int>(gv.off[i]);
-    if (nnz) std::memcpy(hnbr, gv.nbr, b_nbr);
+    parallel_slices(static_cast<std::int64_t>(nl), [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t i = lo; i < hi; ++i) {
+        hxy[i] = make_double2(gv.x[i], gv.y[i]);
+        hnrm[i] = make_double2(gv.nx[i], gv.ny[i]);
+        hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
+        hpart[i] = gv.part ? gv.part[i] : 0;
+      }
+    }, 1 << 15);
+    parallel_slices(static_cast<std::int64_t>(n) + 1, [&](std::int64_t lo, std::int64_t hi) {
+      for (std::int64_t i = lo; i < hi; ++i) hoff[i] = static_cast<int>(gv.off[i]);
+    }, 1 << 16);
+    if (nnz)
+      parallel_slices(static_cast<std::int64_t>(b_nbr), [&](std::int64_t lo, std::int64_t hi) {
+        std::memcpy(reinterpret_cast<char*>(hnbr) + lo, reinterpret_cast<const char*>(gv.nbr) + lo,
+                    static_cast<std::size_t>(hi - lo));
+      }, 1 << 20);
     if (gv.gid) {
       std::memcpy(hgid, gv.gid, b_gid);
       gid_host_.assign(gv.gid, gv.gid + nl);
     }
+    trace("domain: staged");
     xy_.alloc(nl, st_);
     nrm_.alloc(nl, st_);
     kind_.alloc(nl, st_);
@@ -783,6 +840,7 @@ class Domain {
     hpoll_.alloc(kPolls);
     hctl_.alloc(1);
     hsh_.alloc(1);
+    trace("domain: allocated, copies queued");
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
     ck(cudaGetLastError(), "k_min_dist");
     k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0, update_blocks());
