@@ -1007,15 +1007,29 @@ class Domain {
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
           n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
-      // through pinned staging (full-rate D2H), then a parallel host copy
+      // through pinned staging (full-rate D2H) in chunks; host threads copy
+      // each chunk into the store as soon as its transfer completes
       const std::size_t bytes = 21 * n * sizeof(double);
       char* h = static_cast<char*>(t_staging.get(bytes));
-      ck(cudaMemcpyAsync(h, packed.get(), bytes, cudaMemcpyDeviceToHost, st_), "D2H fields");
-      ck(cudaStreamSynchronize(st_), "download");
       char* dst = reinterpret_cast<char*>(f.raw());
-      parallel_slices(static_cast<std::int64_t>(bytes), [&](std::int64_t lo, std::int64_t hi) {
-        std::memcpy(dst + lo, h + lo, static_cast<std::size_t>(hi - lo));
-      }, 1 << 21);
+      const int chunks = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(16, bytes >> 21)));
+      std::vector<cudaEvent_t> done(static_cast<std::size_t>(chunks));
+      for (int c = 0; c < chunks; ++c) {
+        const std::size_t lo = bytes * c / chunks, hi = bytes * (c + 1) / chunks;
+        ck(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaMemcpyAsync(h + lo, packed.get() + lo / sizeof(double), hi - lo, cudaMemcpyDeviceToHost, st_),
+           "D2H fields");
+        ck(cudaEventRecord(done[c], st_), "cudaEventRecord");
+      }
+      parallel_slices(chunks, [&](std::int64_t a, std::int64_t b) {
+        for (std::int64_t c = a; c < b; ++c) {
+          cudaEventSynchronize(done[c]);
+          const std::size_t lo = bytes * c / chunks, hi = bytes * (c + 1) / chunks;
+          std::memcpy(dst + lo, h + lo, hi - lo);
+        }
+      }, 1);
+      ck(cudaStreamSynchronize(st_), "download");
+      for (cudaEvent_t e : done) cudaEventDestroy(e);
       return;
     }
     std::vector<D4> h(6 * n);
