@@ -284,9 +284,15 @@ def rooflines(L, counts, n, n_flux, k, order, inner, step_ms, sweep_ms, flux_ms,
     hbm, hbm_kind = hbm_peak()
     sweep_gbs = sweep_bytes(k) * (n / domains) / (sweep_ms * 1e-3) / 1e9 if sweep_ms else None
     iter_gbs = iteration_bytes(k, order, inner) * n / (step_ms * 1e-3) / 1e9 / domains
+    inst = counts.get("flux_fp64_thread_inst_per_point") or {}
+    inst_pt = sum(inst.get(k, 0.0) for k in ("dfma", "dadd", "dmul"))
+    pipe = inst_pt * n_flux_dom / (flux_ms * 1e-3) / (fp64_peak * 1e12 / 2) if (inst_pt and flux_ms > 0) else None
     flux = {"bound": "fp64", "kernel": "k_flux_ws (fast flux residual: split-stencil weights, cp.async staged)",
             "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak if achieved else None,
+            "fp64_pipe_frac": pipe,
+            "fp64_pipe_note": "FP64 instructions (DFMA+DADD+DMUL, ncu) per second over the DFMA instruction peak "
+                              "(peak TFLOP/s / 2): DADD/DMUL occupy a full pipe slot for one flop",
             "traffic": traffic * n_flux_dom if traffic else None,
             "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
             "peak_source": "DFMA microbenchmark on this GPU (lskum_b200_fp64_peak)",
