@@ -440,11 +440,11 @@ void flux_w_launch(const FluxArgs& a, int kmax, const double2* w1, const double2
 }
 
 // Depth of the per-block nodes of the residue tree: at most ~8 values per
-// thread (256 threads per block), at most 1024 blocks (one block folds the
-// partials).
+// thread (256 threads per block), at most 8192 blocks (the final block folds
+// up to 8 partials per thread, then 10 levels in shared memory).
 int tree_depth(long long n) {
   int d = 0;
-  while (d < 10 && (n >> (d + 8)) > 8) ++d;
+  while (d < 13 && (n >> (d + 8)) > 8) ++d;
   return d;
 }
 
@@ -827,8 +827,8 @@ class Domain {
     which_.alloc(n, st_);
     mag_.alloc(n, st_);
     mag_out_ = mag_.get();
-    pval_.alloc(1024, st_);
-    psz_.alloc(1024, st_);
+    pval_.alloc(8192, st_);
+    psz_.alloc(8192, st_);
     ctl_.alloc(1, st_);
     sh_.alloc(1, shared_st);
     shared_ = sh_.get();
@@ -1009,23 +1009,24 @@ class Domain {
       ck(cudaGetLastError(), "k_pack_fields");
       // through pinned staging (full-rate D2H) in chunks; host threads copy
       // each chunk into the store as soon as its transfer completes
-      const std::size_t bytes = 21 * n * sizeof(double);
-      char* h = static_cast<char*>(t_staging.get(bytes));
-      char* dst = reinterpret_cast<char*>(f.raw());
+      const std::size_t count = 21 * n, bytes = count * sizeof(double);
+      double* h = static_cast<double*>(t_staging.get(bytes));
+      double* dst = f.raw();
       const int chunks = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(16, bytes >> 21)));
       std::vector<cudaEvent_t> done(static_cast<std::size_t>(chunks));
+      auto lo_of = [&](std::int64_t c) { return count * static_cast<std::size_t>(c) / static_cast<std::size_t>(chunks); };
       for (int c = 0; c < chunks; ++c) {
-        const std::size_t lo = bytes * c / chunks, hi = bytes * (c + 1) / chunks;
+        const std::size_t lo = lo_of(c), hi = lo_of(c + 1);
         ck(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaMemcpyAsync(h + lo, packed.get() + lo / sizeof(double), hi - lo, cudaMemcpyDeviceToHost, st_),
+        ck(cudaMemcpyAsync(h + lo, packed.get() + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, st_),
            "D2H fields");
         ck(cudaEventRecord(done[c], st_), "cudaEventRecord");
       }
       parallel_slices(chunks, [&](std::int64_t a, std::int64_t b) {
         for (std::int64_t c = a; c < b; ++c) {
           cudaEventSynchronize(done[c]);
-          const std::size_t lo = bytes * c / chunks, hi = bytes * (c + 1) / chunks;
-          std::memcpy(dst + lo, h + lo, hi - lo);
+          const std::size_t lo = lo_of(c), hi = lo_of(c + 1);
+          std::memcpy(dst + lo, h + lo, (hi - lo) * sizeof(double));
         }
       }, 1);
       ck(cudaStreamSynchronize(st_), "download");
@@ -2533,8 +2534,8 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
 double engine_reduce(const double* v, std::int64_t n, int device) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   if (n <= 0) return 0.0;
-  DBuf<double> dv(static_cast<std::size_t>(n)), pv(1024), out(1);
-  DBuf<long long> ps(1024);
+  DBuf<double> dv(static_cast<std::size_t>(n)), pv(8192), out(1);
+  DBuf<long long> ps(8192);
   DBuf<Ctl> ctl(1);
   ck(cudaMemcpy(dv.get(), v, n * sizeof(double), cudaMemcpyHostToDevice), "H2D reduce");
   DBuf<Shared> sh(1);

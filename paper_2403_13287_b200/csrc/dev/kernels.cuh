@@ -1121,6 +1121,35 @@ __device__ double tree_sum(const double* v, long long lo, long long hi) {
   return X::add(tree_sum(v, lo, mid), tree_sum(v, mid, hi));
 }
 
+// One node of the midpoint tree from its two children (sizes decide how
+// empty and single-element children combine, exactly as the recursion does).
+__device__ __forceinline__ void tree_pair(double vl, long long sl, double vr, long long sr, double& v,
+                                          long long& s) {
+  s = sl + sr;
+  v = s <= 0 ? 0.0 : (s == 1 ? (sr == 1 ? vr : vl) : X::add(vl, vr));
+}
+
+// Loads the 2^d1 partials as 2^min(d1, 10) subtree values: with d1 > 10 each
+// thread folds its 2^(d1-10) consecutive partials (one subtree) serially.
+__device__ __forceinline__ int tree_load_partials(const double* part_val, const long long* part_sz, int d1,
+                                                  double* sv, long long* ss) {
+  const int lv = d1 > 10 ? 10 : d1;
+  const int per = 1 << (d1 - lv);
+  for (int t = threadIdx.x; t < (1 << lv); t += blockDim.x) {
+    double v[8];
+    long long s[8];
+    for (int k = 0; k < per; ++k) {
+      v[k] = part_val[t * per + k];
+      s[k] = part_sz[t * per + k];
+    }
+    for (int w = per; w > 1; w >>= 1)
+      for (int k = 0; k < w / 2; ++k) tree_pair(v[2 * k], s[2 * k], v[2 * k + 1], s[2 * k + 1], v[k], s[k]);
+    sv[t] = v[0];
+    ss[t] = s[0];
+  }
+  return lv;
+}
+
 // Combines 2^levels children (val/sz in ping) up `levels` levels; T threads.
 template <int T>
 __device__ void tree_combine(double* val, long long* sz, double* val2, long long* sz2,
@@ -1201,13 +1230,9 @@ __global__ void __launch_bounds__(1024)
     if (threadIdx.x == 0) ktimer_fold(ctl);
     return;
   }
-  const int m = 1 << d1;
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    sv[0][t] = part_val[t];
-    ss[0][t] = part_sz[t];
-  }
+  const int lv = tree_load_partials(part_val, part_sz, d1, sv[0], ss[0]);
   __syncthreads();
-  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
+  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], lv);
   if (threadIdx.x == 0) {
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
     const int it = iter_of(ctl, 1);
@@ -1230,13 +1255,9 @@ __global__ void k_tree_result(const double* part_val, const long long* part_sz, 
                               double* out) {
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
-  const int m = 1 << d1;
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    sv[0][t] = part_val[t];
-    ss[0][t] = part_sz[t];
-  }
+  const int lv = tree_load_partials(part_val, part_sz, d1, sv[0], ss[0]);
   __syncthreads();
-  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], d1);
+  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], lv);
   if (threadIdx.x == 0) *out = sv[0][0];
 }
 

@@ -1,9 +1,7 @@
 export PROBE_NACA=520x308,4000x2500 PROBE_ORDERS=2
-for v in "LSKUM_FLUX_WS=4x4" "LSKUM_FLUX_WS=4x5" "LSKUM_FLUX_WS=4x6" "LSKUM_FLUX_WS=8x3"; do
-  echo "== $v"; env $v timeout 300 python scripts/probe_perf.py 2>&1 | python -c "
+python scripts/probe_perf.py 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
   try: d=json.loads(l)
   except Exception: print(l.strip()); continue
   k={a:b for a,b,c in d['kernels']}; print(d['n'], round(d['ms_per_it'],4), 'sweep', k.get('q_derivatives'), 'flux', k['flux_residual'])"
-done
