@@ -1230,11 +1230,12 @@ class Domain {
   }
   // Halo gather of `recs` records per point from the owners' buffers, as
   // part of stage `sub` of the iteration (0: q; 1+s: derivatives of sweep s).
-  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src, int sub) {
+  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src, int sub,
+                   bool skip_first = false) {
     const int nh = n_loc_ - n_;
     if (nh <= 0) return;
     k_halo<<<std::min((nh * recs + 255) / 256, 4096), 256, 0, st_>>>(dst, recs, n_, nh, hdom, hidx, src,
-                                                                       ctl_.get(), sub);
+                                                                       ctl_.get(), sub, skip_first ? 1 : 0);
   }
 
   // One iteration starting at parity (a, b); `timed` brackets the first sweep
@@ -2010,7 +2011,15 @@ struct WaitList {
   int n;
 };
 
-__global__ void k_signal(unsigned long long* flag, unsigned long long v) {
+// Progress counters: values are derived on the device from this domain's
+// iteration index t (iter_of): value = t * mult + add, so one captured graph
+// serves every iteration.
+__device__ __forceinline__ unsigned long long iter_value(const Ctl* ctl, long long mult, long long add) {
+  return static_cast<unsigned long long>(static_cast<long long>(iter_of(ctl)) * mult + add);
+}
+
+__global__ void k_signal(unsigned long long* flag, const Ctl* ctl, long long mult, long long add) {
+  const unsigned long long v = iter_value(ctl, mult, add);
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
 }
@@ -2022,9 +2031,13 @@ __global__ void k_signal(unsigned long long* flag, unsigned long long v) {
 // PH_STALL (stage 0) so the host raises instead of hanging the device.
 constexpr unsigned long long kStallNs = 30ull * 1000 * 1000 * 1000;
 
-__global__ void k_wait(WaitList w, unsigned long long target, Ctl* ctl, unsigned long long guard) {
+// guard stage = t * spi + sub (sub may be negative: a stage of the previous
+// iteration index, for waits placed after k_update).
+__global__ void k_wait(WaitList w, long long mult, long long add, Ctl* ctl, int sub) {
   const int m = threadIdx.x;
   if (m >= w.n) return;
+  const unsigned long long target = iter_value(ctl, mult, add);
+  const unsigned long long guard = iter_value(ctl, ctl->spi, sub);
   const unsigned long long t0 = globaltimer();
   for (;;) {
     unsigned long long v;
@@ -2112,6 +2125,7 @@ class RankRun {
 
   ~RankRun() {
     if (dom_) cudaStreamSynchronize(dom_->stream());
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     for (void* p : opened_) cudaIpcCloseMemHandle(p);
     cudaEventDestroy(t0_);
     cudaEventDestroy(t1_);
@@ -2152,21 +2166,36 @@ class RankRun {
     dom_->refresh_ctl();
   }
 
+  // Runs up to n iterations in captured graphs of `chunk` iterations (flag
+  // targets are derived on the device, so graphs are reused across chunks);
+  // stops early on a device error.  Returns the CUDA-event ms of the work.
   double iterate(int n) {
     Domain& d = *dom_;
     ck(cudaSetDevice(device_), "cudaSetDevice");
     d.set_diag(t_ + n - 1);
+    const int chunk = std::max(1, spec_.chunk);
+    {
+      int t = t_, left = n;
+      while (left > 0) {
+        const int c = std::min(chunk, left);
+        graph_for(t, c);
+        t += c;
+        left -= c;
+      }
+    }
     ck(cudaEventRecord(t0_, d.stream()), "EventRecord");
     int issued = 0, waited = 0;
     bool failed = false;
     const int end = t_ + n;
-    for (; t_ < end && !failed; ++t_) {
-      enqueue(t_, t_ == end - 1);
+    while (t_ < end && !failed) {
+      const int c = std::min(chunk, end - t_);
+      ck(cudaGraphLaunch(graph_for(t_, c), d.stream()), "GraphLaunch");
+      t_ += c;
       failed = d.poll(issued, waited);
     }
-    // Every rank returns only after the root's residue of the last enqueued
-    // iteration, so all of them observe the same error word.
-    if (rank_ != 0) wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t_), t_, 0);
+    // Every rank returns only after the root's residue of its last iteration,
+    // so all of them observe the same error word.
+    if (rank_ != 0) wait_for(std::vector<int>{0}, FL_RES, 1, 0, 0);
     ck(cudaEventRecord(t1_, d.stream()), "EventRecord");
     ck(cudaStreamSynchronize(d.stream()), "rank iterate");
     float ms = 0.0f;
@@ -2229,62 +2258,82 @@ class RankRun {
     opened_.push_back(p);
     return p;
   }
-  void signal(int slot, unsigned long long v) {
-    k_signal<<<1, 1, 0, dom_->stream()>>>(flags_.get() + slot, v);
+  void signal(int slot, long long mult, long long add) {
+    k_signal<<<1, 1, 0, dom_->stream()>>>(flags_.get() + slot, dom_->dctl(), mult, add);
     ++launches_;
   }
-  // Waits for the ranks' `slot` counters to reach v, guarding stage `sub` of
-  // iteration t (see k_wait).
-  void wait_for(const std::vector<int>& ranks, int slot, unsigned long long v, int t, int sub) {
+  // Waits until the ranks' `slot` counters reach t * mult + add (t: this
+  // domain's iteration index), guarding stage t * spi + sub (see k_wait).
+  void wait_for(const std::vector<int>& ranks, int slot, long long mult, long long add, int sub) {
     if (ranks.empty()) return;
     WaitList w{};
     w.n = static_cast<int>(ranks.size());
     for (int m = 0; m < w.n; ++m) w.ptr[m] = flag_[ranks[m]] + slot;
-    const unsigned long long guard = static_cast<unsigned long long>(t) * spi_ + static_cast<unsigned>(sub);
-    k_wait<<<1, 32, 0, dom_->stream()>>>(w, v, dom_->dctl(), guard);
+    k_wait<<<1, 32, 0, dom_->stream()>>>(w, mult, add, dom_->dctl(), sub);
     ++launches_;
   }
 
-  void enqueue(int t, bool timed) {
+  // Graph of c iterations starting at iteration t (parities from t).
+  cudaGraphExec_t graph_for(int t, int c) {
+    const int a = t & 1, b = spec_.order == 2 ? (t * spec_.inner) & 1 : 0;
+    const auto key = std::make_tuple(a, b, c);
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) return it->second;
+    cudaStream_t st = dom_->stream();
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+    for (int k = 0; k < c; ++k) enqueue_iteration(t + k, k == c - 1);
+    ck(cudaGetLastError(), "capture launches");
+    ck(cudaStreamEndCapture(st, &graph), "EndCapture");
+    cudaGraphExec_t exec;
+    ck(cudaGraphInstantiate(&exec, graph, 0), "GraphInstantiate");
+    cudaGraphDestroy(graph);
+    graphs_[key] = exec;
+    return exec;
+  }
+
+  // One iteration; only the buffer parities depend on the host-side t (the
+  // counters' targets follow the device iteration index).  Timed: CUDA
+  // events around the first sweep and the flux kernel.
+  void enqueue_iteration(int t, bool timed) {
     Domain& d = *dom_;
     cudaStream_t st = d.stream();
     const int a = t & 1;
     launches_ = 0;
-    if (t > 0) {
-      wait_for(std::vector<int>{0}, FL_RES, static_cast<unsigned long long>(t), t, 0);  // residue(t-1) done
-      wait_for(src_, FL_UPD, static_cast<unsigned long long>(t), t, 0);                  // owners' q(t) ready
-      d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a], 0);
-      ++launches_;
-    }
+    const long long inner = spec_.inner;
+    wait_for(std::vector<int>{0}, FL_RES, 1, 0, 0);  // root's residue of iteration t-1 done
+    wait_for(src_, FL_UPD, 1, 0, 0);                   // owners' q of iteration t ready
+    d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a], 0, true);
+    ++launches_;
     int bfin = 0;
     if (spec_.order == 2) {
       for (int s = 0; s < spec_.inner; ++s) {
-        const int k = t * spec_.inner + s, b = k & 1;
-        if (s >= 2) wait_for(readers_, FL_DQH, static_cast<unsigned long long>(k - 1), t, 1 + s);  // readers gathered k-2
-        if (timed && s == 0) ck(cudaEventRecord(kev_[0], st), "EventRecord");
+        const int b = (t * spec_.inner + s) & 1;
+        if (s >= 2) wait_for(readers_, FL_DQH, inner, s - 1, 1 + s);  // readers gathered sweep k-2
+        if (timed && s == 0) d.record_ext(kev_[0]);
         d.launch_sweep(a, b, s);
         launches_ += 2;  // sweep + dq halo
-        if (timed && s == 0) ck(cudaEventRecord(kev_[1], st), "EventRecord");
-        signal(FL_SW, static_cast<unsigned long long>(k + 1));
-        wait_for(src_, FL_SW, static_cast<unsigned long long>(k + 1), t, 1 + s);
+        if (timed && s == 0) d.record_ext(kev_[1]);
+        signal(FL_SW, inner, s + 1);                  // = k + 1, k = t * inner + s
+        wait_for(src_, FL_SW, inner, s + 1, 1 + s);
         d.launch_halo(d.dq_buf(b ^ 1), 2, hdom_.get(), hidx_.get(), dqp_[b ^ 1], 1 + s);
-        signal(FL_DQH, static_cast<unsigned long long>(k + 1));
+        signal(FL_DQH, inner, s + 1);
       }
       bfin = ((t + 1) * spec_.inner) & 1;
     }
-    if (timed) ck(cudaEventRecord(kev_[2], st), "EventRecord");
+    if (timed) d.record_ext(kev_[2]);
     d.launch_flux(a, bfin, spec_.order != 2);
-    if (timed) ck(cudaEventRecord(kev_[3], st), "EventRecord");
-    d.launch_update(a);
-    launches_ += 2;  // flux + update
-    signal(FL_UPD, static_cast<unsigned long long>(t + 1));
+    if (timed) d.record_ext(kev_[3]);
+    d.launch_update(a);  // the device iteration index is t + 1 from here on
+    launches_ += 2;      // flux + update
+    signal(FL_UPD, 1, 0);
     if (rank_ == 0) {
       std::vector<int> all;
       for (int o = 1; o < world_; ++o) all.push_back(o);
-      wait_for(all, FL_UPD, static_cast<unsigned long long>(t + 1), t, spi_ - 1);
+      wait_for(all, FL_UPD, 1, 0, -1);  // guard: the residue stage of iteration t
       d.launch_residue();
       launches_ += 2;  // tree partial + final
-      signal(FL_RES, static_cast<unsigned long long>(t + 1));
+      signal(FL_RES, 1, 0);
     }
     ck(cudaGetLastError(), "rank launches");
   }
@@ -2303,6 +2352,7 @@ class RankRun {
   RankBlob blob_{};
   cudaEvent_t t0_ = nullptr, t1_ = nullptr, kev_[4] = {};
   int t_ = 0, launches_ = 0, spi_ = 4;
+  std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs_;
 };
 
 RankRun* rank_open(PointSet& ps, const EngineSpec& spec, int rank, int world, int device, int capacity) {

@@ -1030,8 +1030,11 @@ struct PeerTab {
   const D4* base[kMaxDomains];
 };
 
+// skip_first: the gather is a no-op in iteration 0 (the q halo then comes from
+// the domain's own first q_variables).
 __global__ void k_halo(D4* dst, int recs, int n_own, int n_halo, const int* hdom, const int* hidx,
-                       PeerTab src, const Ctl* ctl, int sub) {
+                       PeerTab src, const Ctl* ctl, int sub, int skip_first) {
+  if (skip_first && iter_of(ctl) == 0) return;
   if (skip_stage(ctl, sub)) return;  // keep the failing stage's buffers intact
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_halo * recs; t += gridDim.x * blockDim.x) {
     const int h = t / recs, r = t - h * recs;
