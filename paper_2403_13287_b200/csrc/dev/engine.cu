@@ -375,6 +375,16 @@ bool flux_weighted() {
   return v != 0;
 }
 
+// First order, fast mode: split fluxes evaluated once per point
+// (LSKUM_POINT_FLUX=0 disables).
+bool point_flux_enabled() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_POINT_FLUX");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 // Staged variant for stencils of at most 8 (LSKUM_FLUX_STAGE=0 disables it).
 bool flux_staged() {
   static int v = [] {
@@ -1081,6 +1091,10 @@ class Domain {
     strict_ = fp_mode == 1;
     chunk_ = std::max(1, chunk);
     if (!strict_ && flux_weighted()) ensure_weights();
+    if (!strict_ && order == 1 && point_flux_enabled() && !pf_.get()) {  // not inside a graph capture
+      pf_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
+      pfvalid_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
+    }
     const std::size_t n = static_cast<std::size_t>(n_), nl = static_cast<std::size_t>(n_loc_);
     ck(cudaMemsetAsync(dq_[0].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
@@ -1158,16 +1172,18 @@ class Domain {
     const int blocks = (n_ + 255) / 256;
     DBuf<unsigned long long> zc(1, st_);
     ck(cudaMemsetAsync(zc.get(), 0, sizeof(unsigned long long), st_), "memset");
-    k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, nullptr, nullptr, nullptr, zc.get());
+    k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, nullptr, nullptr, nullptr, zc.get(),
+                                                          nullptr);
     unsigned long long zeros = 0;
     ck(cudaMemcpyAsync(&zeros, zc.get(), sizeof zeros, cudaMemcpyDeviceToHost, st_), "D2H zero pairs");
     ck(cudaStreamSynchronize(st_), "weights count");
     const std::size_t nnz = static_cast<std::size_t>(std::max<std::int64_t>(1, nnz_));
     w1_.alloc(nnz, st_);
+    psign_.alloc(nnz, st_);
     if (zeros) w2_.alloc(nnz, st_);
     sing_.alloc(static_cast<std::size_t>(std::max(1, n_)), st_);
     k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, w1_.get(), w2_.get(), sing_.get(),
-                                                          zc.get());
+                                                          zc.get(), psign_.get());
     ck(cudaGetLastError(), "k_flux_weights");
     ck(cudaStreamSynchronize(st_), "weights");
     weights_ = true;
@@ -1203,8 +1219,22 @@ class Domain {
     fa.stride = stride_;
     fa.mask = 0xF;
     fa.first = 1;
-    if (!strict_ && weights_) flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), st_);
-    else flux_launch(W_, strict_, fa, smem_, st_);
+    if (!strict_ && weights_ && order_ == 1 && point_flux_enabled() && pf_.get() && kmax_ <= 8) {
+      // first order: per-point split fluxes (owned and halo points), then the gather
+      launch_pdl(k_point_flux, std::max(1, (n_loc_ + 255) / 256), 256, 0, st_, n_loc_,
+                 static_cast<const D4*>(q_[a].get()), gas_, pf_.get(), pfvalid_.get(),
+                 static_cast<const Ctl*>(ctl_.get()));
+      const int groups = (n_ + 3) / 4;
+      const int blocks = std::max(1, std::min((groups + 7) / 8, resident_blocks(k_flux1<2>, 7)));
+      launch_pdl(k_flux1<2>, blocks, 256, 0, st_, fa, static_cast<const PointFlux*>(pf_.get()),
+                 static_cast<const std::uint8_t*>(pfvalid_.get()), static_cast<const double2*>(w1_.get()),
+                 static_cast<const double2*>(w2_.get()), static_cast<const std::uint8_t*>(sing_.get()),
+                 static_cast<const std::uint8_t*>(psign_.get()));
+    } else if (!strict_ && weights_) {
+      flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), st_);
+    } else {
+      flux_launch(W_, strict_, fa, smem_, st_);
+    }
   }
   void launch_update(int a) {
     UpdateArgs ua;
@@ -1538,6 +1568,9 @@ class Domain {
   DBuf<D4> prim_, q_[2], dq_[2], res_;
   std::int64_t nnz_ = 0;
   DBuf<double2> w1_, w2_;       // least-squares weights of the split stencils (fast mode)
+  DBuf<PointFlux> pf_;           // first order: split fluxes per point (owned + halo)
+  DBuf<std::uint8_t> psign_;     // first order: half-stencil signs / zero offset per pair
+  DBuf<std::uint8_t> pfvalid_;
   DBuf<std::uint8_t> sing_;     // first singular split direction per point
   bool weights_ = false;
   DBuf<Ctl> ctl_;

@@ -619,8 +619,10 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
 // reference's exact operation sequence, so the singular-stencil decision
 // `!(det > det_tol)` is bitwise the reference's; sing[i] holds the first
 // singular direction of point i (0xFF: none), raised by the flux kernel.
+// psign[e] (first order): bit 0 = the pair's x half is Gx- (dx > 0), bit 1 =
+// its y half is Gy- (dy > 0), bit 2 = a zero offset (both halves).
 __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, std::uint8_t* sing,
-                               unsigned long long* zero_pairs) {
+                               unsigned long long* zero_pairs, std::uint8_t* psign) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   int e0, k;
@@ -671,6 +673,9 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
     const double2 pn = g.xy[g.nbr[e0 + j]];
     const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
     w1[e0 + j] = make_double2(wt(dx <= 0.0 ? 0 : 1, dx, dy), wt(dy <= 0.0 ? 2 : 3, dx, dy));
+    if (psign)
+      psign[e0 + j] = static_cast<std::uint8_t>((dx <= 0.0 ? 0 : 1) | (dy <= 0.0 ? 0 : 2) |
+                                                ((dx == 0.0 || dy == 0.0) ? 4 : 0));
     if (w2) w2[e0 + j] = make_double2(dx == 0.0 ? wt(1, dx, dy) : 0.0, dy == 0.0 ? wt(3, dx, dy) : 0.0);
   }
 }
@@ -796,6 +801,118 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       D4 qxn, qyn;
       dq_load(a.dq, nb, qxn, qyn);
       flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 + (e0 + j), acc);
+    }
+    const double r = reduce8(acc, lane);
+    if (live) store_res8(a.res, i, r, lane);
+  }
+  __syncthreads();
+  ktimer_end(a.ctl, KT_FLUX);
+}
+
+// ---- first order, fp_mode fast: without derivatives the pair states are the
+// points' own states (q~ = q), so each point's split fluxes are evaluated once
+// (k_point_flux: Gx+, Gx-, Gy+, Gy- of every owned and halo point) and the
+// flux kernel only gathers them: per pair dG = G_n - G_i of the pair's x and y
+// half-stencil signs, weighted and reduced as in k_flux_w.
+struct PointFlux {
+  D4 g[4];  // Gx+, Gx-, Gy+, Gy-
+};
+
+__global__ void __launch_bounds__(256) k_point_flux(int n_loc, const D4* __restrict__ q, Gas gas,
+                                                    PointFlux* __restrict__ pf, std::uint8_t* __restrict__ valid,
+                                                    const Ctl* ctl) {
+  pdl_enter();
+  ktimer_begin(const_cast<Ctl*>(ctl), KT_FLUX);  // timed with k_flux1 as one flux phase
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_loc || skip_stage(ctl, sub_flux(ctl))) return;
+  const D4 qi = ld4(q + i);
+  double t[4] = {qi.a, qi.b, qi.c, qi.d};
+  bool ok = t[3] < 0.0;
+  if (!ok) t[3] = -1.0;
+  FluxState f;
+  ok = reconstruct1_fast(t, gas, f) && ok;
+  AxisTerms at[2];
+  axis_terms2_fast(f, at);
+  const double ep = f.e + f.p, kk = fma(0.5, f.p, f.e);
+  double gv[4];
+  split_flux_fast<0>(f, at[0], false, ep, kk, gv);
+  st4(&pf[i].g[0], D4{gv[0], gv[1], gv[2], gv[3]});
+  split_flux_fast<0>(f, at[0], true, ep, kk, gv);
+  st4(&pf[i].g[1], D4{gv[0], gv[1], gv[2], gv[3]});
+  split_flux_fast<1>(f, at[1], false, ep, kk, gv);
+  st4(&pf[i].g[2], D4{gv[0], gv[1], gv[2], gv[3]});
+  split_flux_fast<1>(f, at[1], true, ep, kk, gv);
+  st4(&pf[i].g[3], D4{gv[0], gv[1], gv[2], gv[3]});
+  valid[i] = ok ? 1 : 0;
+}
+
+template <int MB>
+__global__ void __launch_bounds__(256, MB) k_flux1(FluxArgs a, const PointFlux* __restrict__ pf,
+                                                   const std::uint8_t* __restrict__ valid,
+                                                   const double2* __restrict__ w1, const double2* __restrict__ w2,
+                                                   const std::uint8_t* __restrict__ sing,
+                                                   const std::uint8_t* __restrict__ psign) {
+  pdl_enter();
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  __shared__ int s_skip;
+  ktimer_begin(a.ctl, KT_FLUX);
+  if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_flux(a.ctl));
+  __syncthreads();
+  const int lane = threadIdx.x & 7;
+  const int sub = (threadIdx.x >> 3) & 3;
+  const Geo& g = a.g;
+  const int groups = (g.n + 3) >> 2;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // stencil indices of the next group are loaded one group ahead (k <= 8)
+  auto fetch = [&](int gp, int& i, int& kind, int& k, int& e, int& nb, int& ps) {
+    i = gp * 4 + sub;
+    const int ic = i < g.n ? i : g.n - 1;
+    kind = g.kind[ic];
+    int e0 = 0;
+    stencil_of(g, ic, e0, k);
+    e = e0 + lane;
+    const bool in = i < g.n && lane < k;
+    nb = in ? g.nbr[e] : ic;
+    ps = in ? psign[e] : 0;
+  };
+  int ci = 0, ckind = 0, ck_ = 0, ce = 0, cnb = 0, cps = 0;
+  if (!s_skip && grp < groups) fetch(grp, ci, ckind, ck_, ce, cnb, cps);
+  for (; !s_skip && grp < groups; grp += nwarps) {
+    const int i = ci, e = ce, ps = cps;
+    const int ic = i < g.n ? i : g.n - 1;
+    const bool live = i < g.n && ckind != KIND_OUTER;
+    const bool act = live && lane < ck_;
+    const int nb = act ? cnb : ic;
+    if (grp + nwarps < groups) fetch(grp + nwarps, ci, ckind, ck_, ce, cnb, cps);
+    const int sx = ps & 1, sy = 2 + ((ps >> 1) & 1);
+    const double2 w = act ? w1[e] : make_double2(0.0, 0.0);
+    const D4 gix = ld4(&pf[ic].g[sx]), giy = ld4(&pf[ic].g[sy]);
+    const D4 gnx = ld4(&pf[nb].g[sx]), gny = ld4(&pf[nb].g[sy]);
+    const bool ok = valid[ic] != 0 && valid[nb] != 0;
+    if (live && lane == 0) {
+      const unsigned sd = sing[i];
+      if (sd != 0xFFu) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
+    }
+    if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), static_cast<unsigned>(sx), lane),
+                              sub_flux(a.ctl));
+    const bool store = act && ok;
+    const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
+    double acc[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = fma(wx, X::sub(comp(gnx, c), comp(gix, c)), 0.0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(comp(gny, c), comp(giy, c)), acc[c]);
+    // a zero offset belongs to both half stencils: add the minus direction
+    const bool zero = store && (ps & 4);
+    if (__any_sync(kFull, zero)) {
+      const double2 v = zero ? w2[e] : make_double2(0.0, 0.0);
+      const D4 ai = ld4(&pf[ic].g[1]), an = ld4(&pf[nb].g[1]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = fma(v.x, X::sub(comp(an, c), comp(ai, c)), acc[c]);
+      const D4 bi = ld4(&pf[ic].g[3]), bn = ld4(&pf[nb].g[3]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = fma(v.y, X::sub(comp(bn, c), comp(bi, c)), acc[c]);
     }
     const double r = reduce8(acc, lane);
     if (live) store_res8(a.res, i, r, lane);
