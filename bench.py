@@ -337,6 +337,34 @@ def large_run(L, a, counts):
             "l2": "flushed before every timed step (384 MB overwrite); working set ~3 GB > L2"}
 
 
+# BASELINE.json configs as NACA 0012 O-clouds (n_wall x n_rings): the sizes
+# the configs name, with their Mach numbers and angles of attack.
+CONFIG_SIZES = [("configs[0] ~40K, M=0.63 AoA=2", "260x154", 0.63, 2.0),
+                ("configs[1] ~160K, M=0.85 AoA=1", "520x308", 0.85, 1.0),
+                ("configs[2] ~625K, M=1.2 AoA=0", "1000x625", 1.2, 0.0),
+                ("configs[3] ~10M, M=0.85 AoA=1", "4000x2500", 0.85, 1.0)]
+
+
+def sizes_run(L, a, iters=40):
+    """Device-timed throughput at every BASELINE config size, order 2 and 1
+    (back-to-back iterations in captured graphs, after 10 warm-up iterations)."""
+    out = []
+    for label, spec, mach, aoa in CONFIG_SIZES:
+        nw, nr = (int(v) for v in spec.split("x"))
+        cloud = L.Cloud.generate_naca0012(nw, nr, 20.0, 0.0, 7, 8, frozen_wall=True)
+        row = {"config": label, "cloud": f"NACA 0012 {spec}", "n_points": cloud.n}
+        for order in (2, 1):
+            cfg = L.Config(mach=mach, aoa=aoa, order=order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
+                           iters=iters + 10, device=0)
+            with L.Session(cloud, cfg, capacity=iters + 10) as sess:
+                sess.iterate(10)
+                ms = sess.iterate(iters)
+            row[f"order{order}"] = {"value": cloud.n * iters / (ms * 1e-3), "ms_per_iteration": ms / iters}
+        out.append(row)
+    return {"unit": UNIT, "what": f"{iters} back-to-back iterations per size (no L2 flush), free stream; "
+                                   "surface held (frozen NACA variant)", "rows": out}
+
+
 def config_block(a, n, extra=None):
     c = {"workload": workload_text(a, a.dims),
          "n_points": n, "stencil": "kNN k=8 (exact, bit-identical to the reference's build_stencils)",
@@ -476,6 +504,7 @@ def run_b200_arm(a):
     }
     if (a.large_side > 0 if a.cloud == "rect" else a.large_naca != "0") and gpus == 1:
         out["large"] = large_run(L, a, counts)
+        out["sizes"] = sizes_run(L, a)
     if not a.no_cpu_baseline and gpus == 1:
         out["cpu_baseline"] = cpu_baseline(cloud, a, a.cpu_seconds)
     print(json.dumps(out), flush=True)
