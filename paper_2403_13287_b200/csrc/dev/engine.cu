@@ -293,7 +293,8 @@ void sweep8_launch(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
-  const int grid = std::max(1, std::min((2 * g.n + NT - 1) / NT, resident[dev & 63]));
+  const int npts = g.list ? g.nlist : g.n;
+  const int grid = std::max(1, std::min((2 * npts + NT - 1) / NT, resident[dev & 63]));
   launch_pdl(k_sweep2<S, MB, 8, NT>, grid, NT, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
 }
 
@@ -314,7 +315,8 @@ void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, cons
     if (sweep_small_blocks()) sweep8_launch<S, 2 * MB, 128>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
     else sweep8_launch<S, MB, 256>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   } else if (sweep_lanes() == 2) {
-    const int grid = std::max(1, std::min((2 * g.n + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
+    const int npts = g.list ? g.nlist : g.n;
+    const int grid = std::max(1, std::min((2 * npts + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
     launch_pdl(k_sweep2<S, MB, 0>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
   } else {
     const int grid = std::max(1, std::min((g.n + 255) / 256, resident_blocks(k_sweep<S, MB>, slot)));
@@ -375,6 +377,16 @@ bool flux_weighted() {
   return v != 0;
 }
 
+// Per-rank runs: interior/boundary overlap of the halo exchange
+// (LSKUM_RANK_OVERLAP=0 disables).
+bool overlap_enabled() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_RANK_OVERLAP");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 // First order, fast mode: split fluxes evaluated once per point
 // (LSKUM_POINT_FLUX=0 disables).
 bool point_flux_enabled() {
@@ -426,7 +438,7 @@ void flux_ws_launch(const FluxArgs& a, const double2* w1, const double2* w2, con
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
-  const int groups = (a.g.n + 3) / 4;
+  const int groups = ((a.g.list ? a.g.nlist : a.g.n) + 3) / 4;
   const int blocks = std::max(1, std::min((groups + NW - 1) / NW, resident[dev & 63]));
   launch_pdl(k_flux_ws<MB, NW>, blocks, NW * 32, smem, st, a, w1, w2, sing);
 }
@@ -1202,13 +1214,25 @@ class Domain {
 
   // ---- building blocks of one iteration (also used by the multi-domain driver) ----
   // Derivative sweep s of the iteration (s = 0 stamps the iteration start).
-  void launch_sweep(int a, int b, int s) {
-    sweep_launch(strict_, geo(), q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
+  // list/nlist: a subset of the owned points (see Geo::list); only the
+  // unrolled 8-point sweep and the staged flux kernel support it
+  // (subsets_supported()).
+  void launch_sweep(int a, int b, int s, const int* list = nullptr, int nlist = 0) {
+    Geo g = geo();
+    g.list = list;
+    g.nlist = nlist;
+    sweep_launch(strict_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
                  s == 0 ? it0_.get() : nullptr, s, st_);
   }
-  void launch_flux(int a, int b, bool stamp) {
+  bool subsets_supported() const {
+    return !strict_ && weights_ && kmax_ <= 8 && kfix_ == 8 && flux_staged() && sweep_lanes() == 2 &&
+           sweep_unrolled();
+  }
+  void launch_flux(int a, int b, bool stamp, const int* list = nullptr, int nlist = 0) {
     FluxArgs fa;
     fa.g = geo();
+    fa.g.list = list;
+    fa.g.nlist = nlist;
     fa.gas = gas_;
     fa.q = q_[a].get();
     fa.dq = dq_[b].get();
@@ -2069,7 +2093,9 @@ constexpr unsigned long long kStallNs = 30ull * 1000 * 1000 * 1000;
 __global__ void k_wait(WaitList w, long long mult, long long add, Ctl* ctl, int sub) {
   const int m = threadIdx.x;
   if (m >= w.n) return;
-  const unsigned long long target = iter_value(ctl, mult, add);
+  const long long starget = static_cast<long long>(iter_of(ctl)) * mult + add;
+  if (starget <= 0) return;  // counters start at 0
+  const unsigned long long target = static_cast<unsigned long long>(starget);
   const unsigned long long guard = iter_value(ctl, ctl->spi, sub);
   const unsigned long long t0 = globaltimer();
   for (;;) {
@@ -2131,6 +2157,24 @@ class RankRun {
     if (nh) {
       ck(cudaMemcpy(hdom_.get(), g.halo_dom.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hdom");
       ck(cudaMemcpy(hidx_.get(), g.halo_idx.data(), nh * sizeof(int), cudaMemcpyHostToDevice), "H2D hidx");
+    }
+    // owned points whose stencil reaches a halo slot (boundary) and the rest
+    // (interior): interior work runs while the halo is in flight
+    {
+      std::vector<int> in, bd;
+      for (std::int32_t i = 0; i < g.n_own; ++i) {
+        bool touches = false;
+        for (std::int64_t e = g.off[i]; e < g.off[i + 1] && !touches; ++e) touches = g.nbr[e] >= g.n_own;
+        (touches ? bd : in).push_back(i);
+      }
+      n_interior_ = static_cast<int>(in.size());
+      n_boundary_ = static_cast<int>(bd.size());
+      interior_.alloc(std::max<std::size_t>(1, in.size()));
+      boundary_.alloc(std::max<std::size_t>(1, bd.size()));
+      if (!in.empty())
+        ck(cudaMemcpy(interior_.get(), in.data(), in.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D interior");
+      if (!bd.empty())
+        ck(cudaMemcpy(boundary_.get(), bd.data(), bd.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D boundary");
     }
     flags_.alloc(FL_COUNT);
     ck(cudaMemset(flags_.get(), 0, FL_COUNT * sizeof(unsigned long long)), "zero flags");
@@ -2325,10 +2369,69 @@ class RankRun {
     return exec;
   }
 
+  // Second order with halo latency hidden behind interior work: each sweep and
+  // the flux run first over the interior points (no halo reads), then wait for
+  // the owners, gather the halo of the previous stage and finish the boundary
+  // points.  Counters (global sweep index k = t * inner + s): FL_SW = k + 1
+  // after sweep k; FL_DQH = j + 1 once sweep j's output halo is gathered;
+  // FL_UPD = t + 1 after update(t); FL_RES = t + 1 after the root's residue(t).
+  // Write-after-read guards: a sweep overwrites sweep k-2's output, so it waits
+  // for its readers' FL_DQH >= k - 1; update(t) writes residue summands into
+  // the root's array, so it waits for the root's FL_RES >= t.
+  void enqueue_overlapped(int t, bool timed) {
+    Domain& d = *dom_;
+    const int a = t & 1;
+    launches_ = 0;
+    const long long inner = spec_.inner;
+    const int* in = interior_.get();
+    const int* bd = boundary_.get();
+    for (int s = 0; s < spec_.inner; ++s) {
+      const int b = (t * spec_.inner + s) & 1;
+      wait_for(readers_, FL_DQH, inner, s - 1, 1 + s);
+      if (timed && s == 0) d.record_ext(kev_[0]);
+      d.launch_sweep(a, b, s, in, n_interior_);
+      if (s == 0) {
+        wait_for(src_, FL_UPD, 1, 0, 1);  // owners' q of iteration t
+        d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a], 1, true);
+      } else {
+        wait_for(src_, FL_SW, inner, s, 1 + s);  // owners finished sweep k - 1
+        d.launch_halo(d.dq_buf(b), 2, hdom_.get(), hidx_.get(), dqp_[b], 1 + s);
+        signal(FL_DQH, inner, s);
+      }
+      d.launch_sweep(a, b, s, bd, n_boundary_);
+      if (timed && s == 0) d.record_ext(kev_[1]);
+      launches_ += 3;  // interior sweep, halo, boundary sweep
+      signal(FL_SW, inner, s + 1);
+    }
+    const int bfin = ((t + 1) * spec_.inner) & 1;
+    const int sub_fl = spi_ - 3;
+    if (timed) d.record_ext(kev_[2]);
+    d.launch_flux(a, bfin, false, in, n_interior_);
+    wait_for(src_, FL_SW, inner, inner, sub_fl);  // owners finished the last sweep
+    d.launch_halo(d.dq_buf(bfin), 2, hdom_.get(), hidx_.get(), dqp_[bfin], sub_fl);
+    signal(FL_DQH, inner, inner);
+    d.launch_flux(a, bfin, false, bd, n_boundary_);
+    if (timed) d.record_ext(kev_[3]);
+    wait_for(std::vector<int>{0}, FL_RES, 1, 0, spi_ - 2);  // root's residue(t-1) has read the summands
+    d.launch_update(a);  // the device iteration index is t + 1 from here on
+    launches_ += 4;      // interior flux, halo, boundary flux, update
+    signal(FL_UPD, 1, 0);
+    if (rank_ == 0) {
+      std::vector<int> all;
+      for (int o = 1; o < world_; ++o) all.push_back(o);
+      wait_for(all, FL_UPD, 1, 0, -1);
+      d.launch_residue();
+      launches_ += 2;
+      signal(FL_RES, 1, 0);
+    }
+    ck(cudaGetLastError(), "rank launches");
+  }
+
   // One iteration; only the buffer parities depend on the host-side t (the
   // counters' targets follow the device iteration index).  Timed: CUDA
   // events around the first sweep and the flux kernel.
   void enqueue_iteration(int t, bool timed) {
+    if (spec_.order == 2 && dom_->subsets_supported() && overlap_enabled()) return enqueue_overlapped(t, timed);
     Domain& d = *dom_;
     cudaStream_t st = d.stream();
     const int a = t & 1;
@@ -2378,6 +2481,8 @@ class RankRun {
   std::unique_ptr<Domain> dom_;
   std::vector<int> src_, readers_;
   DBuf<int> hdom_, hidx_;
+  DBuf<int> interior_, boundary_;
+  int n_interior_ = 0, n_boundary_ = 0;
   DBuf<unsigned long long> flags_;
   PeerTab qp_[2]{}, dqp_[2]{};
   unsigned long long* flag_[kMaxDomains] = {};

@@ -99,7 +99,18 @@ struct Geo {
   const int* gid;  // local -> global point id (null: local ids are global)
   int n;           // owned points (kernels loop over these)
   int kfix;        // uniform stencil size (offsets are then i*kfix), 0 = use CSR offsets
+  // Optional subset of the owned points (k_sweep2, k_flux_ws): when set, the
+  // kernel visits points list[0..nlist) instead of 0..n — interior points
+  // before the halo arrives, boundary points after.
+  const int* list = nullptr;
+  int nlist = 0;
 };
+
+// Number of points a subset-aware kernel visits, and the t-th of them.
+__device__ __forceinline__ int visit_count(const Geo& g) { return g.list ? g.nlist : g.n; }
+__device__ __forceinline__ int visit_point(const Geo& g, int t) {
+  return g.list ? (t < g.nlist ? g.list[t] : g.n) : t;
+}
 
 __device__ __forceinline__ int gidx(const Geo& g, int i) { return g.gid ? g.gid[i] : i; }
 
@@ -320,19 +331,20 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
   const int h = threadIdx.x & 1;
   const double* qd = reinterpret_cast<const double*>(q) + 2 * h;
   const double* dd = reinterpret_cast<const double*>(dq_in) + 4 * h;  // {qx, qy} of this lane's pair
-  const long long n2 = 2ll * g.n;
+  const long long n2 = 2ll * visit_count(g);
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   // K = 8: the next point's neighbour ids are loaded one point ahead
   int4 na0 = make_int4(0, 0, 0, 0), na1 = na0;
   if constexpr (K == 8) {
     if (t < n2) {
-      na0 = ld_i4(g.nbr + 8 * (t >> 1));
-      na1 = ld_i4(g.nbr + 8 * (t >> 1) + 4);
+      const long long p0 = visit_point(g, static_cast<int>(t >> 1));
+      na0 = ld_i4(g.nbr + 8 * p0);
+      na1 = ld_i4(g.nbr + 8 * p0 + 4);
     }
   }
   for (; !s_skip && t < n2; t += stride) {
-    const int i = static_cast<int>(t >> 1);
+    const int i = visit_point(g, static_cast<int>(t >> 1));
     const double2 pi = g.xy[i];
     const double2 qi = ld2(qd + 4 * i);
     double2 qxi, qyi;
@@ -347,8 +359,9 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
       nbk[0] = na0.x, nbk[1] = na0.y, nbk[2] = na0.z, nbk[3] = na0.w;
       nbk[4] = na1.x, nbk[5] = na1.y, nbk[6] = na1.z, nbk[7] = na1.w;
       if (t + stride < n2) {
-        na0 = ld_i4(g.nbr + 8 * ((t + stride) >> 1));
-        na1 = ld_i4(g.nbr + 8 * ((t + stride) >> 1) + 4);
+        const long long p1 = visit_point(g, static_cast<int>((t + stride) >> 1));
+        na0 = ld_i4(g.nbr + 8 * p1);
+        na1 = ld_i4(g.nbr + 8 * p1 + 4);
       }
     } else {
       stencil_of(g, i, e0, k);
@@ -953,7 +966,7 @@ struct StageRaw {
 __device__ __forceinline__ StageRaw stage_load(const Geo& g, const std::uint8_t* sing, int grp, int lane,
                                                int sub) {
   StageRaw r;
-  r.i = grp * 4 + sub;
+  r.i = visit_point(g, grp * 4 + sub);
   const int ic = r.i < g.n ? r.i : g.n - 1;
   r.kind = g.kind[ic];
   r.sing = lane == 0 ? sing[ic] : 0xFF;  // first singular split direction (k_flux_weights)
@@ -1016,7 +1029,7 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
   const int warp = threadIdx.x >> 5;
   char* const stage0 = fsm + (2 * warp) * kFluxStageBytes;  // stage b at stage0 + b * kFluxStageBytes
   const Geo& g = a.g;
-  const int groups = (g.n + 3) >> 2;
+  const int groups = (visit_count(g) + 3) >> 2;
   const int nwarps = gridDim.x * NW;
   int grp = blockIdx.x * NW + warp;
   if (!s_skip && grp < groups) {

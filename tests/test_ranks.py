@@ -94,6 +94,24 @@ def test_ranks_bitwise_single_domain(bump_cloud_arrays, world, order):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_ranks_overlap_switch_is_bitwise(bump_cloud_arrays, monkeypatch, overlap):
+    """Interior/boundary split on (default) and off give the same bits."""
+    monkeypatch.setenv("LSKUM_RANK_OVERLAP", overlap)  # inherited by the spawned ranks
+    c, prim0 = bump_cloud_arrays
+    cfg = dict(BASE, order=2)
+    want_f, want_r = _single(c, prim0, 30, **cfg)
+    out = W.launch(W.run_rank, 4, arrays_of(c), prim0, cfg, [1, 11, 18], 0)
+    assert all(v[0] == "ok" for v in out), out
+    assert np.array_equal(out[0][1], want_r)
+    from paper_2403_13287_b200 import lskum as L
+
+    owned, _ = L.partition(L.Cloud.from_arrays(*arrays_of(c)), 4)
+    for r, v in enumerate(out):
+        assert np.array_equal(v[2][owned[r]], want_f[owned[r]]), r
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("world,parts", [(2, 1), (4, 8)])
 def test_ranks_abort_matches_reference(bump_cloud_arrays, golden, world, parts):
     c, prim0 = bump_cloud_arrays
