@@ -40,6 +40,23 @@ void ck(cudaError_t e, const char* what) {
   }
 }
 
+// LSKUM_GRAPHS=0: iterations launched kernel by kernel instead of as
+// captured CUDA graphs (single-domain runs).
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSKUM_GRAPHS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// LSKUM_TRACE only: waits for the stream so the trace line times its work.
+void trace_sync(cudaStream_t st, const char* what) {
+  if (!tracing()) return;
+  cudaStreamSynchronize(st);
+  trace(what);
+}
+
 // Device buffers come from the device's stream-ordered memory pool
 // (cudaMallocAsync), whose release threshold is raised once per device so
 // memory freed by one run is reused by the next without driver round trips.
@@ -769,18 +786,10 @@ class Domain {
     ck(cudaEventCreate(&ev1_), "cudaEventCreate");
     for (auto& e : kev_) ck(cudaEventCreate(&e), "cudaEventCreate");
     for (auto& e : poll_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    trace("domain: stream and events");
     if (gv.nnz >= (1ll << 31)) raise(Status::argument, "stencil table exceeds 2^31 entries");
     gas_ = make_gas(gamma, cfl, det_tol);
-    std::int64_t km = 1;
-    for (int i = 0; i < n_; ++i) km = std::max(km, gv.off[i + 1] - gv.off[i]);
-    kmax_ = static_cast<int>(km);
-    kfix_ = kmax_;
-    for (int i = 0; i < n_ && kfix_ > 0; ++i)
-      if (gv.off[i + 1] - gv.off[i] != kmax_ || gv.off[i] != static_cast<std::int64_t>(i) * kmax_) kfix_ = 0;
     nnz_ = gv.nnz;
-    W_ = flux_width(kmax_);
-    smem_ = flux_smem_bytes(W_, kmax_);
-    stride_ = flux_stride(kmax_);
     d1_ = tree_depth(n_);
     n_res_ = n_;
 
@@ -790,7 +799,9 @@ class Domain {
     // geometry, packed on the host into pinned staging, then async copies
     const std::size_t b_xy = nl * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
     const std::size_t b_gid = gv.gid ? nl * sizeof(int) : 0;
+    trace("domain: pool");
     char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 2 * nl + b_off + b_nbr + b_gid + 64));
+    trace("domain: staging buffer");
     double2* hxy = reinterpret_cast<double2*>(hs);
     double2* hnrm = hxy + nl;
     std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hnrm + nl);
@@ -798,24 +809,54 @@ class Domain {
     int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * nl + 15) & ~std::size_t{15}));
     int* hnbr = hoff + n + 1;
     int* hgid = hnbr + nnz;
-    parallel_slices(static_cast<std::int64_t>(nl), [&](std::int64_t lo, std::int64_t hi) {
-      for (std::int64_t i = lo; i < hi; ++i) {
-        hxy[i] = make_double2(gv.x[i], gv.y[i]);
-        hnrm[i] = make_double2(gv.nx[i], gv.ny[i]);
+    // One pass over the cloud on the host threads: stencil-size scan (kmax,
+    // uniform size kfix) and staging.  Staging uses streaming stores / flushed
+    // lines, so the DMA below runs at PCIe rate (hostcopy.cpp).
+    const int tasks = std::max(1, std::min(host_threads(), static_cast<int>(nl >> 14)));
+    const std::int64_t k0 = n ? gv.off[1] - gv.off[0] : 0;
+    std::vector<std::int64_t> t_kmax(static_cast<std::size_t>(tasks), 1);
+    std::vector<char> t_uniform(static_cast<std::size_t>(tasks), 1);
+    parallel_tasks(tasks, [&](int t) {
+      auto part_of = [&](std::size_t len, int k) { return len * static_cast<std::size_t>(k) / tasks; };
+      const std::size_t lo = part_of(nl, t), hi = part_of(nl, t + 1), c = hi - lo;
+      stream_pairs(reinterpret_cast<double*>(hxy + lo), gv.x + lo, gv.y + lo, c);
+      stream_pairs(reinterpret_cast<double*>(hnrm + lo), gv.nx + lo, gv.ny + lo, c);
+      for (std::size_t i = lo; i < hi; ++i) {
         hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
         hpart[i] = gv.part ? gv.part[i] : 0;
       }
-    }, 1 << 15);
-    parallel_slices(static_cast<std::int64_t>(n) + 1, [&](std::int64_t lo, std::int64_t hi) {
-      for (std::int64_t i = lo; i < hi; ++i) hoff[i] = static_cast<int>(gv.off[i]);
-    }, 1 << 16);
-    if (nnz)
-      parallel_slices(static_cast<std::int64_t>(b_nbr), [&](std::int64_t lo, std::int64_t hi) {
-        std::memcpy(reinterpret_cast<char*>(hnbr) + lo, reinterpret_cast<const char*>(gv.nbr) + lo,
-                    static_cast<std::size_t>(hi - lo));
-      }, 1 << 20);
+      flush_lines(hkind + lo, c);
+      flush_lines(hpart + lo, c);
+      const std::size_t olo = part_of(n, t), ohi = part_of(n, t + 1);
+      std::int64_t km = 1;
+      bool uni = true;
+      for (std::size_t i = olo; i < ohi; ++i) {
+        const std::int64_t e0 = gv.off[i], k = gv.off[i + 1] - e0;
+        km = std::max(km, k);
+        uni = uni && k == k0 && e0 == static_cast<std::int64_t>(i) * k0;
+        hoff[i] = static_cast<int>(e0);
+      }
+      if (t == tasks - 1) hoff[n] = static_cast<int>(gv.off[n]);
+      flush_lines(hoff + olo, (ohi - olo + (t == tasks - 1)) * sizeof(int));
+      t_kmax[t] = km;
+      t_uniform[t] = uni;
+      const std::size_t blo = part_of(b_nbr, t), bhi = part_of(b_nbr, t + 1);
+      stream_copy(reinterpret_cast<char*>(hnbr) + blo, reinterpret_cast<const char*>(gv.nbr) + blo, bhi - blo);
+    });
+    std::int64_t km = 1;
+    bool uniform = true;
+    for (int t = 0; t < tasks; ++t) {
+      km = std::max(km, t_kmax[t]);
+      uniform = uniform && t_uniform[t];
+    }
+    kmax_ = static_cast<int>(km);
+    kfix_ = uniform && k0 == km ? kmax_ : 0;
+    W_ = flux_width(kmax_);
+    smem_ = flux_smem_bytes(W_, kmax_);
+    stride_ = flux_stride(kmax_);
     if (gv.gid) {
       std::memcpy(hgid, gv.gid, b_gid);
+      flush_lines(hgid, b_gid);
       gid_host_.assign(gv.gid, gv.gid + nl);
     }
     trace("domain: staged");
@@ -826,13 +867,17 @@ class Domain {
     off_.alloc(n + 1, st_);
     nbr_.alloc(std::max<std::size_t>(1, nnz), st_);
     mind_.alloc(n, st_);
+    trace_sync(st_, "domain: geometry buffers allocated");
     ck(cudaMemcpyAsync(xy_.get(), hxy, b_xy, cudaMemcpyHostToDevice, st_), "H2D xy");
+    trace_sync(st_, "domain: xy copied");
     ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
     ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
     ck(cudaMemcpyAsync(part_.get(), hpart, nl, cudaMemcpyHostToDevice, st_), "H2D part");
     part_host_.assign(hpart, hpart + nl);
     ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
+    trace_sync(st_, "domain: nrm kind part off copied");
     if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
+    trace_sync(st_, "domain: nbr copied");
     if (gv.gid) {
       gid_.alloc(nl, st_);
       ck(cudaMemcpyAsync(gid_.get(), hgid, b_gid, cudaMemcpyHostToDevice, st_), "H2D gid");
@@ -863,6 +908,7 @@ class Domain {
     hctl_.alloc(1);
     hsh_.alloc(1);
     trace("domain: allocated, copies queued");
+    trace_sync(st_, "domain: copies done");
     k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
     ck(cudaGetLastError(), "k_min_dist");
     k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0, update_blocks());
@@ -974,10 +1020,11 @@ class Domain {
       const bool soa = f.layout() == Layout::soa;
       double* h = static_cast<double*>(t_staging.get(4 * n * sizeof(double)));
       if (soa) {
-        std::memcpy(h, f.raw(), 4 * n * sizeof(double));
+        stream_copy(h, f.raw(), 4 * n * sizeof(double));
       } else {
         const double* src = f.raw();
         for (std::size_t i = 0; i < n; ++i) std::memcpy(h + 4 * i, src + 21 * i, 4 * sizeof(double));
+        flush_lines(h, 4 * n * sizeof(double));
       }
       DBuf<double> tmp(4 * n, st_);
       ck(cudaMemcpyAsync(tmp.get(), h, 4 * n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D prim");
@@ -995,6 +1042,7 @@ class Domain {
         const int p = gid_host_[i];
         h[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2), f.at(p, slot::prim + 3)};
       }
+      flush_lines(h, nl * sizeof(D4));
       ck(cudaMemcpyAsync(prim_.get(), h, nl * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D prim");
       ck(cudaStreamSynchronize(st_), "upload");
       return;
@@ -1029,6 +1077,7 @@ class Domain {
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
           n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
+      trace_sync(st_, "download: packed");
       // through pinned staging (full-rate D2H) in chunks; host threads copy
       // each chunk into the store as soon as its transfer completes
       const std::size_t count = 21 * n, bytes = count * sizeof(double);
@@ -1049,9 +1098,11 @@ class Domain {
           cudaEventSynchronize(done[c]);
           const std::size_t lo = lo_of(c), hi = lo_of(c + 1);
           std::memcpy(dst + lo, h + lo, (hi - lo) * sizeof(double));
+          flush_lines(h + lo, (hi - lo) * sizeof(double));  // the next DMA into staging stays at full rate
         }
       }, 1);
       ck(cudaStreamSynchronize(st_), "download");
+      trace("download: stored");
       for (cudaEvent_t e : done) cudaEventDestroy(e);
       return;
     }
@@ -1341,8 +1392,9 @@ class Domain {
     if (done_ + n > capacity_) raise(Status::argument, "session capacity exceeded");
     ck(cudaSetDevice(device_), "cudaSetDevice");
     set_diag(done_ + n - 1);
+    const bool direct = !graphs_enabled();
     // capture graphs before timing
-    {
+    if (!direct) {
       int a = a_, b = b_, left = n;
       while (left > 0) {
         const int c = std::min(chunk_, left);
@@ -1357,8 +1409,12 @@ class Domain {
     bool failed = false;
     while (left > 0 && !failed) {
       const int c = std::min(chunk_, left);
-      ck(cudaGraphLaunch(graph_for(a_, b_, c), st_), "GraphLaunch");
-      advance(a_, b_, c);
+      if (direct) {
+        for (int k = 0; k < c; ++k) enqueue_iteration(a_, b_, k == c - 1);
+      } else {
+        ck(cudaGraphLaunch(graph_for(a_, b_, c), st_), "GraphLaunch");
+        advance(a_, b_, c);
+      }
       left -= c;
       if (left == 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");
       failed = poll(issued, waited);

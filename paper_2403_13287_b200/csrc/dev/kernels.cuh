@@ -1092,6 +1092,55 @@ struct UpdateArgs {
   Ctl* ctl;
 };
 
+// state_update for owned point ip; returns its residue summand (dt*res0)^2
+// (0 for outer points and for a failing point, whose error is recorded).
+__device__ __forceinline__ double update_point(const UpdateArgs& a, int ip, bool diag) {
+  const Geo& g = a.g;
+  if (g.kind[ip] == KIND_OUTER) {
+    st4(a.q_next + ip, ld4(a.q + ip));
+    if (diag) a.dt[ip] = 0.0;
+    return 0.0;
+  }
+  const D4 r = ld4(a.res + ip);
+  const D4 s = ld4_rw(a.prim + ip);
+  const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
+  const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
+  const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
+  double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
+  double en = X::add(s.d / a.gas.gm1,
+                     X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
+  m = X::sub(m, X::mul(dt, r.a));
+  mx = X::sub(mx, X::mul(dt, r.b));
+  my_ = X::sub(my_, X::mul(dt, r.c));
+  en = X::sub(en, X::mul(dt, r.d));
+  bool ok = m > 0.0;
+  double u1 = 0.0, u2 = 0.0, p = 0.0;
+  if (ok) {
+    u1 = mx / m;
+    u2 = my_ / m;
+    p = X::mul(a.gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
+    ok = p > 0.0;
+  }
+  if (!ok) {
+    // keep the failing conserved value for the diagnostic message
+    a.dt[ip] = m > 0.0 ? p : m;
+    a.which[ip] = m > 0.0 ? 1.0 : 0.0;
+    raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0), sub_update(a.ctl));
+    return 0.0;
+  }
+  if (g.kind[ip] == KIND_WALL) {
+    const double2 nv = g.nrm[ip];
+    const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
+    u1 = X::sub(u1, X::mul(un, nv.x));
+    u2 = X::sub(u2, X::mul(un, nv.y));
+  }
+  st4(a.prim + ip, D4{m, u1, u2, p});
+  st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
+  if (diag) a.dt[ip] = dt;
+  const double dm = X::mul(dt, r.a);
+  return X::mul(dm, dm);
+}
+
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   pdl_enter();
   __shared__ int s_skip;
@@ -1101,50 +1150,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   const Geo& g = a.g;
   const bool diag = iter_of(a.ctl) == a.ctl->diag_iter;
   for (int ip = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && ip < g.n; ip += gridDim.x * blockDim.x) {
-    if (g.kind[ip] == KIND_OUTER) {
-      st4(a.q_next + ip, ld4(a.q + ip));
-      a.mag[gidx(g, ip)] = 0.0;
-      if (diag) a.dt[ip] = 0.0;
-    } else {
-      const D4 r = ld4(a.res + ip);
-      const D4 s = ld4_rw(a.prim + ip);
-      const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
-      const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
-      const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
-      double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
-      double en = X::add(s.d / a.gas.gm1,
-                         X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
-      m = X::sub(m, X::mul(dt, r.a));
-      mx = X::sub(mx, X::mul(dt, r.b));
-      my_ = X::sub(my_, X::mul(dt, r.c));
-      en = X::sub(en, X::mul(dt, r.d));
-      bool ok = m > 0.0;
-      double u1 = 0.0, u2 = 0.0, p = 0.0;
-      if (ok) {
-        u1 = mx / m;
-        u2 = my_ / m;
-        p = X::mul(a.gas.gm1, X::sub(en, X::mul(0.5, X::add(X::mul(mx, u1), X::mul(my_, u2)))));
-        ok = p > 0.0;
-      }
-      if (!ok) {
-        // keep the failing conserved value for the diagnostic message
-        a.dt[ip] = m > 0.0 ? p : m;
-        a.which[ip] = m > 0.0 ? 1.0 : 0.0;
-        raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0), sub_update(a.ctl));
-      } else {
-        if (g.kind[ip] == KIND_WALL) {
-          const double2 nv = g.nrm[ip];
-          const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
-          u1 = X::sub(u1, X::mul(un, nv.x));
-          u2 = X::sub(u2, X::mul(un, nv.y));
-        }
-        st4(a.prim + ip, D4{m, u1, u2, p});
-        st4(a.q_next + ip, q_from_prim(m, u1, u2, p, a.gas.gm1));
-        const double dm = X::mul(dt, r.a);
-        a.mag[gidx(g, ip)] = X::mul(dm, dm);
-        if (diag) a.dt[ip] = dt;
-      }
-    }
+    a.mag[gidx(g, ip)] = update_point(a, ip, diag);
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_UPDATE);
@@ -1262,15 +1268,17 @@ __device__ __forceinline__ void tree_pair(double vl, long long sl, double vr, lo
   v = s <= 0 ? 0.0 : (s == 1 ? (sr == 1 ? vr : vl) : X::add(vl, vr));
 }
 
-// Loads the 2^d1 partials as 2^min(d1, 10) subtree values: with d1 > 10 each
-// thread folds its 2^(d1-10) consecutive partials (one subtree) serially.
+// Loads the 2^d1 partials (d1 <= 13) as 2^min(d1, LV) subtree values: with
+// d1 > LV each thread folds its 2^(d1-LV) consecutive partials (one subtree)
+// serially.
+template <int LV = 10>
 __device__ __forceinline__ int tree_load_partials(const double* part_val, const long long* part_sz, int d1,
                                                   double* sv, long long* ss) {
-  const int lv = d1 > 10 ? 10 : d1;
+  const int lv = d1 > LV ? LV : d1;
   const int per = 1 << (d1 - lv);
   for (int t = threadIdx.x; t < (1 << lv); t += blockDim.x) {
-    double v[8];
-    long long s[8];
+    double v[1 << (13 - LV)];
+    long long s[1 << (13 - LV)];
     for (int k = 0; k < per; ++k) {
       v[k] = part_val[t * per + k];
       s[k] = part_sz[t * per + k];
@@ -1348,24 +1356,23 @@ __global__ void __launch_bounds__(kTreeThreads)
   ktimer_end(ctl, KT_RESIDUE, nullptr);
 }
 
-// Stage 2: one block folds the 2^d1 partials, forms sqrt(sum)/n and records
-// the history entry (runtime.cpp:251-269); non-finite -> positivity error.
-__global__ void __launch_bounds__(1024)
-    k_tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
-                 double* history, unsigned long long* iter_t0, unsigned long long* iter_t1, Ctl* ctl) {
-  pdl_enter();
-  __shared__ double sv[2][1024];
-  __shared__ long long ss[2][1024];
-  __shared__ int s_skip;
-  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl), 1);
+// Stage 2: one block of T threads folds the 2^d1 partials, forms sqrt(sum)/n
+// and records the history entry (runtime.cpp:251-269); non-finite ->
+// positivity error.  sv/ss: [2][1024] shared scratch.
+template <int T, int LV = 10>
+__device__ __forceinline__ void tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
+                                           double* history, unsigned long long* iter_t0,
+                                           unsigned long long* iter_t1, Ctl* ctl, double (*sv)[1 << LV],
+                                           long long (*ss)[1 << LV], int* s_skip) {
+  if (threadIdx.x == 0) *s_skip = skip_stage(ctl, sub_residue(ctl), 1);
   __syncthreads();
-  if (s_skip) {
+  if (*s_skip) {
     if (threadIdx.x == 0) ktimer_fold(ctl);
     return;
   }
-  const int lv = tree_load_partials(part_val, part_sz, d1, sv[0], ss[0]);
+  const int lv = tree_load_partials<LV>(part_val, part_sz, d1, sv[0], ss[0]);
   __syncthreads();
-  tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], lv);
+  tree_combine<T>(sv[0], ss[0], sv[1], ss[1], lv);
   if (threadIdx.x == 0) {
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
     const int it = iter_of(ctl, 1);
@@ -1382,13 +1389,23 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+__global__ void __launch_bounds__(1024)
+    k_tree_final(const double* part_val, const long long* part_sz, int d1, long long n,
+                 double* history, unsigned long long* iter_t0, unsigned long long* iter_t1, Ctl* ctl) {
+  pdl_enter();
+  __shared__ double sv[2][1024];
+  __shared__ long long ss[2][1024];
+  __shared__ int s_skip;
+  tree_final<1024>(part_val, part_sz, d1, n, history, iter_t0, iter_t1, ctl, sv, ss, &s_skip);
+}
+
 // Plain tree sum of an arbitrary vector (lskum_b200_reduce): same two stages
 // without the history bookkeeping.
 __global__ void k_tree_result(const double* part_val, const long long* part_sz, int d1,
                               double* out) {
   __shared__ double sv[2][1024];
   __shared__ long long ss[2][1024];
-  const int lv = tree_load_partials(part_val, part_sz, d1, sv[0], ss[0]);
+  const int lv = tree_load_partials<10>(part_val, part_sz, d1, sv[0], ss[0]);
   __syncthreads();
   tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], lv);
   if (threadIdx.x == 0) *out = sv[0][0];

@@ -41,6 +41,13 @@ class Fault : public std::runtime_error {
 
 // Host-phase tracing to stderr when LSKUM_TRACE is set (setup cost analysis).
 void trace(const char* what);
+bool tracing();
+
+// Pinned staging I/O (hostcopy.cpp): streaming stores into staging, and
+// flushing staging lines after the host read them, keep the DMA at PCIe rate.
+void flush_lines(const void* p, std::size_t bytes);
+void stream_copy(void* dst, const void* src, std::size_t bytes);
+void stream_pairs(double* dst, const double* a, const double* b, std::size_t n);  // dst[2i] = a[i], dst[2i+1] = b[i]
 
 // %f rendering, as std::to_string(double) produces in the reference messages.
 std::string fmt_f(double v);

@@ -26,9 +26,13 @@
 
 namespace lskb {
 
-void trace(const char* what) {
+bool tracing() {
   static const bool on = std::getenv("LSKUM_TRACE") != nullptr;
-  if (!on) return;
+  return on;
+}
+
+void trace(const char* what) {
+  if (!tracing()) return;
   static const auto t0 = std::chrono::steady_clock::now();
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   std::fprintf(stderr, "[lskum %10.3f ms] %s\n", ms, what);
