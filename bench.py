@@ -12,9 +12,11 @@ stream lskum_run initialises — an exact fixed point with the full arithmetic
 cost.  `--cloud rect` uses the reference's jittered rectangle instead.  The
 `large` block repeats the measurement on a ~10M-point cloud (configs[3]).
 
-One step = one fixed-point iteration (3 sweeps + fused flux/update + residue).
+One step = one fixed-point iteration (3 sweeps, flux, update, residue tree).
 `value` times K steps with CUDA events on the engine's stream, with the L2
-flushed (384 MB overwrite) before every step; `e2e` times lskum_run through the
+flushed (384 MB overwrite) before every step: each step is one CUDA graph
+[flush, start event, iteration, end event], so the events bracket the cold-L2
+iteration and not the flush or the graph launch; `e2e` times lskum_run through the
 C ABI from host buffers (upload, K iterations, copy-back of the 21-slot store).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -317,13 +319,13 @@ def large_run(L, a, counts):
     cfg = L.Config(mach=a.mach, aoa=a.aoa, order=a.order, inner=a.inner, cfl=0.5, fp_mode=a.fp_mode,
                    iters=a.large_steps, device=0)
     step_ms, sweep_ms, flux_ms = [], [], []
-    with ClockSampler(0) as clocks, L.Session(cloud, cfg, capacity=a.large_steps + 3) as sess:
+    with ClockSampler(0) as clocks, L.Session(cloud, cfg, capacity=2 * a.large_steps + 3) as sess:
         for _ in range(3):
-            sess.flush_l2()
-            sess.iterate(1)
+            sess.step_flushed()
         for _ in range(a.large_steps):
-            sess.flush_l2()
-            step_ms.append(sess.iterate(1))
+            step_ms.append(sess.step_flushed())
+        for _ in range(a.large_steps):  # per-kernel events: separate steps (their event nodes lengthen a step)
+            sess.step_flushed(kernel_events=True)
             sw, fl = sess.event_ms()
             sweep_ms.append(sw)
             flux_ms.append(fl)
@@ -369,7 +371,7 @@ def config_block(a, n, extra=None):
     c = {"workload": workload_text(a, a.dims),
          "n_points": n, "stencil": "kNN k=8 (exact, bit-identical to the reference's build_stencils)",
          "order": a.order, "inner": a.inner, "mach": a.mach, "aoa_deg": a.aoa, "cfl": 0.5,
-         "fp_mode": a.fp_mode, "l2": "flushed before every timed step (384 MB overwrite)",
+         "fp_mode": a.fp_mode, "l2": "flushed before every timed step (384 MB overwrite in the same CUDA graph, ahead of the step's start event)",
          "parallelism": f"rcb{a.gpus}" if a.gpus > 1 else "single-domain"}
     if extra:
         c.update(extra)
@@ -423,14 +425,14 @@ def run_b200_arm(a):
                    iters=a.steps, device=0, gpus=gpus)
     steady_iters = 0
     with ClockSampler(0) as clocks:
-        sess = L.Session(cloud, cfg, capacity=a.warmup + a.steps + 4000)
+        sess = L.Session(cloud, cfg, capacity=a.warmup + 2 * a.steps + 4000)
         for _ in range(a.warmup):
-            sess.flush_l2()
-            sess.iterate(1)
+            sess.step_flushed()
         step_ms, sweep_ms, flux_ms = [], [], []
         for _ in range(a.steps):
-            sess.flush_l2()
-            step_ms.append(sess.iterate(1))
+            step_ms.append(sess.step_flushed())
+        for _ in range(a.steps):  # per-kernel events: separate steps (their event nodes lengthen a step)
+            sess.step_flushed(kernel_events=True)
             sw, fl = sess.event_ms()
             sweep_ms.append(sw)
             flux_ms.append(fl)

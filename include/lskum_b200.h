@@ -127,10 +127,16 @@ int lskum_b200_session_info(const lskum_b200_session* s, int* launches_per_iter,
                             uint64_t* stream);
 int lskum_b200_session_download(lskum_b200_session* s);
 /* CUDA-event milliseconds of the first derivative sweep and of the flux
- * kernel of the most recent iteration (events recorded inside the graph). */
+ * kernel of the latest lskum_b200_session_step_flushed(kernel_events = 1)
+ * (events recorded inside the graph; multi-device sessions: latest iteration). */
 int lskum_b200_session_event_ms(const lskum_b200_session* s, double* sweep_ms, double* flux_ms);
 /* Overwrites a 384 MB scratch buffer on the session stream (cold-L2 steps). */
 int lskum_b200_session_flush_l2(lskum_b200_session* s);
+/* One cold-L2 step: the flush and one iteration in one CUDA graph;
+ * *device_ms = CUDA-event time of the iteration (events inside the graph).
+ * kernel_events != 0 also records the event_ms() events around the first
+ * sweep and the flux kernel (which lengthens the step). */
+int lskum_b200_session_step_flushed(lskum_b200_session* s, int kernel_events, double* device_ms);
 /* Measured FP64 FMA throughput of `device` (TFLOP/s, DFMA = 2 flops). */
 int lskum_b200_fp64_peak(int device, double* tflops);
 void lskum_b200_session_destroy(lskum_b200_session* s);

@@ -50,6 +50,14 @@ bool graphs_enabled() {
   return on;
 }
 
+bool graph_upload() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSKUM_GRAPH_UPLOAD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // LSKUM_TRACE only: waits for the stream so the trace line times its work.
 void trace_sync(cudaStream_t st, const char* what) {
   if (!tracing()) return;
@@ -1369,12 +1377,15 @@ class Domain {
     cudaGraph_t graph;
     ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "BeginCapture");
     int pa = a, pb = b;
-    for (int k = 0; k < c; ++k) enqueue_iteration(pa, pb, k == c - 1);
+    // no per-kernel event nodes (they lengthen the iteration); event_ms()
+    // reads the events of step_flushed(kernel_events = true)
+    for (int k = 0; k < c; ++k) enqueue_iteration(pa, pb, false);
     ck(cudaGetLastError(), "capture launches");
     ck(cudaStreamEndCapture(st_, &graph), "EndCapture");
     cudaGraphExec_t exec;
     ck(cudaGraphInstantiate(&exec, graph, 0), "GraphInstantiate");
     cudaGraphDestroy(graph);
+    if (graph_upload()) ck(cudaGraphUpload(exec, st_), "GraphUpload");  // launch without a first-use upload
     graphs_[key] = exec;
     return exec;
   }
@@ -1421,6 +1432,48 @@ class Domain {
     }
     if (left > 0) ck(cudaEventRecord(ev1_, st_), "EventRecord");  // stopped early
     ck(cudaStreamSynchronize(st_), "iterate");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "EventElapsed");
+    total_ms_ += ms;
+    refresh_ctl();
+    done_ = completed();
+    return ms;
+  }
+
+  // One cold-L2 step (bench.py's timed steps): a graph of [L2 flush, event,
+  // one iteration, event].  The events bracket the iteration inside the
+  // graph, so the step's device time excludes the flush and the graph launch
+  // (a one-iteration graph launched from the host costs ~20 us of GPU-side
+  // start-up that back-to-back iterations never pay).
+  // kernel_events: also bracket the first sweep and the flux kernel with
+  // events (last_event_ms); event nodes between kernels lengthen the step.
+  double step_flushed(bool kernel_events) {
+    if (done_ + 1 > capacity_) raise(Status::argument, "session capacity exceeded");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    if (!flush_.get()) flush_.alloc(static_cast<std::size_t>(48) << 20);  // 384 MB
+    set_diag(done_);
+    const auto key = std::make_tuple(a_, b_, kernel_events ? -2 : -1);
+    auto it = graphs_.find(key);
+    cudaGraphExec_t exec;
+    if (it != graphs_.end()) {
+      exec = it->second;
+    } else {
+      cudaGraph_t graph;
+      ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+      k_flush<<<148 * 8, 256, 0, st_>>>(flush_.get(), static_cast<long long>(flush_.size()), 1.0);
+      record_ext(ev0_);
+      int pa = a_, pb = b_;
+      enqueue_iteration(pa, pb, kernel_events);
+      record_ext(ev1_);
+      ck(cudaGetLastError(), "capture launches");
+      ck(cudaStreamEndCapture(st_, &graph), "EndCapture");
+      ck(cudaGraphInstantiate(&exec, graph, 0), "GraphInstantiate");
+      cudaGraphDestroy(graph);
+      graphs_[key] = exec;
+    }
+    ck(cudaGraphLaunch(exec, st_), "GraphLaunch");
+    advance(a_, b_, 1);
+    ck(cudaStreamSynchronize(st_), "step");
     float ms = 0.0f;
     ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "EventElapsed");
     total_ms_ += ms;
@@ -1484,10 +1537,13 @@ class Domain {
     cudaGetLastError();
   }
 
+  // Overwrites 384 MB (> the 126 MB L2) on this domain's stream.  Stream
+  // ordered, no host wait: the next step's kernels are queued behind it, so a
+  // timed step starts on a cold L2 without an idle GPU waiting for its launch.
   void flush_l2() {
     if (!flush_.get()) flush_.alloc(static_cast<std::size_t>(48) << 20);  // 384 MB
     k_flush<<<148 * 8, 256, 0, st_>>>(flush_.get(), static_cast<long long>(flush_.size()), 1.0);
-    ck(cudaStreamSynchronize(st_), "flush");
+    ck(cudaGetLastError(), "flush");
   }
 
   // q / published dq read by 0-based iteration t (parities start at 0 per run).
@@ -1606,6 +1662,12 @@ class Domain {
     std::vector<KernelTime> out;
     for (int r = 0; r < 5; ++r)
       if (cnt[r] > 0) out.push_back({names[r], secs[r], cnt[r]});
+    static const bool per_sweep = std::getenv("LSKUM_KT_SWEEPS") != nullptr;  // probes: one line per sweep
+    static const char* sweeps[] = {"sweep0", "sweep1", "sweep2", "sweep3", "sweep4", "sweep5", "sweep6", "sweep7+"};
+    for (int k = KT_SWEEP; per_sweep && k < KT_FLUX; ++k) {
+      const KTimer& t = hctl_.get()->kt[k];
+      if (t.launches) out.push_back({sweeps[k - KT_SWEEP], t.total_ns * 1e-9, static_cast<std::int64_t>(t.launches)});
+    }
     return out;
   }
 
@@ -2660,6 +2722,15 @@ void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms) {
 void session_flush_l2(Session* s) {
   if (s->multi) s->multi->flush_l2();
   else s->dom->flush_l2();
+}
+double session_step_flushed(Session* s, bool kernel_events) {
+  if (s->multi) {
+    s->multi->flush_l2();
+    return session_iterate(s, 1);
+  }
+  const double ms = s->dom->step_flushed(kernel_events);
+  if (s->dom->failed()) throw s->dom->fault_in_run();
+  return ms;
 }
 
 __global__ void k_math_selftest(int fn, const double* in, long long n, double* ref, double* ours) {

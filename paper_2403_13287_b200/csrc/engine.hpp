@@ -78,6 +78,7 @@ std::uint64_t session_stream(const Session* s);
 void session_download(Session* s);
 void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms);
 void session_flush_l2(Session* s);
+double session_step_flushed(Session* s, bool kernel_events);  // L2 flush + one iteration; device ms of the iteration
 double engine_fp64_peak_tflops(int device);
 // Evaluates libdevice erf/exp (fn 0/1) and the engine's constant-table replicas.
 void engine_math_selftest(int fn, const double* in, std::int64_t n, double* ref, double* ours);

@@ -555,6 +555,14 @@ int lskum_b200_session_flush_l2(lskum_b200_session* s) {
   return guard([&] { lskb::session_flush_l2(s->session); });
 }
 
+int lskum_b200_session_step_flushed(lskum_b200_session* s, int kernel_events, double* device_ms) {
+  NONNULL(s);
+  return guard([&] {
+    const double ms = lskb::session_step_flushed(s->session, kernel_events != 0);
+    if (device_ms) *device_ms = ms;
+  });
+}
+
 int lskum_b200_fp64_peak(int device, double* tflops) {
   NONNULL(tflops);
   return guard([&] { *tflops = lskb::engine_fp64_peak_tflops(device); });

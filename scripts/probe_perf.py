@@ -2,6 +2,7 @@
 
   python scripts/probe_perf.py [side ...]            rect side x side clouds
   PROBE_NACA=4000x2500 python scripts/probe_perf.py   NACA 0012 O-clouds (n_wall x n_rings, comma list)
+  PROBE_FLUSH=1 ...                                    flush L2 before every timed iteration
 """
 import sys, time, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -20,10 +21,16 @@ for label, make in clouds:
         t0 = time.time()
         c = make()
         tg = time.time() - t0
-        cfg = L.Config(mach=0.85, aoa=1.0, order=order, iters=60, fp_mode=os.environ.get("PROBE_FP", "fast"))
+        cfg = L.Config(mach=0.85, aoa=1.0, order=order, iters=60, fp_mode=os.environ.get("PROBE_FP", "fast"),
+                       chunk=int(os.environ.get("PROBE_CHUNK", "16")))
         s = L.Session(c, cfg, capacity=60)
         s.iterate(10)
-        ms = s.iterate(40)
+        if os.environ.get("PROBE_FLUSH"):  # L2 flushed before every iteration (bench.py's headline timing)
+            ms = 0.0
+            for _ in range(40):
+                ms += s.step_flushed()
+        else:
+            ms = s.iterate(40)
         n = c.n
         k = s.kernels()
         print(json.dumps({"cloud": label, "n": n, "order": order, "fp": os.environ.get("PROBE_FP", "fast"),
