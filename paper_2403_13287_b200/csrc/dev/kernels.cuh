@@ -125,14 +125,13 @@ __device__ __forceinline__ void stencil_of(const Geo& g, int i, int& e0, int& k)
 }
 
 // Programmatic dependent launch: the iteration's kernels are launched with
-// programmatic stream serialisation, so each can be scheduled while its
-// predecessor drains; it waits here for the predecessor's completion (and
-// memory) before touching anything, then lets its own successor launch.
-// Without the launch attribute both are no-ops.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// programmatic stream serialisation, so each one's launch is processed while
+// its predecessor's last blocks drain; it waits here for the predecessor's
+// completion (and memory) before touching anything.  No explicit trigger:
+// the dependent launch fires as the predecessor's blocks exit (triggering at
+// block start measured slower — early dependents occupy SM slots).  Without
+// the launch attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
