@@ -1396,6 +1396,16 @@ class Domain {
     if (order_ == 2 && ((c * inner_) & 1)) b ^= 1;
   }
 
+  // Iterations per graph launch for an n-iteration call: an even divisor of
+  // n of at least chunk/2 when there is one (one graph, parities preserved,
+  // fewer nodes to instantiate than chunk + remainder), else `chunk`.
+  int run_chunk(int n) const {
+    if (n <= chunk_) return n;
+    for (int c = chunk_ & ~1; c >= std::max(2, chunk_ / 2); c -= 2)
+      if (n % c == 0) return c;
+    return chunk_;
+  }
+
   void set_diag(int it) { k_set_diag<<<1, 1, 0, st_>>>(ctl_.get(), it); }
 
   // Runs up to n iterations; stops early on a device error.  Returns the
@@ -1405,11 +1415,12 @@ class Domain {
     ck(cudaSetDevice(device_), "cudaSetDevice");
     set_diag(done_ + n - 1);
     const bool direct = !graphs_enabled();
+    const int chunk = run_chunk(n);
     // capture graphs before timing
     if (!direct) {
       int a = a_, b = b_, left = n;
       while (left > 0) {
-        const int c = std::min(chunk_, left);
+        const int c = std::min(chunk, left);
         graph_for(a, b, c);
         advance(a, b, c);
         left -= c;
@@ -1420,7 +1431,7 @@ class Domain {
     int left = n, issued = 0, waited = 0;
     bool failed = false;
     while (left > 0 && !failed) {
-      const int c = std::min(chunk_, left);
+      const int c = std::min(chunk, left);
       if (direct) {
         for (int k = 0; k < c; ++k) enqueue_iteration(a_, b_, k == c - 1);
       } else {
