@@ -47,6 +47,15 @@ int lskum_b200_surface_forces(const lskum_cloud* cloud, const lskum_config* cfg,
 /* validate_cloud (reference cloud.cpp:252-321) computed on `device` — the
  * screening lskum_run performs there; same report and
  * defective ids (ascending) as lskum_cloud_validate / _defective_ids. */
+/* Device numbering a run with config key reorder = mode (0 none, 1 hilbert,
+ * 2 auto, 3 rcm) uses: *permuted = 1 when the device holds the points in a
+ * locality order (Hilbert curve, or reverse Cuthill-McKee for rcm and auto);
+ * *lines_before / *lines_after = sampled 128-byte derivative-record lines the
+ * neighbours of 16 consecutive points touch, per point, in the cloud's own
+ * order and in the locality order (0 when not computed).
+ * Host-only (no device needed); cached on the cloud. */
+int lskum_b200_cloud_locality(lskum_cloud* cloud, int mode, double* lines_before, double* lines_after,
+                              int* permuted);
 int lskum_b200_cloud_validate_device(lskum_cloud* cloud, int device, lskum_validation* out, int32_t* ids,
                                      int32_t cap, int32_t* n_out);
 /* Synthetic NACA 0012 O-cloud (no reference counterpart, the

@@ -600,8 +600,9 @@ __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter
 // Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
 // major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
 __global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, const D4* res,
-                              const double* dt, double* out) {
+                              const double* dt, const int* gid, double* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = gid ? gid[i] : i;  // position in the store
     D4 qx, qy;
     dq_load(dq, i, qx, qy);
     const D4 v[5] = {prim[i], q[i], qx, qy, res[i]};
@@ -616,10 +617,10 @@ __global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const
     r[20] = dt[i];
     if (soa) {
 #pragma unroll
-      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(k) * n + i] = r[k];
+      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(k) * n + p] = r[k];
     } else {
 #pragma unroll
-      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(i) * 21 + k] = r[k];
+      for (int k = 0; k < 21; ++k) out[static_cast<size_t>(p) * 21 + k] = r[k];
     }
   }
 }
@@ -754,6 +755,23 @@ struct GeomView {
   const std::int32_t* gid = nullptr;                                      // n_loc or null
   std::int64_t nnz = 0;
 };
+
+GeomView view_of(const LocalGeom& g) {
+  GeomView v;
+  v.n_own = g.n_own;
+  v.n_loc = g.n_loc;
+  v.x = g.x.data();
+  v.y = g.y.data();
+  v.nx = g.nx.data();
+  v.ny = g.ny.data();
+  v.kind = g.kind.data();
+  v.off = g.off.data();
+  v.nbr = g.nbr.data();
+  v.part = g.part.data();
+  v.gid = g.gid.data();
+  v.nnz = static_cast<std::int64_t>(g.nbr.size());
+  return v;
+}
 
 GeomView view_of(const PointSet& ps, const std::vector<std::uint8_t>& part) {
   GeomView v;
@@ -970,6 +988,12 @@ class Domain {
   int n_loc() const { return n_loc_; }
   int device() const { return device_; }
   int global_of(int local) const { return gid_host_.empty() ? local : gid_host_[local]; }
+  // Local index of an owned cloud point (failure diagnostics; linear search).
+  int local_of(long long global) const {
+    if (gid_host_.empty()) return static_cast<int>(global);
+    const auto it = std::find(gid_host_.begin(), gid_host_.begin() + n_, static_cast<int>(global));
+    return it == gid_host_.begin() + n_ ? 0 : static_cast<int>(it - gid_host_.begin());
+  }
 
   // ---- stencil screening (validate_cloud) on the device-resident geometry ----
   Screening screen() {
@@ -1008,6 +1032,7 @@ class Domain {
     if (head.n_defective > 0) {
       ck(cudaMemcpy(out.defective.data(), bad.get(), sizeof(int) * head.n_defective, cudaMemcpyDeviceToHost),
          "D2H defective");
+      for (auto& p : out.defective) p = global_of(p);  // point ids of the cloud
       std::sort(out.defective.begin(), out.defective.end());
     }
     return out;
@@ -1080,11 +1105,13 @@ class Domain {
 
   void download(FieldBlock& f, bool with_q, const D4* qsrc, const D4* dqsrc) {
     const std::size_t n = static_cast<std::size_t>(n_);
-    if (with_q && gid_host_.empty()) {
-      // pack on the device in the host layout, one D2H into the FieldBlock
+    if (with_q && (gid_host_.empty() || (n_loc_ == n_ && static_cast<std::size_t>(f.size()) == n))) {
+      // pack on the device in the host layout (scattered to cloud order when
+      // the domain is a permutation of the whole cloud), one D2H into the store
       DBuf<double> packed(21 * n, st_);
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
-          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(), packed.get());
+          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(),
+          static_cast<const int*>(gid_.get()), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
       trace_sync(st_, "download: packed");
       // through pinned staging (full-rate D2H) in chunks; host threads copy
@@ -1581,7 +1608,7 @@ class Domain {
     if (phase == PH_RESIDUE)
       return Fault(Status::positivity, "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
     if (phase == PH_STALL) return Fault(Status::argument, "peer rank stopped making progress (wait timed out)");
-    const int li = local >= 0 ? local : static_cast<int>(point);
+    const int li = local >= 0 ? local : local_of(point);
     if (strict_)
       k_diagnose<true><<<1, 1, 0, st_>>>(geo(), qsrc, dqsrc, prim_.get(), dt_.get(), which_.get(), gas_, key, li,
                                          diag_.get());
@@ -1745,9 +1772,26 @@ class Domain {
 // ===========================================================================
 namespace {
 
+// A single-device domain of the whole cloud in the numbering `loc` chooses:
+// the cloud's own order, or its locality permutation (reorder.cpp).
+std::unique_ptr<Domain> cloud_domain(const PointSet& ps, const std::shared_ptr<const Locality>& loc,
+                                     const std::vector<std::uint8_t>& part_of, int device, double gamma,
+                                     double cfl, double det_tol, int capacity) {
+  if (loc->order.empty())
+    return std::make_unique<Domain>(view_of(ps, part_of), device, gamma, cfl, det_tol, capacity);
+  const LocalGeom g = permuted_geom(ps, loc->order, part_of);
+  trace("engine: locality permutation");
+  return std::make_unique<Domain>(view_of(g), device, gamma, cfl, det_tol, capacity);
+}
+
+std::shared_ptr<const Locality> locality_of(const PointSet& ps, int reorder) {
+  cloud_locality(ps, reorder);
+  return ps.locality;
+}
+
 std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
-  auto d = std::make_unique<Domain>(view_of(ps, spec.part_of), spec.device, spec.gamma, spec.cfl,
-                                    spec.det_tol, capacity);
+  auto d = cloud_domain(ps, locality_of(ps, spec.reorder), spec.part_of, spec.device, spec.gamma, spec.cfl,
+                        spec.det_tol, capacity);
   trace("engine: geometry uploaded");
   d->upload(ps.fields, false);
   trace("engine: state uploaded");
@@ -1762,11 +1806,19 @@ std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int ca
 struct EngineCache {
   std::unique_ptr<Domain> dom;
   int device = -1;
+  std::shared_ptr<const Locality> loc;  // device numbering the domain was built with
 };
+
+// The cached domain is reusable when it was built in the same numbering.
+bool same_numbering(const EngineCache& c, const std::shared_ptr<const Locality>& loc) {
+  return c.loc == loc || (c.loc && c.loc->order.empty() && loc->order.empty());
+}
+
 
 Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
   auto* c = static_cast<EngineCache*>(ps.engine_cache.get());
-  if (c && c->device == spec.device && c->dom) {
+  const std::shared_ptr<const Locality> loc = locality_of(ps, spec.reorder);
+  if (c && c->device == spec.device && c->dom && same_numbering(*c, loc)) {
     c->dom->reconfigure(spec.gamma, spec.cfl, spec.det_tol, spec.part_of.empty() ? nullptr : spec.part_of.data(),
                         capacity);
     trace("engine: cached domain reconfigured");
@@ -1774,8 +1826,8 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
     ps.engine_cache.reset();  // release the old device's buffers first
     auto fresh = std::make_shared<EngineCache>();
     fresh->device = spec.device;
-    fresh->dom = std::make_unique<Domain>(view_of(ps, spec.part_of), spec.device, spec.gamma, spec.cfl,
-                                          spec.det_tol, capacity);
+    fresh->loc = loc;
+    fresh->dom = cloud_domain(ps, loc, spec.part_of, spec.device, spec.gamma, spec.cfl, spec.det_tol, capacity);
     trace("engine: geometry uploaded");
     ps.engine_cache = fresh;
     c = fresh.get();
@@ -1793,13 +1845,15 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
 // lskum_run's stencil screening on the device: uploads the
 // geometry into the cloud's resident domain (which the run then reuses) and
 // screens it there.  The report is cached on the cloud like the host one.
-Screening engine_screen(PointSet& ps, int device, double gamma, double cfl, int capacity) {
+Screening engine_screen(PointSet& ps, int device, double gamma, double cfl, int capacity, int reorder) {
   auto* c = static_cast<EngineCache*>(ps.engine_cache.get());
-  if (!(c && c->device == device && c->dom)) {
+  const std::shared_ptr<const Locality> loc = locality_of(ps, reorder);
+  if (!(c && c->device == device && c->dom && same_numbering(*c, loc))) {
     ps.engine_cache.reset();
     auto fresh = std::make_shared<EngineCache>();
     fresh->device = device;
-    fresh->dom = std::make_unique<Domain>(view_of(ps, {}), device, gamma, cfl, 0.0, std::max(1, capacity));
+    fresh->loc = loc;
+    fresh->dom = cloud_domain(ps, loc, {}, device, gamma, cfl, 0.0, std::max(1, capacity));
     trace("engine: geometry uploaded");
     ps.engine_cache = fresh;
     c = fresh.get();
@@ -1811,7 +1865,7 @@ Screening engine_screen(PointSet& ps, int device, double gamma, double cfl, int 
 
 void engine_prescreen(PointSet& ps, const Settings& s) {
   if (ps.screening || s.gpus > 1) return;
-  ps.screening = std::make_shared<const Screening>(engine_screen(ps, s.device, s.gamma, s.cfl, s.iters));
+  ps.screening = std::make_shared<const Screening>(engine_screen(ps, s.device, s.gamma, s.cfl, s.iters, s.reorder));
 }
 
 namespace {
@@ -1921,22 +1975,6 @@ void enable_peers(const std::vector<int>& devs) {
     }
 }
 
-GeomView view_of(const LocalGeom& g) {
-  GeomView v;
-  v.n_own = g.n_own;
-  v.n_loc = g.n_loc;
-  v.x = g.x.data();
-  v.y = g.y.data();
-  v.nx = g.nx.data();
-  v.ny = g.ny.data();
-  v.kind = g.kind.data();
-  v.off = g.off.data();
-  v.nbr = g.nbr.data();
-  v.part = g.part.data();
-  v.gid = g.gid.data();
-  v.nnz = static_cast<std::int64_t>(g.nbr.size());
-  return v;
-}
 
 }  // namespace
 

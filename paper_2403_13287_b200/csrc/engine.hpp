@@ -21,6 +21,7 @@ struct EngineSpec {
   int chunk = 16;   // iterations per captured graph
   int device = 0;
   int gpus = 1;     // device domains (sessions; lskum_run decides in solve.cpp)
+  int reorder = 0;  // single-device numbering: kReorderNone / Hilbert / Auto (reorder.cpp)
   // Partition of each point (reference error tie-break, runtime.cpp:115-118).
   std::vector<std::uint8_t> part_of;
   // lskum_run's free-stream initialisation done on the device (single-domain
@@ -36,7 +37,8 @@ struct EngineSpec {
 // when the report is cached or gpus > 1).
 void engine_prescreen(PointSet& ps, const Settings& s);
 // The same report computed on `device` (kept resident in the cloud's cache).
-Screening engine_screen(PointSet& ps, int device, double gamma = 1.4, double cfl = 0.5, int capacity = 1);
+Screening engine_screen(PointSet& ps, int device, double gamma = 1.4, double cfl = 0.5, int capacity = 1,
+                        int reorder = 0);
 
 // Config check + stencil screening gate + bisection (host side of a run).
 EngineSpec prepare_run(const PointSet& ps, const Settings& s);
@@ -61,6 +63,10 @@ struct LocalGeom {
   std::vector<std::int32_t> halo_idx;    // n_loc - n_own
 };
 std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of);
+// The whole cloud as one domain in the given device order (reorder.cpp):
+// point k of the domain is point order[k] of the cloud; no halo.
+LocalGeom permuted_geom(const PointSet& ps, const std::vector<std::int32_t>& order,
+                        const std::vector<std::uint8_t>& part_of);
 
 // Multi-domain run: one Domain per RCB piece, devices assigned round-robin
 // from spec.device; halos exchanged by peer-memory gathers; residue summed

@@ -135,6 +135,18 @@ int lskum_cloud_validate(const lskum_cloud* cloud, lskum_validation* out) {
   });
 }
 
+int lskum_b200_cloud_locality(lskum_cloud* cloud, int mode, double* lines_before, double* lines_after,
+                              int* permuted) {
+  NONNULL(cloud);
+  if (mode < 0 || mode > 3) return fail(LSKUM_ERR_ARGUMENT, "reorder mode must be 0, 1, 2 or 3");
+  return guard([&] {
+    const lskb::Locality& loc = lskb::cloud_locality(cloud->ps, mode);
+    if (lines_before) *lines_before = loc.lines_before;
+    if (lines_after) *lines_after = loc.lines_after;
+    if (permuted) *permuted = loc.order.empty() ? 0 : 1;
+  });
+}
+
 int lskum_b200_cloud_validate_device(lskum_cloud* cloud, int device, lskum_validation* out, int32_t* ids,
                                      int32_t cap, int32_t* n_out) {
   if (!cloud || !out || !n_out || (cap > 0 && !ids)) return fail(LSKUM_ERR_ARGUMENT, "null argument");

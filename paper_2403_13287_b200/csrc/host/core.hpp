@@ -117,6 +117,8 @@ bool fields_identical(const FieldBlock& a, const FieldBlock& b);
 // Columnar point set + CSR stencils (reference cloud.hpp:37-74).
 struct Screening;
 
+struct Locality;
+
 struct PointSet {
   std::vector<double> x, y, nx, ny;
   std::vector<Kind> kind;
@@ -131,6 +133,8 @@ struct PointSet {
   }
   // Screening report of this (immutable) geometry, computed on first use.
   mutable std::shared_ptr<const Screening> screening;
+  // Device numbering chosen by the last run's reorder mode (reorder.cpp).
+  mutable std::shared_ptr<const Locality> locality;
   // Device-resident copy of this geometry kept between lskum_run calls (the
   // engine's single-device domain: geometry, weights, state buffers, CUDA
   // graphs); released with the cloud.
@@ -200,6 +204,7 @@ struct Settings {
   double outer_radius = 10.0;
   // B200 additions
   int device = 0, gpus = 1, fp_mode = 0, chunk = 16;
+  int reorder = 2;  // kReorderAuto (none | hilbert | rcm | auto)
 
   void check() const;  // ErrorCode::config on bad values (reference config.cpp:47-56)
   void set(const std::string& key, const std::string& value);
@@ -207,6 +212,21 @@ struct Settings {
   void load(const std::string& path);
 };
 PointSet acquire_points(const Settings& s);
+
+// ---- locality permutation of the device numbering (reorder.cpp) ----
+enum : int { kReorderNone = 0, kReorderHilbert = 1, kReorderAuto = 2, kReorderRcm = 3 };
+struct Locality {
+  int mode = kReorderNone;
+  std::vector<std::int32_t> order;   // device index k -> point id; empty: identity
+  double lines_before = 0.0, lines_after = 0.0;  // gather lines per point (sampled)
+};
+// Mean distinct 128-byte derivative-record lines touched by the neighbours of
+// 16 consecutive points in the given order (empty: the cloud's own).
+double gather_lines_per_point(const PointSet& ps, const std::vector<std::int32_t>& order);
+std::vector<std::int32_t> hilbert_order(const PointSet& ps);
+std::vector<std::int32_t> rcm_order(const PointSet& ps);
+// The cloud's device numbering for `mode`, cached on the cloud.
+const Locality& cloud_locality(const PointSet& ps, int mode);
 
 // ---- run results / reports (reference runtime.hpp:29-47, bench.cpp) ----
 struct KernelTime {

@@ -4,7 +4,7 @@
 // (config.cpp:10-162, lskum_capi.cpp:153-195): unknown keys and malformed
 // values raise ErrorCode::config, the file loader strips '#' comments and
 // blank lines, lskum_config_get renders reals with %.17g.  Additional keys
-// for the device backend: backend, device, gpus, fp_mode, chunk.
+// for the device backend: backend, device, gpus, fp_mode, chunk, reorder.
 #include <cerrno>
 #include <charconv>
 #include <cstdio>
@@ -114,7 +114,13 @@ void Settings::set(const std::string& key, const std::string& v) {
     else if (v == "strict") fp_mode = 1;
     else raise(Status::config, "unknown fp_mode '" + v + "' (expected fast or strict)");
   } else if (key == "chunk") chunk = static_cast<int>(int_value(key, v));
-  else raise(Status::config, "unknown config key '" + key + "'");
+  else if (key == "reorder") {
+    if (v == "none") reorder = 0;
+    else if (v == "hilbert") reorder = 1;
+    else if (v == "auto") reorder = 2;
+    else if (v == "rcm") reorder = 3;
+    else raise(Status::config, "unknown reorder '" + v + "' (expected none, hilbert, rcm or auto)");
+  } else raise(Status::config, "unknown config key '" + key + "'");
 }
 
 std::string Settings::get(const std::string& key) const {
@@ -144,6 +150,10 @@ std::string Settings::get(const std::string& key) const {
   if (key == "gpus") return std::to_string(gpus);
   if (key == "fp_mode") return fp_mode ? "strict" : "fast";
   if (key == "chunk") return std::to_string(chunk);
+  if (key == "reorder") {
+    static const char* names[] = {"none", "hilbert", "auto", "rcm"};
+    return names[reorder & 3];
+  }
   raise(Status::config, "unknown config key '" + key + "'");
 }
 

@@ -34,6 +34,7 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
   spec.chunk = s.chunk;
   spec.device = s.device;
   spec.gpus = s.gpus;
+  spec.reorder = s.reorder;
   if (s.parts > ps.n())
     raise(Status::argument, "more partitions than points (" + std::to_string(s.parts) + " > " +
                                 std::to_string(ps.n()) + ")");
