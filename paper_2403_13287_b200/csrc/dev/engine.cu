@@ -925,6 +925,9 @@ class Domain {
     psz_.alloc(8192, st_);
     ctl_.alloc(1, st_);
     sh_.alloc(1, shared_st);
+    // whole words defined (refresh_ctl copies them back, padding included)
+    ck(cudaMemsetAsync(ctl_.get(), 0, sizeof(Ctl), st_), "memset ctl");
+    ck(cudaMemsetAsync(sh_.get(), 0, sizeof(Shared), st_), "memset shared");
     shared_ = sh_.get();
     diag_.alloc(8, st_);
     capacity_ = std::max(capacity, 1);

@@ -642,6 +642,8 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
   if (g.kind[i] == KIND_OUTER) {
     if (w1)
       for (int j = 0; j < k; ++j) w1[e0 + j] = make_double2(0.0, 0.0);
+    if (psign)
+      for (int j = 0; j < k; ++j) psign[e0 + j] = 0;
     if (sing) sing[i] = 0xFF;
     return;
   }
