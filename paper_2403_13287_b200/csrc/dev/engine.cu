@@ -2305,7 +2305,7 @@ class RankRun {
       : ps_(ps), spec_(spec), rank_(rank), world_(world), device_(device) {
     if (world < 1 || world > kMaxDomains || rank < 0 || rank >= world)
       raise(Status::argument, "rank/world out of range");
-    geoms_ = decompose(ps, world, spec.part_of);
+    geoms_ = decompose(ps, world, spec.part_of, spec.reorder);
     spi_ = (spec.order == 2 ? spec.inner : 0) + 4;
     const LocalGeom& g = geoms_[rank];
     dom_ = std::make_unique<Domain>(view_of(g), device, spec.gamma, spec.cfl, spec.det_tol, capacity, true);
@@ -2738,7 +2738,7 @@ Session* session_open(PointSet& ps, const EngineSpec& spec, int capacity) {
   auto s = std::make_unique<Session>();
   s->ps = &ps;
   if (spec.gpus > 1) {
-    s->multi = std::make_unique<MultiRun>(ps, spec, decompose(ps, spec.gpus, spec.part_of), capacity);
+    s->multi = std::make_unique<MultiRun>(ps, spec, decompose(ps, spec.gpus, spec.part_of, spec.reorder), capacity);
     if (s->multi->failed()) throw s->multi->fault();
   } else {
     s->dom = open_domain(ps, spec, capacity);

@@ -62,7 +62,8 @@ struct LocalGeom {
   std::vector<std::int32_t> halo_dom;    // n_loc - n_own
   std::vector<std::int32_t> halo_idx;    // n_loc - n_own
 };
-std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of);
+std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of,
+                                 int reorder = 0);
 // The whole cloud as one domain in the given device order (reorder.cpp):
 // point k of the domain is point order[k] of the cloud; no halo.
 LocalGeom permuted_geom(const PointSet& ps, const std::vector<std::int32_t>& order,

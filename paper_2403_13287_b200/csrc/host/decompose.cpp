@@ -1,7 +1,8 @@
 // decompose.cpp — RCB pieces -> device domains with halo maps.
 //
 // Each piece of bisect_cloud (the reference's partition_cloud, bit-exact) becomes
-// one device domain: its owned points in ascending global id, then its halo
+// one device domain: its owned points in ascending global id (or in the
+// cloud's locality order, config key reorder), then its halo
 // (stencil closure minus owned, ascending) as read-only copies.  Stencils are
 // rewritten to local ids in the original (ascending global id) order, so every
 // per-point sum keeps the reference's operation order and results do not
@@ -14,9 +15,19 @@
 
 namespace lskb {
 
-std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of) {
-  const std::vector<Piece> pieces = bisect_cloud(ps, n_domains);
+std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of,
+                                 int reorder) {
+  std::vector<Piece> pieces = bisect_cloud(ps, n_domains);
   const std::int32_t n = ps.n();
+  // Locality numbering (reorder.cpp): each domain's owned points follow the
+  // cloud's locality order instead of ascending id.
+  const Locality& loc = cloud_locality(ps, reorder);
+  if (!loc.order.empty()) {
+    std::vector<std::int32_t> rank(static_cast<std::size_t>(n));
+    for (std::int32_t k = 0; k < n; ++k) rank[loc.order[k]] = k;
+    for (Piece& pc : pieces)
+      std::sort(pc.owned.begin(), pc.owned.end(), [&](std::int32_t a, std::int32_t b) { return rank[a] < rank[b]; });
+  }
   std::vector<std::int32_t> owner(static_cast<std::size_t>(n)), owner_local(static_cast<std::size_t>(n));
   for (std::size_t d = 0; d < pieces.size(); ++d)
     for (std::size_t k = 0; k < pieces[d].owned.size(); ++k) {

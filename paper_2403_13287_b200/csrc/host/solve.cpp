@@ -105,7 +105,7 @@ RunRecord solve_on_device(PointSet& ps, const Settings& s) {
   const EngineSpec spec = prepare_run(ps, s);
   if (s.gpus > 1) {
     if (s.gpus > ps.n()) raise(Status::config, "more gpus than points");
-    const std::vector<LocalGeom> geoms = decompose(ps, s.gpus, spec.part_of);
+    const std::vector<LocalGeom> geoms = decompose(ps, s.gpus, spec.part_of, spec.reorder);
     trace("prepare: decomposed");
     return engine_run_multi(ps, spec, geoms);
   }

@@ -145,3 +145,43 @@ def test_session_on_permuted_domain_equals_run(bump_cloud_arrays):
         assert np.array_equal(s.residues(), rw.residues())
         s.download()
     assert pc.fields_equal(whole)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_multi_domain_locality_numbering_is_bitwise(bump_cloud_arrays, gpus):
+    """Multi-domain runs order each domain's owned points by the cloud's
+    locality order (reorder=rcm/hilbert/auto); results stay bitwise those of
+    the single-domain run in cloud order."""
+    c, prim0 = bump_cloud_arrays
+    base, rb = bump_run(c, prim0, 25, reorder="none")
+    for mode in ("rcm", "hilbert"):
+        other, ro = bump_run(c, prim0, 25, gpus=gpus, reorder=mode)
+        assert np.array_equal(ro.residues(), rb.residues()), mode
+        assert other.fields_equal(base), mode
+
+
+@pytest.mark.gpu
+def test_ranks_on_shuffled_cloud_use_locality_numbering():
+    """Per-rank domains of a shuffled cloud (reorder=auto -> RCM inside each
+    RCB piece) give the single-domain run's bits."""
+    import rank_worker as W
+
+    c = shuffled(naca(80, 30))
+    g = c.geometry()
+    arrays = (g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"])
+    assert c.locality("auto")["permuted"]
+    pc = L.Cloud.from_arrays(*arrays)
+    pc.reset_store(0)
+    cfg = dict(mach=0.85, aoa=1.0, iters=8, inner=3, cfl=0.5, order=2)
+    rng = np.random.default_rng(3)  # perturbed free stream: a non-trivial transient
+    prim0 = np.tile([1.0, 0.85, 0.01, 1.0 / 1.4], (c.n, 1))
+    prim0[:, [0, 3]] *= 1.0 + 1e-4 * rng.standard_normal((c.n, 2))
+    pc.set_primitives(prim0)
+    want = L.run_fixed_point(pc, L.Config(reorder="none", **cfg))
+    out = W.launch(W.run_rank, 2, arrays, prim0, dict(cfg, reorder="auto"), [3, 5], 0)
+    assert all(v[0] == "ok" for v in out), out
+    assert np.array_equal(out[0][1], want.residues()) and want.residues()[-1] > 0.0
+    owned, _ = L.partition(L.Cloud.from_arrays(*arrays), 2)
+    for r, v in enumerate(out):
+        assert np.array_equal(v[2][owned[r]], pc.fields()[owned[r]]), r
