@@ -344,7 +344,8 @@ def large_run(L, a, counts):
 CONFIG_SIZES = [("configs[0] ~40K, M=0.63 AoA=2", "260x154", 0.63, 2.0),
                 ("configs[1] ~160K, M=0.85 AoA=1", "520x308", 0.85, 1.0),
                 ("configs[2] ~625K, M=1.2 AoA=0", "1000x625", 1.2, 0.0),
-                ("configs[3] ~10M, M=0.85 AoA=1", "4000x2500", 0.85, 1.0)]
+                ("configs[3] ~10M, M=0.85 AoA=1", "4000x2500", 0.85, 1.0),
+                ("configs[4] ~40M, M=0.85 AoA=1", "8000x5000", 0.85, 1.0)]
 
 
 def sizes_run(L, a, iters=40):
