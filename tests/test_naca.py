@@ -109,16 +109,17 @@ def test_rejects_bad_arguments():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("order,iters", [(1, 60), (2, 20)])
-def test_frozen_naca_run_matches_oracle(naca, order, iters):
+@pytest.mark.parametrize("mach,aoa", [(0.63, 2.0), (0.85, 1.0), (1.2, 0.0)])  # BASELINE configs[0..2]
+def test_frozen_naca_run_matches_oracle(naca, order, iters, mach, aoa):
     g = naca.geometry()
     c = P.Cloud(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"])
-    prim0 = P.center_bump(c, mach=0.85, aoa=1.0)
-    want = P.orc_run(c, mach=0.85, aoa=1.0, iters=iters, order=order, prim0=prim0)
+    prim0 = P.center_bump(c, mach=mach, aoa=aoa)
+    want = P.orc_run(c, mach=mach, aoa=aoa, iters=iters, order=order, prim0=prim0)
     assert want.code == 0, want.msg
     pc = L.Cloud.from_arrays(c.x, c.y, c.kind, c.nx, c.ny, c.off, c.nbr)
     pc.reset_store(0)
     pc.set_primitives(prim0)
-    res = L.run_fixed_point(pc, L.Config(mach=0.85, aoa=1.0, iters=iters, order=order, inner=3, cfl=0.5))
+    res = L.run_fixed_point(pc, L.Config(mach=mach, aoa=aoa, iters=iters, order=order, inner=3, cfl=0.5))
     got = res.residues()
     assert float(np.max(np.abs(got - want.residue) / np.abs(want.residue))) <= 1e-10
     assert rel_err(pc.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-12
