@@ -1,3 +1,6 @@
+# Round-end measurement: bench line + ncu --set full of the flux, sweep and update kernels at
+# 10M points + the ncu launch list of a short bench (run under gpurun; outputs in gpurun_out/,
+# summarised into profiles/ by scripts/ncu_summary.py and scripts/sass_mix.py).
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 export PROBE_NACA=4000x2500 PROBE_ORDERS=2
