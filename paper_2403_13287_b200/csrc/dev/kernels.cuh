@@ -687,6 +687,7 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
 // reconstructions, the x and y split fluxes of each side (the pair's half
 // stencils), acc += w . dG.  Warp-convergent (inactive lanes evaluate their
 // own point with zero offsets and add nothing).
+template <int HP = -1>
 __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, bool act, double2 pi,
                                                const D4& qi, const D4& qxi, const D4& qyi, double2 pn,
                                                const D4& qn, const D4& qxn, const D4& qyn, double2 w,
@@ -706,7 +707,7 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
     tn[3] = -1.0;
   }
   FluxState fi, fn;
-  ok = reconstruct2<false>(ti, tn, a.gas, fi, fn) && ok;
+  ok = reconstruct2<false, HP>(ti, tn, a.gas, fi, fn) && ok;
   if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
   AxisTerms at[4];
   axis_terms4<false>(fi, fn, at);
@@ -1003,7 +1004,7 @@ __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1
   }
 }
 
-template <int MB, int NW = kFluxWarps>
+template <int MB, int NW = kFluxWarps, int HP = -1>
 __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
                                                      const double2* __restrict__ w2,
                                                      const std::uint8_t* __restrict__ sing) {
@@ -1051,7 +1052,7 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       if (cur.live && lane == 0 && cur.sing != 0xFF)
         raise_err(a.ctl, err_key(PH_FLUX, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      flux_pair_fast(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
+      flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
                      D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
                      D4{y01.x, y01.y, y23.x, y23.y}, w, w2 + cur.e, acc);

@@ -138,3 +138,23 @@ def test_frozen_trailing_edge_points_are_valid_boundary_points(tmp_path):
     path = str(tmp_path / "naca.grid")
     c.write_file(path)
     assert L.Cloud.read_file(path).validate()["n_defective"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gamma", [1.4, 1.3, 5.0 / 3.0])
+def test_gas_constant_paths_match_oracle(naca, gamma):
+    """The density power 2/(gamma-1): 5 (gamma 1.4, the compile-time
+    specialised flux kernel), 6.67 (gamma 1.3, logarithm path) and 3
+    (gamma 5/3, integer power) against the oracle."""
+    g = naca.geometry()
+    c = P.Cloud(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"])
+    prim0 = P.center_bump(c, mach=0.85, aoa=1.0)
+    want = P.orc_run(c, mach=0.85, aoa=1.0, gamma=gamma, iters=15, order=2, prim0=prim0)
+    assert want.code == 0, want.msg
+    pc = L.Cloud.from_arrays(c.x, c.y, c.kind, c.nx, c.ny, c.off, c.nbr)
+    pc.reset_store(0)
+    pc.set_primitives(prim0)
+    res = L.run_fixed_point(pc, L.Config(mach=0.85, aoa=1.0, gamma=gamma, iters=15, order=2, inner=3, cfl=0.5))
+    got = res.residues()
+    assert float(np.max(np.abs(got - want.residue) / np.abs(want.residue))) <= 1e-10
+    assert rel_err(pc.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-12
