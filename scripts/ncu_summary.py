@@ -68,8 +68,8 @@ def main():
         json.dump({"source": os.path.basename(report), "n_points": n,
                    "flux_fp64_flops_per_point": flops, "flux_dram_bytes_per_point": dram / n,
                    "flux_fp64_thread_inst_per_point": fp,
-                   "note": "dynamic counts of k_flux from one ncu --set full capture "
-                           "(rect cloud, order 2; n_points above); flops = 2*DFMA + DADD + DMUL"},
+                   "note": "dynamic counts of the flux kernel from one ncu --set full capture "
+                           "(NACA 0012 O-cloud, order 2; n_points above); flops = 2*DFMA + DADD + DMUL"},
                   open(path, "w"), indent=1)
         print("wrote", path)
 
