@@ -168,7 +168,7 @@ __device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int 
 // ---- per-kernel device timing (globaltimer) ----
 // Each launch marks its slot with fire-and-forget atomics: first block start
 // (min) and last block end (max).  k_tree_final, the iteration's last kernel,
-// folds the slots into totals and resets them (ktimer_fold) — no fences or
+// folds the slots into totals and resets them (ktimer_fold_warp) — no fences or
 // completion counters in the kernels' tails.
 __device__ __forceinline__ void ktimer_begin(Ctl* ctl, int k) {
   if (threadIdx.x == 0) atomicMin(&ctl->kt[k].t0, globaltimer());
@@ -177,18 +177,27 @@ __device__ __forceinline__ void ktimer_begin(Ctl* ctl, int k) {
 __device__ __forceinline__ void ktimer_end(Ctl* ctl, int k, unsigned long long* = nullptr) {
   if (threadIdx.x == 0) atomicMax(&ctl->kt[k].t1, globaltimer());
 }
-// Folds every marked slot (single thread); returns the earliest start of the
-// iteration's kernels (slots other than q_variables).
-__device__ __forceinline__ unsigned long long ktimer_fold(Ctl* ctl) {
+// Folds every marked slot into its totals and resets it; one lane per slot
+// (call with the whole first warp; the slots' loads are then in flight
+// together instead of one slot after another).  Returns, in every lane, the
+// earliest start of the iteration's kernels (slots other than q_variables).
+__device__ __forceinline__ unsigned long long ktimer_fold_warp(Ctl* ctl) {
+  const int lane = threadIdx.x & 31;
   unsigned long long first = ~0ull;
-  for (int k = 0; k < KT_COUNT; ++k) {
-    KTimer& t = ctl->kt[k];
-    if (t.t1 == 0 || t.t0 == ~0ull) continue;
-    if (k != KT_QVAR && t.t0 < first) first = t.t0;
-    t.total_ns += t.t1 > t.t0 ? t.t1 - t.t0 : 0;
-    t.launches += 1;
-    t.t0 = ~0ull;
-    t.t1 = 0;
+  if (lane < KT_COUNT) {
+    KTimer& t = ctl->kt[lane];
+    const unsigned long long t0 = t.t0, t1 = t.t1;
+    if (!(t1 == 0 || t0 == ~0ull)) {
+      if (lane != KT_QVAR) first = t0;
+      t.total_ns += t1 > t0 ? t1 - t0 : 0;
+      t.launches += 1;
+      t.t0 = ~0ull;
+      t.t1 = 0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xFFFFFFFFu, first, o);
+    first = v < first ? v : first;
   }
   return first;
 }
@@ -1358,15 +1367,18 @@ __device__ __forceinline__ void tree_final(const double* part_val, const long lo
   if (threadIdx.x == 0) *s_skip = skip_stage(ctl, sub_residue(ctl), 1);
   __syncthreads();
   if (*s_skip) {
-    if (threadIdx.x == 0) ktimer_fold(ctl);
+    if (threadIdx.x < 32) ktimer_fold_warp(ctl);
     return;
   }
   const int lv = tree_load_partials<LV>(part_val, part_sz, d1, sv[0], ss[0]);
   __syncthreads();
   tree_combine<T>(sv[0], ss[0], sv[1], ss[1], lv);
+  __shared__ int s_it, s_ok;
   if (threadIdx.x == 0) {
     const double res = sqrt(sv[0][0]) / static_cast<double>(n);
     const int it = iter_of(ctl, 1);
+    s_it = it;
+    s_ok = isfinite(res) ? 1 : 0;
     if (!isfinite(res)) {
       raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0), sub_residue(ctl), 1);
     } else {
@@ -1375,8 +1387,11 @@ __device__ __forceinline__ void tree_final(const double* part_val, const long lo
       ctl->sh->iter = it + 1;  // iterations completed (residue recorded)
     }
     atomicMax(&ctl->kt[KT_RESIDUE].t1, globaltimer());
-    const unsigned long long t0 = ktimer_fold(ctl);
-    if (iter_t0 && !(res != res) && isfinite(res)) iter_t0[it] = t0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned long long t0 = ktimer_fold_warp(ctl);
+    if (threadIdx.x == 0 && iter_t0 && s_ok) iter_t0[s_it] = t0;
   }
 }
 
