@@ -1141,6 +1141,7 @@ class Domain {
            "D2H fields");
         ck(cudaEventRecord(done[c], st_), "cudaEventRecord");
       }
+      trace("download: copies queued");
       parallel_slices(chunks, [&](std::int64_t a, std::int64_t b) {
         for (std::int64_t c = a; c < b; ++c) {
           cudaEventSynchronize(done[c]);
@@ -1149,6 +1150,7 @@ class Domain {
           flush_lines(h + lo, (hi - lo) * sizeof(double));  // the next DMA into staging stays at full rate
         }
       }, 1);
+      trace("download: copied out");
       ck(cudaStreamSynchronize(st_), "download");
       trace("download: stored");
       for (cudaEvent_t e : done) cudaEventDestroy(e);

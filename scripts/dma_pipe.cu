@@ -28,14 +28,31 @@ static void nt_copy(char* dst, const char* src, size_t n) {
   std::memcpy(dst + i, src + i, n - i);
   _mm_sfence();
 }
+// streaming (MOVNTDQA) loads from write-combined memory, NT stores out
+__attribute__((target("sse4.1"))) static void nt_load_copy(char* dst, const char* src, size_t n) {
+  size_t i = 0;
+  for (; i + 64 <= n; i += 64) {
+    __m128i a = _mm_stream_load_si128((__m128i*)(src + i));
+    __m128i b = _mm_stream_load_si128((__m128i*)(src + i + 16));
+    __m128i c = _mm_stream_load_si128((__m128i*)(src + i + 32));
+    __m128i d = _mm_stream_load_si128((__m128i*)(src + i + 48));
+    _mm_stream_si128((__m128i*)(dst + i), a);
+    _mm_stream_si128((__m128i*)(dst + i + 16), b);
+    _mm_stream_si128((__m128i*)(dst + i + 32), c);
+    _mm_stream_si128((__m128i*)(dst + i + 48), d);
+  }
+  std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
 static void flush(char* p, size_t n) {
   for (size_t i = 0; i < n; i += 64) _mm_clflushopt(p + i);
   _mm_sfence();
 }
 
 int main() {
-  char *h, *d;
+  char *h, *d, *hwc;
   cudaHostAlloc((void**)&h, N, 0);
+  cudaHostAlloc((void**)&hwc, N, cudaHostAllocWriteCombined);
   cudaMalloc((void**)&d, N);
   cudaMemset(d, 1, N);
   char* store = (char*)aligned_alloc(64, N);
@@ -43,7 +60,8 @@ int main() {
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   const int T = 16;
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 6; ++mode) {
+    char* hb = mode >= 4 ? hwc : h;
     for (int chunks : {1, 4, 8, 16, 32, 64}) {
       double best = 1e9, sum = 0;
       for (int rep = 0; rep < 7; ++rep) {
@@ -53,7 +71,7 @@ int main() {
         for (int c = 0; c < chunks; ++c) {
           size_t lo = (N * c / chunks) & ~size_t(63), hi = c == chunks - 1 ? N : (N * (c + 1) / chunks) & ~size_t(63);
           cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
-          cudaMemcpyAsync(h + lo, d + lo, hi - lo, cudaMemcpyDeviceToHost, st);
+          cudaMemcpyAsync(hb + lo, d + lo, hi - lo, cudaMemcpyDeviceToHost, st);
           cudaEventRecord(ev[c], st);
         }
         std::atomic<int> next{0};
@@ -64,7 +82,9 @@ int main() {
             size_t lo = (N * c / chunks) & ~size_t(63), hi = c == chunks - 1 ? N : (N * (c + 1) / chunks) & ~size_t(63);
             cudaEventSynchronize(ev[c]);
             if (mode == 0 || mode == 1) std::memcpy(store + lo, h + lo, hi - lo);
-            else nt_copy(store + lo, h + lo, hi - lo);
+            else if (mode == 2 || mode == 3) nt_copy(store + lo, h + lo, hi - lo);
+            else if (mode == 4) nt_load_copy(store + lo, hwc + lo, hi - lo);
+            else std::memcpy(store + lo, hwc + lo, hi - lo);
             if (mode == 1 || mode == 3) flush(h + lo, hi - lo);
           }
         };
@@ -76,7 +96,7 @@ int main() {
         for (auto e : ev) cudaEventDestroy(e);
         if (rep >= 2) { best = std::min(best, ms); sum += ms; }
       }
-      const char* names[] = {"memcpy", "memcpy+flush", "NT", "NT+flush"};
+      const char* names[] = {"memcpy", "memcpy+flush", "NT", "NT+flush", "WC+ntload", "WC+memcpy"};
       std::printf("%-13s chunks %2d: best %.3f ms  mean %.3f ms\n", names[mode], chunks, best, sum / 5);
     }
   }
