@@ -737,7 +737,8 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
   // a zero offset belongs to both half stencils: add the minus direction
-  if (__any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
+  // (w2e null: the stencil table has no zero offset — k_flux_weights' count)
+  if (w2e != nullptr && __any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
     const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? *w2e : make_double2(0.0, 0.0);
     split_flux_fast<0>(fi, at[0], true, epi, kki, gi);
     split_flux_fast<0>(fn, at[1], true, epn, kkn, gn);
@@ -813,7 +814,8 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       const D4 qn = ld4(a.q + nb);
       D4 qxn, qyn;
       dq_load(a.dq, nb, qxn, qyn);
-      flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 + (e0 + j), acc);
+      flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 ? w2 + (e0 + j) : nullptr,
+                     acc);
     }
     const double r = reduce8(acc, lane);
     if (live) store_res8(a.res, i, r, lane);
@@ -1064,7 +1066,7 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
                      D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
-                     D4{y01.x, y01.y, y23.x, y23.y}, w, w2 + cur.e, acc);
+                     D4{y01.x, y01.y, y23.x, y23.y}, w, w2 ? w2 + cur.e : nullptr, acc);
       const double r = reduce8(acc, lane);
       if (cur.live) store_res8(a.res, cur.i, r, lane);
       __syncwarp();  // the stage is refilled two groups on
