@@ -433,20 +433,21 @@ bool flux_staged() {
 }
 
 // Block shape of the staged flux kernel: LSKUM_FLUX_WS = "<warps>x<blocks/SM>"
-// (4x4 default: 16 warps/SM in 128-thread blocks, 4% faster at 10M points than
-// 8x2; 8x3, 4x5, 6x3 spill and are slower).
-int flux_ws_shape() {
+// (default by size, both 16 warps/SM: 4x4 below 512K owned points — finer
+// blocks balance the short 160K-point launch better — and 8x2 above, 0.8-1.6%
+// faster from 625K to 10M points; 8x3, 4x5, 6x3 spill and are slower).
+int flux_ws_shape(int n) {
   static int v = [] {
     const char* e = std::getenv("LSKUM_FLUX_WS");
-    const std::string s = e ? e : "4x4";
+    const std::string s = e ? e : "";
     if (s == "8x2") return 82;
     if (s == "8x3") return 83;
     if (s == "4x4") return 44;
     if (s == "4x5") return 45;
     if (s == "6x3") return 63;
-    return 44;
+    return 0;
   }();
-  return v;
+  return v ? v : (n >= (1 << 19) ? 82 : 44);
 }
 
 // The staged flux kernel, instantiated for gamma = 1.4 (2/(gamma-1) = 5 at
@@ -482,7 +483,7 @@ void flux_w_launch(const FluxArgs& a, int kmax, const double2* w1, const double2
                    cudaStream_t st) {
   const int groups = (a.g.n + 3) / 4;
   if (kmax <= 8 && flux_staged()) {
-    switch (flux_ws_shape()) {
+    switch (flux_ws_shape(a.g.n)) {
       case 83: flux_ws_launch<3, 8>(a, w1, w2, sing, st); break;
       case 44: flux_ws_launch<4, 4>(a, w1, w2, sing, st); break;
       case 45: flux_ws_launch<5, 4>(a, w1, w2, sing, st); break;
