@@ -12,6 +12,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -511,9 +512,9 @@ int tree_depth(long long n) {
 template <bool S>
 __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, const double* uval,
                            const double* uwhich, Gas gas, unsigned long long key, int i, double* out) {
-  const unsigned phase = static_cast<unsigned>(key >> 61);
-  const unsigned dir = static_cast<unsigned>((key >> 20) & 3ull);
-  const unsigned j = static_cast<unsigned>(key & 0xFFFFFull);
+  const unsigned phase = key_phase(key);
+  const unsigned dir = key_dir(key);
+  const unsigned j = key_j(key);
   for (int t = 0; t < 6; ++t) out[t] = 0.0;
   if (phase == PH_RESIDUE) return;
   if (phase == PH_QVAR) {
@@ -585,8 +586,10 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
 
 // Resets this domain's timers, points it at the run's shared word and (for
 // the domain that owns it) resets that word.
-__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, int spi, int upd_blocks) {
+__global__ void k_ctl_init(Ctl* ctl, Shared* sh, int own_shared, int diag_iter, int spi, int upd_blocks,
+                           int split4 = 0) {
   ctl->sh = sh;
+  ctl->split4 = split4;
   ctl->diag_iter = diag_iter;
   ctl->spi = spi;
   ctl->upd_blocks = upd_blocks > 0 ? upd_blocks : 1;
@@ -762,7 +765,7 @@ struct GeomView {
   const Kind* kind = nullptr;                                             // n_loc
   const std::int64_t* off = nullptr;                                      // n_own + 1
   const std::int32_t* nbr = nullptr;                                      // local ids
-  const std::uint8_t* part = nullptr;                                     // n_loc or null
+  const std::uint16_t* part = nullptr;                                    // n_loc or null
   const std::int32_t* gid = nullptr;                                      // n_loc or null
   std::int64_t nnz = 0;
 };
@@ -784,7 +787,7 @@ GeomView view_of(const LocalGeom& g) {
   return v;
 }
 
-GeomView view_of(const PointSet& ps, const std::vector<std::uint8_t>& part) {
+GeomView view_of(const PointSet& ps, const std::vector<std::uint16_t>& part) {
   GeomView v;
   v.n_own = v.n_loc = ps.n();
   v.x = ps.x.data();
@@ -838,13 +841,13 @@ class Domain {
     const std::size_t b_xy = nl * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
     const std::size_t b_gid = gv.gid ? nl * sizeof(int) : 0;
     trace("domain: pool");
-    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 2 * nl + b_off + b_nbr + b_gid + 64));
+    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 3 * nl + b_off + b_nbr + b_gid + 64));
     trace("domain: staging buffer");
     double2* hxy = reinterpret_cast<double2*>(hs);
     double2* hnrm = hxy + nl;
-    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hnrm + nl);
-    std::uint8_t* hpart = hkind + nl;
-    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 2 * nl + 15) & ~std::size_t{15}));
+    std::uint16_t* hpart = reinterpret_cast<std::uint16_t*>(hnrm + nl);
+    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hpart + nl);
+    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 3 * nl + 15) & ~std::size_t{15}));
     int* hnbr = hoff + n + 1;
     int* hgid = hnbr + nnz;
     // One pass over the cloud on the host threads: stencil-size scan (kmax,
@@ -864,7 +867,7 @@ class Domain {
         hpart[i] = gv.part ? gv.part[i] : 0;
       }
       flush_lines(hkind + lo, c);
-      flush_lines(hpart + lo, c);
+      flush_lines(hpart + lo, c * sizeof(std::uint16_t));
       const std::size_t olo = part_of(n, t), ohi = part_of(n, t + 1);
       std::int64_t km = 1;
       bool uni = true;
@@ -888,6 +891,8 @@ class Domain {
       uniform = uniform && t_uniform[t];
     }
     kmax_ = static_cast<int>(km);
+    if (kmax_ > kMaxStencil)
+      raise(Status::argument, "stencils of more than " + std::to_string(kMaxStencil) + " neighbours are not supported");
     kfix_ = uniform && k0 == km ? kmax_ : 0;
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
@@ -910,7 +915,7 @@ class Domain {
     trace_sync(st_, "domain: xy copied");
     ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
     ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
-    ck(cudaMemcpyAsync(part_.get(), hpart, nl, cudaMemcpyHostToDevice, st_), "H2D part");
+    ck(cudaMemcpyAsync(part_.get(), hpart, nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_), "H2D part");
     part_host_.assign(hpart, hpart + nl);
     ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
     trace_sync(st_, "domain: nrm kind part off copied");
@@ -1144,15 +1149,25 @@ class Domain {
         ck(cudaEventRecord(done[c], st_), "cudaEventRecord");
       }
       trace("download: copies queued");
+      std::atomic<int> sync_err{0};
       parallel_slices(chunks, [&](std::int64_t a, std::int64_t b) {
         for (std::int64_t c = a; c < b; ++c) {
-          cudaEventSynchronize(done[c]);
+          const cudaError_t e = cudaEventSynchronize(done[c]);
+          if (e != cudaSuccess) {  // never copy stale staging bytes into the store
+            int none = 0;
+            sync_err.compare_exchange_strong(none, static_cast<int>(e));
+            continue;
+          }
           const std::size_t lo = lo_of(c), hi = lo_of(c + 1);
           std::memcpy(dst + lo, h + lo, (hi - lo) * sizeof(double));
           flush_lines(h + lo, (hi - lo) * sizeof(double));  // the next DMA into staging stays at full rate
         }
       }, 1);
       trace("download: copied out");
+      if (sync_err.load() != 0) {
+        for (cudaEvent_t e : done) cudaEventDestroy(e);
+        ck(static_cast<cudaError_t>(sync_err.load()), "download (copy-back event)");
+      }
       ck(cudaStreamSynchronize(st_), "download");
       trace("download: stored");
       for (cudaEvent_t e : done) cudaEventDestroy(e);
@@ -1216,7 +1231,7 @@ class Domain {
     ck(cudaMemsetAsync(res_.get(), 0, n * sizeof(D4), st_), "zero res");
     ck(cudaMemsetAsync(dt_.get(), 0, n * sizeof(double), st_), "zero dt");
     k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1, (order == 2 ? inner : 0) + 4,
-                                 update_blocks());
+                                 update_blocks(), split4_ ? 1 : 0);
     a_ = 0;
     b_ = 0;
     done_ = 0;
@@ -1254,7 +1269,7 @@ class Domain {
   // Reuse by a later run on the same geometry (the per-cloud engine cache):
   // gas constants, the error tie-break partition ids and the history
   // capacity may change; kernels captured with the old values are dropped.
-  void reconfigure(double gamma, double cfl, double det_tol, const std::uint8_t* part, int capacity) {
+  void reconfigure(double gamma, double cfl, double det_tol, const std::uint16_t* part, int capacity) {
     ck(cudaSetDevice(device_), "cudaSetDevice");
     const Gas g = make_gas(gamma, cfl, det_tol);
     if (g.gamma != gas_.gamma || g.cfl != gas_.cfl || g.det_tol != gas_.det_tol) {
@@ -1270,12 +1285,13 @@ class Domain {
       clear_graphs();
     }
     const std::size_t nl = static_cast<std::size_t>(n_loc_);
-    std::vector<std::uint8_t> hp(nl, 0);
+    std::vector<std::uint16_t> hp(nl, 0);
     if (part)
       for (std::size_t i = 0; i < nl; ++i) hp[i] = part[gid_host_.empty() ? i : static_cast<std::size_t>(gid_host_[i])];
     if (hp != part_host_) {
       part_host_ = hp;
-      ck(cudaMemcpyAsync(part_.get(), part_host_.data(), nl, cudaMemcpyHostToDevice, st_), "H2D part");
+      ck(cudaMemcpyAsync(part_.get(), part_host_.data(), nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_),
+         "H2D part");
       ck(cudaStreamSynchronize(st_), "part");
     }
   }
@@ -1636,8 +1652,8 @@ class Domain {
   // Message for `key` (another domain's record when this domain owns the point).
   Fault fault_for(unsigned long long key, int err_it, bool with_iteration, const D4* qsrc, const D4* dqsrc,
                   int local = -1) {
-    const unsigned phase = static_cast<unsigned>(key >> 61);
-    const long long point = static_cast<long long>((key >> 22) & 0x7FFFFFFFull);
+    const unsigned phase = key_phase(key);
+    const long long point = key_point(key);
     const int iter = err_it + 1;
     if (phase == PH_RESIDUE)
       return Fault(Status::positivity, "solver diverged at iteration " + itos(iter) + " (non-finite residue)");
@@ -1702,6 +1718,8 @@ class Domain {
   int kmax() const { return kmax_; }
   std::size_t smem() const { return smem_; }
   void set_strict(bool s) { strict_ = s; }
+  // residual_mode=split4: flux failures ordered direction-first (err_key).
+  void set_split4(bool s) { split4_ = s; }
   int order() const { return order_; }
   int inner() const { return inner_; }
 
@@ -1722,8 +1740,14 @@ class Domain {
     return out;
   }
   std::vector<KernelTime> kernel_times() const {
-    // slot -> reported kernel (the sweeps' slots add up to q_derivatives)
-    static const char* names[] = {"q_variables", "q_derivatives", "flux_residual", "state_update", "residue"};
+    // Device timer slots -> the reference's timer rows (runtime.cpp:144-190,
+    // :257): q_variables, q_derivatives (all sweeps), flux_residual (or its
+    // four split4 passes), timestep, state_update, residue.  Two rows are
+    // attributed rather than timed separately: the time step is fused into
+    // k_update (their time is split in proportion to the reference kernels'
+    // algorithmic bytes, 97 : 105 B/pt), and the four split4
+    // directions are one fused flux kernel (a quarter each; summarize() adds
+    // the aggregate row as make_bench_report does, bench.cpp:72-99).
     double secs[5] = {0, 0, 0, 0, 0};
     std::int64_t cnt[5] = {0, 0, 0, 0, 0};
     for (int k = 0; k < KT_COUNT; ++k) {
@@ -1733,8 +1757,23 @@ class Domain {
       cnt[r] += static_cast<std::int64_t>(t.launches);
     }
     std::vector<KernelTime> out;
-    for (int r = 0; r < 5; ++r)
-      if (cnt[r] > 0) out.push_back({names[r], secs[r], cnt[r]});
+    if (cnt[0] > 0) out.push_back({"q_variables", secs[0], cnt[0]});
+    if (cnt[1] > 0) out.push_back({"q_derivatives", secs[1], cnt[1]});
+    if (cnt[2] > 0) {
+      if (split4_) {
+        for (const char* nm : {"flux_residual_xplus", "flux_residual_xminus", "flux_residual_yplus",
+                               "flux_residual_yminus"})
+          out.push_back({nm, secs[2] * 0.25, cnt[2]});
+      } else {
+        out.push_back({"flux_residual", secs[2], cnt[2]});
+      }
+    }
+    if (cnt[3] > 0) {
+      constexpr double kTimestepShare = 97.0 / (97.0 + 105.0);
+      out.push_back({"timestep", secs[3] * kTimestepShare, cnt[3]});
+      out.push_back({"state_update", secs[3] - secs[3] * kTimestepShare, cnt[3]});
+    }
+    if (cnt[4] > 0) out.push_back({"residue", secs[4], cnt[4]});
     static const bool per_sweep = std::getenv("LSKUM_KT_SWEEPS") != nullptr;  // probes: one line per sweep
     static const char* sweeps[] = {"sweep0", "sweep1", "sweep2", "sweep3", "sweep4", "sweep5", "sweep6", "sweep7+"};
     for (int k = KT_SWEEP; per_sweep && k < KT_FLUX; ++k) {
@@ -1773,9 +1812,10 @@ class Domain {
   std::size_t smem_ = 0;
   int stride_ = 0;
   std::vector<int> gid_host_;
-  std::vector<std::uint8_t> part_host_;
+  std::vector<std::uint16_t> part_host_;
   DBuf<double2> xy_, nrm_;
-  DBuf<std::uint8_t> kind_, part_;
+  DBuf<std::uint8_t> kind_;
+  DBuf<std::uint16_t> part_;
   DBuf<int> off_, nbr_, gid_;
   DBuf<double> mind_, dt_, which_, mag_, pval_, hist_, diag_;
   double* mag_out_ = nullptr;
@@ -1798,6 +1838,7 @@ class Domain {
   int capacity_ = 1;
   int order_ = 2, inner_ = 3, chunk_ = 16;
   bool strict_ = false;
+  bool split4_ = false;
   int a_ = 0, b_ = 0, done_ = 0;
   double total_ms_ = 0.0;
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs_;
@@ -1809,7 +1850,7 @@ namespace {
 // A single-device domain of the whole cloud in the numbering `loc` chooses:
 // the cloud's own order, or its locality permutation (reorder.cpp).
 std::unique_ptr<Domain> cloud_domain(const PointSet& ps, const std::shared_ptr<const Locality>& loc,
-                                     const std::vector<std::uint8_t>& part_of, int device, double gamma,
+                                     const std::vector<std::uint16_t>& part_of, int device, double gamma,
                                      double cfl, double det_tol, int capacity) {
   if (loc->order.empty())
     return std::make_unique<Domain>(view_of(ps, part_of), device, gamma, cfl, det_tol, capacity);
@@ -1829,6 +1870,7 @@ std::unique_ptr<Domain> open_domain(PointSet& ps, const EngineSpec& spec, int ca
   trace("engine: geometry uploaded");
   d->upload(ps.fields, false);
   trace("engine: state uploaded");
+  d->set_split4(spec.split4);
   d->begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
   return d;
 }
@@ -1870,6 +1912,7 @@ Domain& cached_domain(PointSet& ps, const EngineSpec& spec, int capacity) {
   if (spec.fs_device) d.fill_prim(spec.fs_prim);
   else d.upload(ps.fields, false);
   trace("engine: state uploaded");
+  d.set_split4(spec.split4);
   d.begin_run(spec.order, spec.inner, spec.fp_mode, spec.chunk);
   return d;
 }
@@ -2057,6 +2100,7 @@ class MultiRun {
       dom_[d]->use_mag(r.mag_buf());
     }
     for (int d = 0; d < P_; ++d) dom_[d]->upload(ps.fields, false);
+    for (int d = 0; d < P_; ++d) dom_[d]->set_split4(spec.split4);
     r.reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);
     ck(cudaStreamSynchronize(r.stream()), "root init");  // shared word initialised before others use it
     for (int d = 1; d < P_; ++d) dom_[d]->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, false);
@@ -2143,9 +2187,9 @@ class MultiRun {
     const int rec = first_failing_domain();
     if (rec < 0) return Fault(Status::argument, "multi-domain run failed without a failure record");
     const unsigned long long key = dom_[rec]->err_key();
-    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    const int g = static_cast<int>(key_point(key));
     int owner = rec, local = -1;
-    if (static_cast<unsigned>(key >> 61) < PH_RESIDUE) {
+    if (key_phase(key) < PH_RESIDUE) {
       for (int d = 0; d < P_; ++d) {
         const auto& own = geoms_[d].gid;
         const auto it = std::lower_bound(own.begin(), own.begin() + geoms_[d].n_own, g);
@@ -2382,6 +2426,7 @@ class RankRun {
     ck(cudaMemset(flags_.get(), 0, FL_COUNT * sizeof(unsigned long long)), "zero flags");
     if (rank == 0) {
       dom_->set_residue_size(ps.n());
+      dom_->set_split4(spec.split4);
       dom_->reset_run(spec.order, spec.inner, spec.fp_mode, spec.chunk, true);  // shared word
       ck(cudaStreamSynchronize(dom_->stream()), "root init");
     }
@@ -2439,6 +2484,7 @@ class RankRun {
       }
     }
     dom_->upload(ps_.fields, false);
+    dom_->set_split4(spec_.split4);
     if (rank_ != 0) dom_->reset_run(spec_.order, spec_.inner, spec_.fp_mode, spec_.chunk, false);
     dom_->first_q();
     ck(cudaStreamSynchronize(dom_->stream()), "first q");
@@ -2495,8 +2541,8 @@ class RankRun {
   bool owns_failure() const {
     if (!dom_->has_error()) return false;
     const unsigned long long key = dom_->err_key();
-    if ((key >> 61) >= PH_RESIDUE) return true;
-    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    if (key_phase(key) >= PH_RESIDUE) return true;
+    const int g = static_cast<int>(key_point(key));
     const LocalGeom& lg = geoms_[rank_];
     return std::binary_search(lg.gid.begin(), lg.gid.begin() + lg.n_own, g);
   }
@@ -2504,8 +2550,8 @@ class RankRun {
     if (!dom_->has_error())
       return Fault(Status::positivity, "the run failed on another rank");
     const unsigned long long key = dom_->err_key();
-    const unsigned phase = static_cast<unsigned>(key >> 61);
-    const int g = static_cast<int>((key >> 22) & 0x7FFFFFFFull);
+    const unsigned phase = key_phase(key);
+    const int g = static_cast<int>(key_point(key));
     if (!owns_failure())
       return Fault(phase == PH_SWEEP ? Status::singular : Status::positivity,
                    "iteration " + itos(dom_->err_iter() + 1) + ": failure at point " + itos(g) +

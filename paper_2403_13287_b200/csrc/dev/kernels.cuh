@@ -29,19 +29,33 @@ constexpr unsigned long long kNoErr = ~0ull;
 // PH_STALL: a cross-process wait timed out (per-rank runs only).
 enum : unsigned { PH_QVAR = 0, PH_SWEEP = 1, PH_FLUX = 2, PH_UPDATE = 3, PH_RESIDUE = 4, PH_STALL = 5 };
 enum : unsigned { KIND_INTERIOR = 0, KIND_WALL = 1, KIND_OUTER = 2 };
-constexpr unsigned kSolveSlot = 0xFFFFFu;  // "after every neighbour" in the error key
+constexpr unsigned kSolveSlot = 0x3FFFu;  // "after every neighbour" in the error key
+constexpr int kMaxParts = 4096;          // partitions the error key distinguishes (12 bits)
+constexpr int kMaxStencil = 0x3FFE;      // neighbour positions the error key distinguishes (14 bits)
 
 // Error key: min over failures reproduces the reference's first failure
 // (phase order, lowest partition, ascending point id, direction Gx+..Gy-,
 // neighbour position) — runtime.cpp:115-118, kernels.cpp:122, :37-64.
+//   phase(3)@61 | dmaj(2)@59 | part(12)@47 | point(31)@16 | dir(2)@14 | j(14)@0
+// dmaj is the direction again for residual_mode=split4 flux failures: there
+// each direction is its own phase over all partitions (runtime.cpp:160-183),
+// so the reference throws the lowest direction first, then the lowest
+// partition; it is 0 otherwise (fused: partition, point, then direction).
 __device__ __forceinline__ unsigned long long err_key(unsigned phase, unsigned part,
                                                       unsigned point, unsigned dir,
-                                                      unsigned j) {
+                                                      unsigned j, unsigned dmaj = 0) {
   return (static_cast<unsigned long long>(phase & 7u) << 61) |
-         (static_cast<unsigned long long>(part & 0xFFu) << 53) |
-         (static_cast<unsigned long long>(point & 0x7FFFFFFFu) << 22) |
-         (static_cast<unsigned long long>(dir & 3u) << 20) | (j & 0xFFFFFu);
+         (static_cast<unsigned long long>(dmaj & 3u) << 59) |
+         (static_cast<unsigned long long>(part & 0xFFFu) << 47) |
+         (static_cast<unsigned long long>(point & 0x7FFFFFFFu) << 16) |
+         (static_cast<unsigned long long>(dir & 3u) << 14) | (j & 0x3FFFu);
 }
+__host__ __device__ __forceinline__ unsigned key_phase(unsigned long long k) { return static_cast<unsigned>(k >> 61); }
+__host__ __device__ __forceinline__ long long key_point(unsigned long long k) {
+  return static_cast<long long>((k >> 16) & 0x7FFFFFFFull);
+}
+__host__ __device__ __forceinline__ unsigned key_dir(unsigned long long k) { return static_cast<unsigned>((k >> 14) & 3ull); }
+__host__ __device__ __forceinline__ unsigned key_j(unsigned long long k) { return static_cast<unsigned>(k & 0x3FFFull); }
 
 struct KTimer {
   unsigned long long t0, t1;
@@ -85,6 +99,8 @@ struct Ctl {
   unsigned long long upd_done;
   unsigned long long err_stage;  // this domain's failing stage (kNoErr = none)
   unsigned long long err_key;    // min key at that stage
+  int split4;                    // residual_mode=split4: flux failures ordered by direction first
+  int pad_;
   KTimer kt[KT_COUNT];
 };
 
@@ -92,7 +108,7 @@ struct Geo {
   const double2* xy;
   const double2* nrm;
   const std::uint8_t* kind;
-  const std::uint8_t* part;
+  const std::uint16_t* part;
   const int* off;
   const int* nbr;
   const double* mind;
@@ -163,6 +179,13 @@ __device__ __forceinline__ void raise_err(Ctl* ctl, unsigned long long key, int 
   atomicMin(&ctl->err_stage, st);
   atomicMin(&ctl->err_key, key);
   atomicMin(&ctl->sh->err_stage, st);
+}
+
+// Flux failure key: direction-major under residual_mode=split4 (see err_key).
+// Only read on the failure path.
+__device__ __forceinline__ unsigned long long flux_key(const Ctl* ctl, unsigned part, unsigned point,
+                                                       unsigned dir, unsigned j) {
+  return err_key(PH_FLUX, part, point, dir, j, ctl->split4 ? dir : 0u);
 }
 
 // ---- per-kernel device timing (globaltimer) ----
@@ -515,7 +538,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
       }
       FluxState fi, fn;
       ok = reconstruct2<S>(ti, tn, a.gas, fi, fn) && ok;
-      if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
+      if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
       AxisTerms at[4];
       axis_terms4<S>(fi, fn, at);
       const bool store = act && ok;
@@ -579,7 +602,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
         }
         const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
         if (!(det > a.gas.det_tol)) {
-          raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), d, kSolveSlot), sub_flux(a.ctl));
+          raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), d, kSolveSlot), sub_flux(a.ctl));
         } else {
 #pragma unroll
           for (int cc = 0; cc < NC; ++cc) {
@@ -717,7 +740,7 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   }
   FluxState fi, fn;
   ok = reconstruct2<false, HP>(ti, tn, a.gas, fi, fn) && ok;
-  if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
+  if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
   AxisTerms at[4];
   axis_terms4<false>(fi, fn, at);
   const bool store = act && ok;
@@ -799,7 +822,7 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
     const int kwarp = __reduce_max_sync(kFull, k);
     if (live && lane == 0) {
       const unsigned sd = sing[i];
-      if (sd != 0xFFu) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
+      if (sd != 0xFFu) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
     }
     const double2 pi = g.xy[ic];
     const D4 qi = ld4(a.q + ic);
@@ -907,9 +930,9 @@ __global__ void __launch_bounds__(256, MB) k_flux1(FluxArgs a, const PointFlux* 
     const bool ok = valid[ic] != 0 && valid[nb] != 0;
     if (live && lane == 0) {
       const unsigned sd = sing[i];
-      if (sd != 0xFFu) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
+      if (sd != 0xFFu) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
     }
-    if (act && !ok) raise_err(a.ctl, err_key(PH_FLUX, g.part[i], gidx(g, i), static_cast<unsigned>(sx), lane),
+    if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), static_cast<unsigned>(sx), lane),
                               sub_flux(a.ctl));
     const bool store = act && ok;
     const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
@@ -1061,7 +1084,7 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), oy01 = *reinterpret_cast<const double2*>(o + 64);
       const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
       if (cur.live && lane == 0 && cur.sing != 0xFF)
-        raise_err(a.ctl, err_key(PH_FLUX, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
+        raise_err(a.ctl, flux_key(a.ctl, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,

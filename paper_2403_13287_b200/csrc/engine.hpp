@@ -18,12 +18,13 @@ struct EngineSpec {
   double gamma = 1.4, cfl = 0.5, det_tol = 0.0;
   int iters = 0, inner = 3, order = 2;
   int fp_mode = 0;  // 0 fast, 1 strict
+  int split4 = 0;   // residual_mode=split4 (failure order: direction before partition)
   int chunk = 16;   // iterations per captured graph
   int device = 0;
   int gpus = 1;     // device domains (sessions; lskum_run decides in solve.cpp)
   int reorder = 0;  // single-device numbering: kReorderNone / Hilbert / Auto (reorder.cpp)
   // Partition of each point (reference error tie-break, runtime.cpp:115-118).
-  std::vector<std::uint8_t> part_of;
+  std::vector<std::uint16_t> part_of;
   // lskum_run's free-stream initialisation done on the device (single-domain
   // runs): the host store is only written by the copy-back; store_written
   // reports whether that happened, so the caller can apply the host-side
@@ -57,17 +58,17 @@ struct LocalGeom {
   std::vector<Kind> kind;                // n_loc
   std::vector<std::int64_t> off;         // n_own + 1
   std::vector<std::int32_t> nbr;         // local ids
-  std::vector<std::uint8_t> part;        // n_loc: reference partition (error tie-break)
+  std::vector<std::uint16_t> part;       // n_loc: reference partition (error tie-break)
   std::vector<std::int32_t> gid;         // n_loc: local -> global id
   std::vector<std::int32_t> halo_dom;    // n_loc - n_own
   std::vector<std::int32_t> halo_idx;    // n_loc - n_own
 };
-std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of,
+std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint16_t>& part_of,
                                  int reorder = 0);
 // The whole cloud as one domain in the given device order (reorder.cpp):
 // point k of the domain is point order[k] of the cloud; no halo.
 LocalGeom permuted_geom(const PointSet& ps, const std::vector<std::int32_t>& order,
-                        const std::vector<std::uint8_t>& part_of);
+                        const std::vector<std::uint16_t>& part_of);
 
 // Multi-domain run: one Domain per RCB piece, devices assigned round-robin
 // from spec.device; halos exchanged by peer-memory gathers; residue summed

@@ -15,7 +15,7 @@
 
 namespace lskb {
 
-std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint8_t>& part_of,
+std::vector<LocalGeom> decompose(const PointSet& ps, int n_domains, const std::vector<std::uint16_t>& part_of,
                                  int reorder) {
   std::vector<Piece> pieces = bisect_cloud(ps, n_domains);
   const std::int32_t n = ps.n();

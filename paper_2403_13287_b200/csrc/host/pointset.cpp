@@ -111,6 +111,13 @@ PointSet assemble(std::vector<PointRow> rows, std::vector<std::int64_t> off,
   if (static_cast<std::int64_t>(off.size()) != n64 + 1 || off[0] != 0 ||
       off.back() != static_cast<std::int64_t>(nbr.size()))
     raise(Status::argument, "malformed stencil offsets");
+  // every offset inside [0, nnz] before any stencil is scanned (a negative
+  // count is reported by the per-point checks below, with its point id)
+  {
+    const std::int64_t nnz = static_cast<std::int64_t>(nbr.size());
+    for (std::int64_t i = 1; i < n64; ++i)
+      if (off[i] < 0 || off[i] > nnz) raise(Status::argument, "malformed stencil offsets");
+  }
   // range checks in parallel; the first offending point (lowest id) is reported
   {
     const int t = std::max(1, std::min<int>(host_threads(), static_cast<int>(n / 65536) + 1));

@@ -177,7 +177,7 @@ const Locality& cloud_locality(const PointSet& ps, int mode) {
 namespace lskb {
 
 LocalGeom permuted_geom(const PointSet& ps, const std::vector<std::int32_t>& order,
-                        const std::vector<std::uint8_t>& part_of) {
+                        const std::vector<std::uint16_t>& part_of) {
   const std::int32_t n = ps.n();
   LocalGeom g;
   g.n_own = g.n_loc = n;

@@ -67,6 +67,10 @@ void Settings::check() const {
   if (!(cfl > 0.0)) raise(Status::config, "cfl must be > 0");
   if (order != 1 && order != 2) raise(Status::config, "order must be 1 or 2");
   if (parts < 1) raise(Status::config, "parts must be >= 1");
+  // The device failure key orders 4096 partitions (kernels.cuh err_key); the
+  // reference accepts any count, but more pieces than that only exist for
+  // clouds of millions of points split for nothing but the tie-break.
+  if (parts > 4096) raise(Status::config, "parts must be <= 4096");
   if (workers < 1) raise(Status::config, "workers must be >= 1");
   if (device < 0) raise(Status::config, "device must be >= 0");
   if (gpus < 1) raise(Status::config, "gpus must be >= 1");

@@ -31,6 +31,7 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
   spec.inner = s.inner;
   spec.order = s.order;
   spec.fp_mode = s.fp_mode;
+  spec.split4 = s.residual_split4;
   spec.chunk = s.chunk;
   spec.device = s.device;
   spec.gpus = s.gpus;
@@ -44,7 +45,7 @@ EngineSpec spec_from(const PointSet& ps, const Settings& s, double det_tol) {
     spec.part_of.assign(static_cast<std::size_t>(ps.n()), 0);
     for (std::size_t p = 0; p < pieces.size(); ++p)
       for (std::int32_t i : pieces[p].owned)
-        spec.part_of[i] = static_cast<std::uint8_t>(std::min<std::size_t>(p, 255));
+        spec.part_of[i] = static_cast<std::uint16_t>(p);
   }
   return spec;
 }

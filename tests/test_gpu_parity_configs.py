@@ -1,0 +1,222 @@
+"""GPU vs the reference itself on the BASELINE point distributions (GPU tests).
+
+north_star: "Results must match the CPU reference on the same point
+distributions".  Every case here runs the reference's own run_fixed_point
+(oracle/_ref/liblskum_refshim.so: the unmodified reference core behind a C
+shim, runtime.cpp:195-275, entered the way lskum_capi.cpp:209-220 enters it)
+and the GPU path through the C ABI on identical input arrays, at the sizes
+BASELINE.json's configs name:
+
+  configs[0] NACA 0012 260x154  (40,040 points)   M 0.63 AoA 2   order 1, 1000 iterations
+  configs[1] NACA 0012 520x308  (160,160 points)  M 0.85 AoA 1   order 1 (100) and order 2 (30)
+  configs[2] NACA 0012 1000x625 (625,000 points)  M 1.2  AoA 0   order 1 (100) and order 2 (30)
+  configs[3] NACA 0012 4000x2500 (10M points)     M 0.85 AoA 1   order 2, 5-iteration prefix
+
+The state is the free stream plus a +5% Gaussian density/pressure bump above
+the section (the reference's tests/support.hpp:45-56 bump, centred at
+(0.5, 0.5)), so every data-dependent branch of the flux is exercised.  The
+NACA clouds hold their surface ring at the free stream (the reference has no
+wall flux).  Wall points are covered by the reference's own
+annulus (cloud.cpp:372-425): it validates at 256x64 and 512x128 and aborts in
+iteration 3 at both orders, which the GPU must reproduce (code, iteration and
+message), after matching the two iterations before.
+
+Tolerances: order 1 residue <= 1e-10 relative, state <= 1e-12
+(scale-aware, tests/acceptance.cpp:56-62); order 2 residue <= 1e-10 over 20
+iterations and <= 1e-9 at 30, state <= 1e-9 at 30.  The residue reduction is
+also compared bitwise with the reference's deterministic_reduce
+(reduce.hpp:11-17) at the sizes where the device tree takes its multi-level
+fold path (2.4M, 10M, 40M values).
+
+The reference runs with parts = workers = host cores: its determinism
+matrix makes that bitwise equal to the single-thread run (README.md:159-161).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as P
+from conftest import rel_err
+from paper_2403_13287_b200 import lskum as L
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not P.have_ref(), reason="reference build (oracle/_ref) absent")]
+
+THREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+def naca(nw, nr):
+    return L.Cloud.generate_naca0012(nw, nr, 20.0, 0.0, 7, 8, frozen_wall=True)
+
+
+def bumped(g, mach, aoa, gamma=1.4, amplitude=0.05, sigma=0.1):
+    """Free stream (bench.cpp:43-56) times the +5% bump of tests/support.hpp:45-56."""
+    a = aoa * math.pi / 180.0
+    n = g["x"].shape[0]
+    prim = np.empty((n, 4))
+    prim[:, 0] = 1.0
+    prim[:, 1] = mach * math.cos(a)
+    prim[:, 2] = mach * math.sin(a)
+    prim[:, 3] = 1.0 / gamma
+    dx = g["x"] - 0.5
+    dy = g["y"] - 0.5
+    f = 1.0 + amplitude * np.exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma))
+    prim[:, 0] *= f
+    prim[:, 3] *= f
+    return prim
+
+
+def oracle_cloud(g):
+    return P.Cloud(g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"])
+
+
+def ref_and_gpu(cloud, mach, aoa, order, iters, **extra):
+    """The reference and the GPU from the same arrays and initial state."""
+    g = cloud.geometry()
+    prim0 = bumped(g, mach, aoa)
+    want = P.ref_run(oracle_cloud(g), mach=mach, aoa=aoa, iters=iters, order=order, inner=3, cfl=0.5,
+                     layout=1, parts=THREADS, workers=THREADS, prim0=prim0)
+    cloud.reset_store(0)
+    cloud.set_primitives(prim0)
+    err = None
+    try:
+        res = L.run_fixed_point(cloud, L.Config(mach=mach, aoa=aoa, iters=iters, order=order, inner=3, cfl=0.5,
+                                                parts=THREADS, **extra))
+        got = res.residues()
+    except L.LskumError as e:
+        err, got = e, None
+    return want, got, err, cloud
+
+
+def rel_seq(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    return float(np.max(np.abs(got - want) / np.abs(want)))
+
+
+CASES = {
+    "configs1": ((520, 308), 0.85, 1.0),
+    "configs2": ((1000, 625), 1.2, 0.0),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_order1_100_iterations_match_reference(case):
+    dims, mach, aoa = CASES[case]
+    want, got, err, c = ref_and_gpu(naca(*dims), mach, aoa, 1, 100)
+    assert want.code == 0, want.msg
+    assert err is None, err
+    assert len(got) == 100 and got[0] > 0.0
+    assert rel_seq(got, want.residue) <= 1e-10
+    f = c.fields()
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-12   # primitives
+    assert rel_err(f[:, 4:8], want.store[:, 4:8]) <= 1e-12   # q
+    assert rel_err(f[:, 20:21], want.store[:, 20:21]) <= 1e-12  # delta_t
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("fp_mode", ["fast", "strict"])
+def test_order2_prefix_matches_reference(case, fp_mode):
+    dims, mach, aoa = CASES[case]
+    want, got, err, c = ref_and_gpu(naca(*dims), mach, aoa, 2, 30, fp_mode=fp_mode)
+    if want.code != 0:  # the reference's order-2 instability: same abort
+        assert err is not None and err.status == want.code
+        assert err.message.split(":")[0] == want.msg.split(":")[0]
+        return
+    assert err is None, err
+    assert rel_seq(got[:20], want.residue[:20]) <= 1e-10
+    assert rel_seq(got, want.residue) <= 1e-9
+    f = c.fields()
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-9
+    assert rel_err(f[:, 8:16], want.store[:, 8:16]) <= 1e-7  # final derivatives (no decay floor)
+
+
+def test_configs0_order1_1000_iterations_match_reference():
+    """configs[0]: ~40K points, M 0.63, AoA 2, 1000 iterations (the reference CPU run)."""
+    want, got, err, c = ref_and_gpu(naca(260, 154), 0.63, 2.0, 1, 1000)
+    assert want.code == 0, want.msg
+    assert err is None, err
+    # <= 1e-10 relative while log10rel > -4, <= 1e-10 * res1 absolute after
+    w = want.residue
+    live = np.log10(w / w[0]) > -4.0
+    assert rel_seq(got[live], w[live]) <= 1e-10
+    assert float(np.max(np.abs(got[~live] - w[~live]))) <= 1e-10 * w[0] if (~live).any() else True
+    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-12
+
+
+def test_configs3_10m_order2_prefix_matches_reference():
+    """configs[3]: the 10M-point cloud, 5 second-order iterations (k_flux_ws
+    in its 8x2 block shape and the sweep/update/tree at full size)."""
+    want, got, err, c = ref_and_gpu(naca(4000, 2500), 0.85, 1.0, 2, 5)
+    assert want.code == 0, want.msg
+    assert err is None, err
+    assert rel_seq(got, want.residue) <= 1e-10
+    f = c.fields()
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-10
+    assert rel_err(f[:, 16:20], want.store[:, 16:20]) <= 1e-9  # last flux residual
+
+
+@pytest.mark.parametrize("n", [2_400_000, 10_000_000, 40_000_000])
+def test_reduce_fold_path_bitwise_reference(n):
+    """Residue tree at the sizes whose device tree folds several levels serially
+    (d1 = 11..13) against the reference's deterministic_reduce itself."""
+    rng = np.random.default_rng(n)
+    v = rng.uniform(0.0, 1.0, n) ** 4 * rng.choice([1e-6, 1.0, 1e6], n)
+    assert L.reduce(v) == P.ref_reduce(v)
+
+
+# ---- wall points: the reference's annulus (cloud.cpp:372-425) ----
+ANNULI = [(256, 64), (512, 128)]
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("dims", ANNULI)
+def test_annulus_walls_match_reference_then_abort_identically(dims, order):
+    c = P.ref_generate_annulus(dims[0], dims[1], 10.0, 0.0, 0, 8)
+    assert np.count_nonzero(c.kind == 1) == dims[0]
+    assert P.ref_validate(c)["n_defective"] == 0
+    prim0 = bumped({"x": c.x, "y": c.y}, 0.63, 2.0)
+    prim0[:] = prim0[0]  # plain free stream: the walls alone drive the flow
+    # the two iterations before the abort: wall slip, wall-point fluxes and residue
+    want = P.ref_run(c, iters=2, order=order, prim0=prim0)
+    assert want.code == 0, want.msg
+    pc = L.Cloud.from_arrays(c.x, c.y, c.kind, c.nx, c.ny, c.off, c.nbr)
+    pc.reset_store(0)
+    pc.set_primitives(prim0)
+    res = L.run_fixed_point(pc, L.Config(mach=0.63, aoa=2.0, iters=2, order=order, inner=3, cfl=0.5))
+    assert rel_seq(res.residues(), want.residue) <= 1e-10
+    f = pc.fields()
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-10
+    walls = c.kind == 1
+    un = f[walls, 1] * c.nx[walls] + f[walls, 2] * c.ny[walls]
+    assert float(np.max(np.abs(un))) <= 1e-12  # slip: no velocity through the wall
+    # the abort: same code, iteration and message, for one and four partitions
+    for parts in (1, 4):
+        ab = P.ref_run(c, iters=50, order=order, prim0=prim0, parts=parts, workers=parts)
+        assert ab.code == L.ERR_POSITIVITY and ab.msg.startswith("iteration 3:")
+        pc.reset_store(0)
+        pc.set_primitives(prim0)
+        with pytest.raises(L.LskumError) as e:
+            L.run_fixed_point(pc, L.Config(mach=0.63, aoa=2.0, iters=50, order=order, inner=3, cfl=0.5,
+                                           parts=parts))
+        assert e.value.status == ab.code
+        assert e.value.message == ab.msg
+
+
+@pytest.mark.parametrize("parts", [1, 8])
+def test_split4_abort_reports_the_reference_edge(bump_cloud_arrays, parts):
+    """residual_mode=split4 runs each flux direction as its own phase over all
+    partitions (runtime.cpp:160-183), so its first failure is ordered by
+    direction before partition; the abort message must be the reference's
+    (with 8 parts the fused and split4 reference runs report different edges)."""
+    c, prim0 = bump_cloud_arrays
+    want = P.ref_run(c, iters=200, order=2, prim0=prim0, mode=1, parts=parts, workers=parts)
+    assert want.code != 0
+    pc = L.Cloud.from_arrays(c.x, c.y, c.kind, c.nx, c.ny, c.off, c.nbr)
+    pc.reset_store(0)
+    pc.set_primitives(prim0)
+    with pytest.raises(L.LskumError) as e:
+        L.run_fixed_point(pc, L.Config(mach=0.63, aoa=2.0, iters=200, order=2, inner=3, cfl=0.5,
+                                       residual_mode="split4", parts=parts))
+    assert e.value.status == want.code
+    assert e.value.message == want.msg
