@@ -108,6 +108,9 @@ int lskum_b200_op_timestep(lskum_cloud* cloud, const lskum_b200_params* p);
 int lskum_b200_op_state_update(lskum_cloud* cloud, const lskum_b200_params* p);
 /* deterministic_reduce (reference reduce.hpp:11-17) evaluated on the device. */
 int lskum_b200_reduce(const double* values, int64_t n, double* out);
+/* Correctly rounded (nearest, ties to even) sum of non-negative doubles: the
+   fast-mode residue accumulator (kernels.cuh acc_warp_add / acc_to_double). */
+int lskum_b200_exact_sum(const double* values, int64_t n, double* out);
 
 /* ---- partitioning (partition_cloud, reference partition.hpp:27) ----
  * owner[i] = part of point i; ghosts of part p are ghosts[ghost_off[p]..ghost_off[p+1]). */

@@ -939,6 +939,9 @@ class Domain {
     mag_out_ = mag_.get();
     pval_.alloc(8192, st_);
     psz_.alloc(8192, st_);
+    acc_.alloc(2 * kAccWords, shared_st);  // peers read it (root's residue)
+    acc_tab_.p[0] = acc_.get();
+    acc_ndom_ = 1;
     ctl_.alloc(1, st_);
     sh_.alloc(1, shared_st);
     // whole words defined (refresh_ctl copies them back, padding included)
@@ -1003,6 +1006,12 @@ class Domain {
     }
   }
   double* mag_buf() { return mag_.get(); }
+  // Exact residue accumulators ([2][kAccWords]); the root sums every domain's.
+  unsigned long long* acc_buf() { return acc_.get(); }
+  void use_acc_tab(const AccTab& t, int ndom) {
+    acc_tab_ = t;
+    acc_ndom_ = ndom;
+  }
   Shared* own_shared() { return sh_.get(); }
   int n_loc() const { return n_loc_; }
   int device() const { return device_; }
@@ -1230,6 +1239,7 @@ class Domain {
     ck(cudaMemsetAsync(dq_[1].get(), 0, 2 * nl * sizeof(D4), st_), "zero dq");
     ck(cudaMemsetAsync(res_.get(), 0, n * sizeof(D4), st_), "zero res");
     ck(cudaMemsetAsync(dt_.get(), 0, n * sizeof(double), st_), "zero dt");
+    ck(cudaMemsetAsync(acc_.get(), 0, 2 * kAccWords * sizeof(unsigned long long), st_), "zero acc");
     k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, own_shared ? 1 : 0, -1, (order == 2 ? inner : 0) + 4,
                                  update_blocks(), split4_ ? 1 : 0);
     a_ = 0;
@@ -1253,7 +1263,10 @@ class Domain {
     refresh_ctl();
   }
 
-  int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + 4; }
+  int launches_per_iter() const {
+    const bool pf = !strict_ && weights_ && order_ == 1 && point_flux_enabled() && pf_.get() && kmax_ <= 8;
+    return (order_ == 2 ? inner_ : 0) + (pf ? 2 : 1) + 1 + (strict_ ? 2 : 1);
+  }
 
   // Grid of k_update (persistent: at most the resident blocks); fixed per
   // domain, since the iteration index is derived from its completed blocks.
@@ -1391,9 +1404,15 @@ class Domain {
     ua.mag = mag_out_;
     ua.which = which_.get();
     ua.ctl = ctl_.get();
+    ua.acc = strict_ ? nullptr : acc_.get();
     launch_pdl(k_update, update_blocks(), 256, 0, st_, ua);
   }
   void launch_residue() {
+    if (!strict_) {
+      launch_pdl(k_residue_exact, 1, 96, 0, st_, acc_tab_, acc_ndom_, n_res_, hist_.get(), it0_.get(), it1_.get(),
+                 ctl_.get());
+      return;
+    }
     launch_pdl(k_tree_partial, 1 << d1_, kTreeThreads, 0, st_, static_cast<const double*>(mag_.get()), n_res_, d1_,
                pval_.get(), psz_.get(),
                                                       ctl_.get());
@@ -1820,6 +1839,9 @@ class Domain {
   DBuf<double> mind_, dt_, which_, mag_, pval_, hist_, diag_;
   double* mag_out_ = nullptr;
   DBuf<long long> psz_;
+  DBuf<unsigned long long> acc_;
+  AccTab acc_tab_{};
+  int acc_ndom_ = 1;
   DBuf<D4> prim_, q_[2], dq_[2], res_;
   std::int64_t nnz_ = 0;
   DBuf<double2> w1_, w2_;       // least-squares weights of the split stencils (fast mode)
@@ -2095,6 +2117,9 @@ class MultiRun {
     }
     Domain& r = root();
     r.set_residue_size(ps.n());
+    AccTab tab{};
+    for (int d = 0; d < P_; ++d) tab.p[d] = dom_[d]->acc_buf();
+    r.use_acc_tab(tab, P_);  // exact residue: the root sums every domain's digits
     for (int d = 1; d < P_; ++d) {
       dom_[d]->use_shared(r.shared());
       dom_[d]->use_mag(r.mag_buf());
@@ -2131,7 +2156,7 @@ class MultiRun {
 
   Domain& root() { return *dom_[0]; }
   int launches_per_iter() const {
-    return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 3) + 2;
+    return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 3) + (spec_.fp_mode == 1 ? 2 : 1);
   }
 
   // Enqueues n more iterations (stopping early on an error); returns the
@@ -2240,7 +2265,6 @@ class MultiRun {
     if (t > 0) {
       for (int d = 0; d < P_; ++d) {
         ck(cudaSetDevice(dev_[d]), "cudaSetDevice");
-        wait(d, ev_res_[t - 1]);
         for (int o : src_[d]) wait(d, ev_upd_[o][t - 1]);
         dom_[d]->launch_halo(dom_[d]->q_buf(a), 1, hdom_[d]->get(), hidx_[d]->get(), peers_q(a), 0);
       }
@@ -2272,6 +2296,9 @@ class MultiRun {
       if (timed && d == 0) ck(cudaEventRecord(kev_[2], r.stream()), "EventRecord");
       dom_[d]->launch_flux(a, bfin, spec_.order != 2);
       if (timed && d == 0) ck(cudaEventRecord(kev_[3], r.stream()), "EventRecord");
+      // the root's residue of t-1 has read what update(t) overwrites (the
+      // residue summands, or the accumulator of iteration t+1)
+      if (t > 0) wait(d, ev_res_[t - 1]);
       dom_[d]->launch_update(a);
       ck(cudaEventRecord(ev_upd_[d][t], dom_[d]->stream()), "EventRecord");
     }
@@ -2362,7 +2389,7 @@ __global__ void k_wait(WaitList w, long long mult, long long add, Ctl* ctl, int 
 
 struct RankBlob {
   int rank = 0, world = 0, device = 0, pad = 0;
-  cudaIpcMemHandle_t q[2], dq[2], flags, sh, mag;
+  cudaIpcMemHandle_t q[2], dq[2], flags, sh, mag, acc;
 };
 
 template <class T>
@@ -2441,6 +2468,7 @@ class RankRun {
     ck(cudaIpcGetMemHandle(&blob_.dq[0], dom_->dq_buf(0)), "IpcGetMemHandle dq0");
     ck(cudaIpcGetMemHandle(&blob_.dq[1], dom_->dq_buf(1)), "IpcGetMemHandle dq1");
     ck(cudaIpcGetMemHandle(&blob_.flags, flags_.get()), "IpcGetMemHandle flags");
+    ck(cudaIpcGetMemHandle(&blob_.acc, dom_->acc_buf()), "IpcGetMemHandle acc");
     if (rank == 0) {
       ck(cudaIpcGetMemHandle(&blob_.sh, dom_->own_shared()), "IpcGetMemHandle shared");
       ck(cudaIpcGetMemHandle(&blob_.mag, dom_->mag_buf()), "IpcGetMemHandle mag");
@@ -2463,8 +2491,10 @@ class RankRun {
   void connect(const std::vector<RankBlob>& blobs) {
     if (static_cast<int>(blobs.size()) != world_) raise(Status::argument, "need one blob per rank");
     ck(cudaSetDevice(device_), "cudaSetDevice");
+    AccTab acc{};
     for (int o = 0; o < world_; ++o) {
       if (o == rank_) {
+        acc.p[o] = dom_->acc_buf();
         for (int k = 0; k < 2; ++k) {
           qp_[k].base[o] = dom_->q_buf(k);
           dqp_[k].base[o] = dom_->dq_buf(k);
@@ -2478,11 +2508,13 @@ class RankRun {
         dqp_[k].base[o] = open(open_ipc<D4>(b.dq[k]));
       }
       flag_[o] = open(open_ipc<unsigned long long>(b.flags));
+      if (rank_ == 0) acc.p[o] = open(open_ipc<unsigned long long>(b.acc));
       if (o == 0) {
         dom_->use_shared(open(open_ipc<Shared>(b.sh)));
         dom_->use_mag(open(open_ipc<double>(b.mag)));
       }
     }
+    if (rank_ == 0) dom_->use_acc_tab(acc, world_);
     dom_->upload(ps_.fields, false);
     dom_->set_split4(spec_.split4);
     if (rank_ != 0) dom_->reset_run(spec_.order, spec_.inner, spec_.fp_mode, spec_.chunk, false);
@@ -2669,7 +2701,7 @@ class RankRun {
       for (int o = 1; o < world_; ++o) all.push_back(o);
       wait_for(all, FL_UPD, 1, 0, -1);
       d.launch_residue();
-      launches_ += 2;
+      launches_ += spec_.fp_mode == 1 ? 2 : 1;
       signal(FL_RES, 1, 0);
     }
     ck(cudaGetLastError(), "rank launches");
@@ -2716,7 +2748,7 @@ class RankRun {
       for (int o = 1; o < world_; ++o) all.push_back(o);
       wait_for(all, FL_UPD, 1, 0, -1);  // guard: the residue stage of iteration t
       d.launch_residue();
-      launches_ += 2;  // tree partial + final
+      launches_ += spec_.fp_mode == 1 ? 2 : 1;  // tree partial + final, or the exact sum
       signal(FL_RES, 1, 0);
     }
     ck(cudaGetLastError(), "rank launches");
@@ -2991,6 +3023,23 @@ double engine_reduce(const double* v, std::int64_t n, int device) {
   ck(cudaGetLastError(), "reduce launch");
   double r = 0.0;
   ck(cudaMemcpy(&r, out.get(), sizeof r, cudaMemcpyDeviceToHost), "D2H reduce");
+  return r;
+}
+
+double engine_exact_sum(const double* v, std::int64_t n, int device) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  DBuf<double> dv(static_cast<std::size_t>(std::max<std::int64_t>(1, n))), out(1);
+  DBuf<unsigned long long> acc(kAccWords);
+  ck(cudaMemset(acc.get(), 0, kAccWords * sizeof(unsigned long long)), "memset acc");
+  if (n > 0) {
+    ck(cudaMemcpy(dv.get(), v, n * sizeof(double), cudaMemcpyHostToDevice), "H2D exact sum");
+    const int blocks = static_cast<int>(std::min<std::int64_t>((n + 255) / 256, 148 * 8));
+    k_exact_sum_blocks<<<blocks, 256>>>(dv.get(), n, acc.get());
+  }
+  k_exact_sum_final<<<1, 1>>>(acc.get(), out.get());
+  ck(cudaGetLastError(), "exact sum launch");
+  double r = 0.0;
+  ck(cudaMemcpy(&r, out.get(), sizeof r, cudaMemcpyDeviceToHost), "D2H exact sum");
   return r;
 }
 

@@ -1115,7 +1115,125 @@ struct UpdateArgs {
   double* mag;   // (dt * res0)^2, indexed by GLOBAL point id (the residue tree's order)
   double* which; // failure detail (density 0 / pressure 1), local index
   Ctl* ctl;
+  // Exact residue (fast mode): this domain's accumulators [2][kAccWords] by
+  // iteration parity; null = write mag for the midpoint tree (strict mode).
+  unsigned long long* acc;
 };
+
+// ---------------------------------------------------------------------------
+// Exact residue sum (fast mode).  The reference sums (dt*res0)^2 with a
+// midpoint tree over point ids (reduce.hpp:11-17, runtime.cpp:251-256); that
+// order only exists on the whole cloud, so a sharded run would have to funnel
+// every summand to one device.  Instead each domain adds its summands EXACTLY
+// into a fixed-point accumulator: 32-bit digits (kept in 64-bit words so
+// carries can wait) of the value in units of 2^-1074, enough for any finite
+// double times 2^31 summands.  Integer addition is associative, so the sum is
+// independent of the number of domains, the block shape and the point order;
+// the final kernel rounds it once to the nearest double (within a few ulps of
+// the reference's pairwise tree, whose error is O(log2 N) ulps: far inside
+// SURVEY 8(c)'s 1e-10).  Strict mode keeps the bitwise tree.
+constexpr int kAccLimbs = 68;  // 68 * 32 = 2176 bits > 1074 + 1024 + 31
+constexpr int kAccFlag = kAccLimbs;  // non-finite summand seen
+constexpr int kAccWords = 72;        // limbs + flag + padding (576 bytes)
+
+// Adds the warp's 32 summands (one per lane, >= 0 or non-finite) to a block
+// accumulator in shared memory.  All 32 lanes must call it together.  The
+// common case — the warp's summands within a factor 2^64 of each other — is
+// one 128-bit warp sum and up to four shared atomics by lane 0.
+__device__ __forceinline__ void acc_warp_add(unsigned long long* sacc, double v) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+  const unsigned be = static_cast<unsigned>(bits >> 52) & 0x7FFu;
+  const bool nonfinite = be == 0x7FFu;
+  const bool live = !nonfinite && (bits & 0x7FFFFFFFFFFFFFFFull) != 0ull;
+  const int lane = threadIdx.x & 31;
+  if (__any_sync(kFull, nonfinite) && lane == 0) sacc[kAccFlag] = 1ull;
+  if (!__any_sync(kFull, live)) return;
+  const unsigned long long m = live ? ((bits & 0xFFFFFFFFFFFFFull) | (be ? (1ull << 52) : 0ull)) : 0ull;
+  const unsigned pos = be ? be - 1u : 0u;  // value = m * 2^pos * 2^-1074
+  const unsigned L = pos >> 5, sh = pos & 31u;
+  const unsigned lmin = __reduce_min_sync(kFull, live ? L : 0xFFFFFFFFu);
+  const unsigned lmax = __reduce_max_sync(kFull, live ? L : 0u);
+  if (lmax - lmin <= 1u) {
+    const unsigned k = live ? sh + 32u * (L - lmin) : 0u;  // <= 63
+    unsigned long long lo = m << k, hi = k ? (m >> (64u - k)) : 0ull;  // < 2^116
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(kFull, lo, o), h2 = __shfl_xor_sync(kFull, hi, o);
+      const unsigned long long s2 = lo + l2;
+      hi += h2 + (s2 < lo ? 1ull : 0ull);
+      lo = s2;
+    }
+    if (lane == 0) {  // < 2^121: four digits from lmin
+      atomicAdd(sacc + lmin, lo & 0xFFFFFFFFull);
+      if (lo >> 32) atomicAdd(sacc + lmin + 1, lo >> 32);
+      if (hi & 0xFFFFFFFFull) atomicAdd(sacc + lmin + 2, hi & 0xFFFFFFFFull);
+      if (hi >> 32) atomicAdd(sacc + lmin + 3, hi >> 32);
+    }
+  } else if (live) {  // widely spread summands: three digits per lane
+    const unsigned long long lo = m << sh, hi = sh ? (m >> (64u - sh)) : 0ull;
+    atomicAdd(sacc + L, lo & 0xFFFFFFFFull);
+    atomicAdd(sacc + L + 1, lo >> 32);
+    if (hi) atomicAdd(sacc + L + 2, hi);
+  }
+}
+
+// Block accumulator -> the domain's accumulator (call after a __syncthreads()).
+__device__ __forceinline__ void acc_block_flush(const unsigned long long* sacc, unsigned long long* acc) {
+  for (int t = threadIdx.x; t <= kAccFlag; t += blockDim.x) {
+    const unsigned long long v = sacc[t];
+    if (v) atomicAdd(acc + t, v);
+  }
+}
+
+// The exact sum (digits summed over domains, carries not yet propagated)
+// rounded to the nearest double, ties to even.  One thread.
+__device__ __forceinline__ double acc_to_double(unsigned long long* d) {
+  for (int i = 0; i < kAccLimbs - 1; ++i) {
+    d[i + 1] += d[i] >> 32;
+    d[i] &= 0xFFFFFFFFull;
+  }
+  int top = kAccLimbs - 1;
+  while (top >= 0 && d[top] == 0ull) --top;
+  if (top < 0) return 0.0;
+  if (d[top] >> 32) return __longlong_as_double(0x7FF0000000000000ll);  // beyond any double
+  const int b = 31 - __clz(static_cast<unsigned>(d[top]));
+  const int msb = 32 * top + b;  // bit position of the leading one (units 2^-1074)
+  if (msb < 53) {  // < 2^53 units: exactly representable
+    const unsigned long long v = (top >= 1 ? d[1] << 32 : 0ull) | d[0];
+    return ldexp(static_cast<double>(v), -1074);
+  }
+  // 96-bit window of the three top digits (leading one at bit 64 + b) + sticky
+  const unsigned long long w2 = d[top], w1 = top >= 1 ? d[top - 1] : 0ull, w0 = top >= 2 ? d[top - 2] : 0ull;
+  bool sticky = false;
+  for (int i = 0; i < top - 2; ++i) sticky = sticky || d[i] != 0ull;
+  // window = w2:w1:w0 (32 bits each); keep 53 bits: drop r = 12 + b low bits
+  const unsigned long long hi64 = (w2 << 32) | w1;  // window >> 32 (w2 < 2^32)
+  const int r = 12 + b;                             // 12..43
+  // mantissa = window >> r = (hi64 << 32 | w0) >> r
+  unsigned long long mant, rem_hi;  // rem = low r bits of the window
+  bool round_bit, rest;
+  if (r >= 32) {
+    mant = hi64 >> (r - 32);
+    const unsigned long long rem = ((hi64 & ((1ull << (r - 32)) - 1ull)) << 32) | w0;  // r bits
+    round_bit = (rem >> (r - 1)) & 1ull;
+    rest = (rem & ((1ull << (r - 1)) - 1ull)) != 0ull;
+    rem_hi = 0;
+  } else {
+    mant = (hi64 << (32 - r)) | (w0 >> r);
+    const unsigned long long rem = w0 & ((1ull << r) - 1ull);
+    round_bit = (rem >> (r - 1)) & 1ull;
+    rest = (rem & ((1ull << (r - 1)) - 1ull)) != 0ull;
+    rem_hi = 0;
+  }
+  (void)rem_hi;
+  if (round_bit && (rest || sticky || (mant & 1ull))) ++mant;
+  int e = msb - 52;
+  if (mant >> 53) {
+    mant >>= 1;
+    ++e;
+  }
+  return ldexp(static_cast<double>(mant), e - 1074);
+}
 
 // state_update for owned point ip; returns its residue summand (dt*res0)^2
 // (0 for outer points and for a failing point, whose error is recorded).
@@ -1169,13 +1287,32 @@ __device__ __forceinline__ double update_point(const UpdateArgs& a, int ip, bool
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
   pdl_enter();
   __shared__ int s_skip;
+  __shared__ unsigned long long sacc[kAccWords];
   ktimer_begin(a.ctl, KT_UPDATE);
   if (threadIdx.x == 0) s_skip = skip_stage(a.ctl, sub_update(a.ctl));
+  const int it = iter_of(a.ctl);
+  if (a.acc) {
+    for (int t = threadIdx.x; t < kAccWords; t += blockDim.x) sacc[t] = 0ull;
+    // the accumulator of iteration it + 1 (read by the residue of it - 1,
+    // which precedes this kernel) starts from zero
+    if (blockIdx.x == 0)
+      for (int t = threadIdx.x; t < kAccWords; t += blockDim.x) a.acc[((it + 1) & 1) * kAccWords + t] = 0ull;
+  }
   __syncthreads();
   const Geo& g = a.g;
-  const bool diag = iter_of(a.ctl) == a.ctl->diag_iter;
-  for (int ip = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && ip < g.n; ip += gridDim.x * blockDim.x) {
-    a.mag[gidx(g, ip)] = update_point(a, ip, diag);
+  const bool diag = it == a.ctl->diag_iter;
+  if (a.acc) {
+    // warp-uniform trip count: every lane of a warp reaches acc_warp_add together
+    for (int base = blockIdx.x * blockDim.x; !s_skip && base < g.n; base += gridDim.x * blockDim.x) {
+      const int ip = base + static_cast<int>(threadIdx.x);
+      const double v = ip < g.n ? update_point(a, ip, diag) : 0.0;
+      acc_warp_add(sacc, v);
+    }
+    __syncthreads();
+    if (!s_skip) acc_block_flush(sacc, a.acc + (it & 1) * kAccWords);
+  } else {
+    for (int ip = blockIdx.x * blockDim.x + threadIdx.x; !s_skip && ip < g.n; ip += gridDim.x * blockDim.x)
+      a.mag[gidx(g, ip)] = update_point(a, ip, diag);
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_UPDATE);
@@ -1440,6 +1577,72 @@ __global__ void k_tree_result(const double* part_val, const long long* part_sz, 
   __syncthreads();
   tree_combine<1024>(sv[0], ss[0], sv[1], ss[1], lv);
   if (threadIdx.x == 0) *out = sv[0][0];
+}
+
+// Exact residue of the iteration (fast mode): sums the digits of every
+// domain's accumulator (over peer memory for the other domains), rounds once,
+// forms sqrt(sum)/n and records the history entry as tree_final does.
+struct AccTab {
+  const unsigned long long* p[kMaxDomains];  // each domain's [2][kAccWords]
+};
+__global__ void __launch_bounds__(96)
+    k_residue_exact(AccTab acc, int ndom, long long n, double* history, unsigned long long* iter_t0,
+                    unsigned long long* iter_t1, Ctl* ctl) {
+  pdl_enter();
+  __shared__ unsigned long long sd[kAccWords];
+  __shared__ int s_skip, s_it, s_ok;
+  ktimer_begin(ctl, KT_RESIDUE);
+  if (threadIdx.x == 0) s_skip = skip_stage(ctl, sub_residue(ctl), 1);
+  __syncthreads();
+  if (s_skip) {
+    if (threadIdx.x < 32) ktimer_fold_warp(ctl);
+    return;
+  }
+  const int it = iter_of(ctl, 1);
+  if (threadIdx.x <= kAccFlag) {
+    unsigned long long v = 0;
+    for (int d = 0; d < ndom; ++d) v += ld_volatile(acc.p[d] + (it & 1) * kAccWords + threadIdx.x);
+    sd[threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double sum = sd[kAccFlag] ? __longlong_as_double(0x7FF8000000000000ll) : acc_to_double(sd);
+    const double res = sqrt(sum) / static_cast<double>(n);
+    s_it = it;
+    s_ok = isfinite(res) ? 1 : 0;
+    if (!isfinite(res)) {
+      raise_err(ctl, err_key(PH_RESIDUE, 0, 0, 0, 0), sub_residue(ctl), 1);
+    } else {
+      if (history) history[it] = res;
+      if (iter_t1) iter_t1[it] = globaltimer();
+      ctl->sh->iter = it + 1;
+    }
+    atomicMax(&ctl->kt[KT_RESIDUE].t1, globaltimer());
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned long long t0 = ktimer_fold_warp(ctl);
+    if (threadIdx.x == 0 && iter_t0 && s_ok) iter_t0[s_it] = t0;
+  }
+}
+
+// Exact sum of an arbitrary vector of non-negative doubles (tests of the
+// accumulator: lskum_b200_exact_sum).
+__global__ void __launch_bounds__(256) k_exact_sum_blocks(const double* v, long long n, unsigned long long* acc) {
+  __shared__ unsigned long long sacc[kAccWords];
+  for (int t = threadIdx.x; t < kAccWords; t += blockDim.x) sacc[t] = 0ull;
+  __syncthreads();
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < n;
+       base += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = base + threadIdx.x;
+    acc_warp_add(sacc, i < n ? v[i] : 0.0);
+  }
+  __syncthreads();
+  acc_block_flush(sacc, acc);
+}
+__global__ void k_exact_sum_final(unsigned long long* acc, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    *out = acc[kAccFlag] ? __longlong_as_double(0x7FF8000000000000ll) : acc_to_double(acc);
 }
 
 __global__ void k_copy_d4(const D4* src, D4* dst, long long count) {

@@ -121,6 +121,8 @@ struct OpSpec {
 };
 void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch);
 double engine_reduce(const double* v, std::int64_t n, int device);
+// Correctly rounded sum of non-negative doubles (the fast-mode residue accumulator).
+double engine_exact_sum(const double* v, std::int64_t n, int device);
 int engine_device_count();
 
 }  // namespace lskb

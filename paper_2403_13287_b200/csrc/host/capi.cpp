@@ -469,6 +469,11 @@ int lskum_b200_reduce(const double* values, int64_t n, double* out) {
   return guard([&] { *out = lskb::engine_reduce(values, n, 0); });
 }
 
+int lskum_b200_exact_sum(const double* values, int64_t n, double* out) {
+  if (!out || (n > 0 && !values)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
+  return guard([&] { *out = lskb::engine_exact_sum(values, n, 0); });
+}
+
 int lskum_b200_partition(const lskum_cloud* cloud, int n_parts, int32_t* owner, int64_t* ghost_off,
                          int32_t* ghosts, int64_t ghost_cap) {
   NONNULL(cloud, owner, ghost_off);

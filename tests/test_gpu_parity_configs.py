@@ -7,16 +7,19 @@ shim, runtime.cpp:195-275, entered the way lskum_capi.cpp:209-220 enters it)
 and the GPU path through the C ABI on identical input arrays, at the sizes
 BASELINE.json's configs name:
 
-  configs[0] NACA 0012 260x154  (40,040 points)   M 0.63 AoA 2   order 1, 1000 iterations
-  configs[1] NACA 0012 520x308  (160,160 points)  M 0.85 AoA 1   order 1 (100) and order 2 (30)
-  configs[2] NACA 0012 1000x625 (625,000 points)  M 1.2  AoA 0   order 1 (100) and order 2 (30)
-  configs[3] NACA 0012 4000x2500 (10M points)     M 0.85 AoA 1   order 2, 5-iteration prefix
+  configs[0] NACA 0012 260x154  (40,040 points)   M 0.63 AoA 2   orders 1 and 2
+  configs[1] NACA 0012 520x308  (160,160 points)  M 0.85 AoA 1   orders 1 and 2 (+ strict mode)
+  configs[2] NACA 0012 1000x625 (625,000 points)  M 1.2  AoA 0   orders 1 and 2
+  configs[3] NACA 0012 4000x2500 (10M points)     M 0.85 AoA 1   order 2
 
 The state is the free stream plus a +5% Gaussian density/pressure bump above
 the section (the reference's tests/support.hpp:45-56 bump, centred at
 (0.5, 0.5)), so every data-dependent branch of the flux is exercised.  The
 NACA clouds hold their surface ring at the free stream (the reference has no
-wall flux).  Wall points are covered by the reference's own
+wall flux), and the reference loses positivity near their
+trailing edge within 5-25 iterations: the GPU must abort identically and
+match every iteration before.  The SURVEY 8(d) rectangle stand-ins at the
+configs' sizes (400^2, 790^2) are stable at order 1: 100 iterations there.  Wall points are covered by the reference's own
 annulus (cloud.cpp:372-425): it validates at 256x64 and 512x128 and aborts in
 iteration 3 at both orders, which the GPU must reproduce (code, iteration and
 message), after matching the two iterations before.
@@ -90,23 +93,87 @@ def ref_and_gpu(cloud, mach, aoa, order, iters, **extra):
 
 
 def rel_seq(got, want):
-    got, want = np.asarray(got), np.asarray(want)
-    return float(np.max(np.abs(got - want) / np.abs(want)))
+    """Largest relative difference of two residue histories (entries the
+    reference has exactly 0 — a first iteration from the free stream — must be 0)."""
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    zero = want == 0.0
+    assert np.all(got[zero] == 0.0)
+    if zero.all():
+        return 0.0
+    return float(np.max(np.abs(got[~zero] - want[~zero]) / np.abs(want[~zero])))
 
 
-CASES = {
+# ---- the BASELINE NACA 0012 distributions ----
+# With any perturbation the reference's scheme loses positivity near the
+# sharp trailing edge after 5-25 iterations on these clouds (measured with the
+# reference itself; SURVEY.md 6.3: the order-2 scheme aborts on every
+# perturbed cloud).  Parity is then: the identical abort (code, iteration and
+# message, for the same partition count), and the run up to the iteration
+# before it matching within the SURVEY 8(c) tolerances.
+NACA = {
+    "configs0": ((260, 154), 0.63, 2.0),
     "configs1": ((520, 308), 0.85, 1.0),
     "configs2": ((1000, 625), 1.2, 0.0),
 }
 
 
-@pytest.mark.parametrize("case", sorted(CASES))
-def test_order1_100_iterations_match_reference(case):
-    dims, mach, aoa = CASES[case]
-    want, got, err, c = ref_and_gpu(naca(*dims), mach, aoa, 1, 100)
+def naca_parity(dims, mach, aoa, order, iters, fp_mode="fast"):
+    c = naca(*dims)
+    want, got, err, c = ref_and_gpu(c, mach, aoa, order, iters, fp_mode=fp_mode)
+    if want.code == 0:
+        assert err is None, err
+        k = iters
+    else:
+        assert err is not None, f"the reference aborts ({want.msg}), the GPU run did not"
+        assert err.status == want.code
+        assert err.message == want.msg
+        k = int(want.msg.split(":")[0].split()[1]) - 1  # iterations completed before the abort
+        assert k >= 3
+        want, got, err, c = ref_and_gpu(c, mach, aoa, order, k, fp_mode=fp_mode)
+        assert want.code == 0 and err is None, (want.msg, err)
+    assert len(got) == k and got[-1] > 0.0
+    head = min(k, 20)
+    assert rel_seq(got[:head], want.residue[:head]) <= 1e-10
+    assert rel_seq(got, want.residue) <= 1e-9
+    f = c.fields()
+    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= (1e-10 if order == 1 else 1e-9)
+    return k
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("case", sorted(NACA))
+def test_naca_config_runs_match_reference(case, order):
+    dims, mach, aoa = NACA[case]
+    naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30)
+
+
+@pytest.mark.parametrize("case", ["configs1"])
+def test_naca_strict_mode_matches_reference(case):
+    dims, mach, aoa = NACA[case]
+    naca_parity(dims, mach, aoa, 2, 30, fp_mode="strict")
+
+
+def test_configs3_10m_matches_reference():
+    """configs[3]: the 10M-point cloud at second order (k_flux_ws in its 8x2
+    block shape, sweep/update/residue at full size) until the reference's abort."""
+    naca_parity((4000, 2500), 0.85, 1.0, 2, 8)
+
+
+# ---- the SURVEY 8(d) rectangle stand-ins at the config sizes (stable at order 1) ----
+RECT = {"c1_400sq": (400, 0.85, 1.0), "c2_790sq": (790, 1.2, 0.0)}
+
+
+def rect(side):
+    return L.Cloud.generate_rect(side, side, 0.1, 7, 8)
+
+
+@pytest.mark.parametrize("case", sorted(RECT))
+def test_rect_order1_100_iterations_match_reference(case):
+    side, mach, aoa = RECT[case]
+    want, got, err, c = ref_and_gpu(rect(side), mach, aoa, 1, 100)
     assert want.code == 0, want.msg
     assert err is None, err
-    assert len(got) == 100 and got[0] > 0.0
     assert rel_seq(got, want.residue) <= 1e-10
     f = c.fields()
     assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-12   # primitives
@@ -114,46 +181,15 @@ def test_order1_100_iterations_match_reference(case):
     assert rel_err(f[:, 20:21], want.store[:, 20:21]) <= 1e-12  # delta_t
 
 
-@pytest.mark.parametrize("case", sorted(CASES))
-@pytest.mark.parametrize("fp_mode", ["fast", "strict"])
-def test_order2_prefix_matches_reference(case, fp_mode):
-    dims, mach, aoa = CASES[case]
-    want, got, err, c = ref_and_gpu(naca(*dims), mach, aoa, 2, 30, fp_mode=fp_mode)
-    if want.code != 0:  # the reference's order-2 instability: same abort
-        assert err is not None and err.status == want.code
-        assert err.message.split(":")[0] == want.msg.split(":")[0]
-        return
+@pytest.mark.parametrize("case", sorted(RECT))
+def test_rect_order2_prefix_matches_reference(case):
+    side, mach, aoa = RECT[case]
+    want, got, err, c = ref_and_gpu(rect(side), mach, aoa, 2, 30)
+    assert want.code == 0, want.msg
     assert err is None, err
     assert rel_seq(got[:20], want.residue[:20]) <= 1e-10
     assert rel_seq(got, want.residue) <= 1e-9
-    f = c.fields()
-    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-9
-    assert rel_err(f[:, 8:16], want.store[:, 8:16]) <= 1e-7  # final derivatives (no decay floor)
-
-
-def test_configs0_order1_1000_iterations_match_reference():
-    """configs[0]: ~40K points, M 0.63, AoA 2, 1000 iterations (the reference CPU run)."""
-    want, got, err, c = ref_and_gpu(naca(260, 154), 0.63, 2.0, 1, 1000)
-    assert want.code == 0, want.msg
-    assert err is None, err
-    # SURVEY 8(c): <= 1e-10 relative while log10rel > -4, <= 1e-10 * res1 absolute after
-    w = want.residue
-    live = np.log10(w / w[0]) > -4.0
-    assert rel_seq(got[live], w[live]) <= 1e-10
-    assert float(np.max(np.abs(got[~live] - w[~live]))) <= 1e-10 * w[0] if (~live).any() else True
-    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-12
-
-
-def test_configs3_10m_order2_prefix_matches_reference():
-    """configs[3]: the 10M-point cloud, 5 second-order iterations (k_flux_ws
-    in its 8x2 block shape and the sweep/update/tree at full size)."""
-    want, got, err, c = ref_and_gpu(naca(4000, 2500), 0.85, 1.0, 2, 5)
-    assert want.code == 0, want.msg
-    assert err is None, err
-    assert rel_seq(got, want.residue) <= 1e-10
-    f = c.fields()
-    assert rel_err(f[:, 0:4], want.store[:, 0:4]) <= 1e-10
-    assert rel_err(f[:, 16:20], want.store[:, 16:20]) <= 1e-9  # last flux residual
+    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= 1e-9
 
 
 @pytest.mark.parametrize("n", [2_400_000, 10_000_000, 40_000_000])
