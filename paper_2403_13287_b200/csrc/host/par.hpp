@@ -14,15 +14,24 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 #include <vector>
 
 namespace lskb {
 
+// Host threads for setup work: all hardware threads (at most 64), or
+// LSKUM_HOST_THREADS (one process per GPU shares the host between ranks).
 inline int host_threads() {
-  const unsigned hw = std::thread::hardware_concurrency();
-  return static_cast<int>(std::clamp<unsigned>(hw == 0 ? 1 : hw, 1, 64));
+  static const int n = [] {
+    const char* e = std::getenv("LSKUM_HOST_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    if (v > 0) return std::clamp(v, 1, 64);
+    const unsigned hw = std::thread::hardware_concurrency();
+    return static_cast<int>(std::clamp<unsigned>(hw == 0 ? 1 : hw, 1, 64));
+  }();
+  return n;
 }
 
 class WorkPool {
