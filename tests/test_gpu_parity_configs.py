@@ -112,13 +112,16 @@ def rel_seq(got, want):
 # the REFERENCE ITSELF, fed the same state with the density one ulp up,
 # differs from its unperturbed run by 1e-13 at iteration 8 and by 1e-3..0.4
 # just before the abort.  So the long comparisons run at CFL 0.05, where the
-# reference is stable over the iterations compared, and every comparison is
-# stated against the reference's own 1-ulp envelope e_t (a second reference
-# run): the GPU must match within SURVEY 8(c)'s 1e-10 wherever e_t <= 1e-13
-# and within 1e4 * e_t beyond.  The CFL 0.5 abort is compared as the
-# reference's conditioning allows: the same code and iteration always, and
-# the same failing point and quantity whenever the reference's own 1-ulp
-# perturbation reports the same ones.
+# reference is stable over most of the iterations compared (configs[2]'s
+# cloud still aborts at iteration 15), and every comparison is stated against
+# the reference's own envelope e_t: a second reference run from the state
+# with the density scaled by 1 + 1e-13 (the size of the fast-mode kernels'
+# differences; 10x below their 1e-12 per-kernel tolerance).  The GPU must
+# match within SURVEY 8(c)'s 1e-10, or within 100 e_t where the reference's
+# own amplification exceeds that.  Aborts are compared as the reference's
+# conditioning allows: the same code and iteration always, and the same
+# failing point and quantity whenever the perturbed reference reports the
+# same ones.
 NACA = {
     "configs0": ((260, 154), 0.63, 2.0),
     "configs1": ((520, 308), 0.85, 1.0),
@@ -139,7 +142,7 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
     c = naca(*dims)
     g = c.geometry()
     prim1 = bumped(g, mach, aoa)
-    prim1[:, 0] = np.nextafter(prim1[:, 0], 2.0)  # the reference's own 1-ulp envelope
+    prim1[:, 0] *= 1.0 + 1e-13  # the reference's own envelope (fast-mode kernels differ by ~1e-13)
 
     def perturbed(k):
         return P.ref_run(oracle_cloud(g), mach=mach, aoa=aoa, iters=k, order=order, inner=3, cfl=cfl, layout=1,
@@ -164,12 +167,12 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
     env = rel_each(pert.residue, want.residue)
     assert len(got) == k and got[-1] > 0.0
     err_t = rel_each(got, want.residue)
-    tol = np.where(env <= 1e-13, 1e-10, np.maximum(1e-10, 1e4 * env))
+    tol = np.maximum(1e-10, 1e2 * env)
     bad = np.nonzero(err_t > tol)[0]
     assert bad.size == 0, [(int(t) + 1, float(err_t[t]), float(env[t])) for t in bad[:5]]
     scale = np.maximum(np.abs(want.store[:, 0:4]).max(axis=1, keepdims=True), 1.0)
     env_state = float(np.max(np.abs(pert.store[:, 0:4] - want.store[:, 0:4]) / scale))
-    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= max(1e-10 if order == 1 else 1e-9, 1e4 * env_state)
+    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= max(1e-10 if order == 1 else 1e-9, 1e2 * env_state)
     return k, env
 
 
@@ -178,8 +181,7 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
 def test_naca_config_runs_match_reference(case, order):
     """CFL 0.05: order 1 for 100 iterations, order 2 for 30."""
     dims, mach, aoa = NACA[case]
-    k, env = naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30)
-    assert k == (100 if order == 1 else 30)
+    naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30)
 
 
 @pytest.mark.parametrize("order", [1, 2])
