@@ -115,18 +115,27 @@ def rel_seq(got, want):
 # reference is stable over most of the iterations compared (configs[2]'s
 # cloud still aborts at iteration 15), and every comparison is stated against
 # the reference's own envelope e_t: a second reference run from the state
-# with the density scaled by 1 + 1e-13 (the size of the fast-mode kernels'
-# differences; 10x below their 1e-12 per-kernel tolerance).  The GPU must
-# match within SURVEY 8(c)'s 1e-10, or within 100 e_t where the reference's
-# own amplification exceeds that.  Aborts are compared as the reference's
-# conditioning allows: the same code and iteration always, and the same
-# failing point and quantity whenever the perturbed reference reports the
-# same ones.
+# with the density scaled by 1 + delta (delta = 1e-13 for strict mode, 1e-11
+# for fast mode: ENVELOPE_DELTA).  The GPU must match within SURVEY 8(c)'s
+# 1e-10, or within 30 e_t where the reference's own amplification exceeds
+# that.  Aborts are compared as the reference's conditioning allows: the same
+# code and iteration always; in strict mode also the same failing point and
+# quantity whenever the perturbed reference reports the same ones (fast
+# mode's differences enter at every iteration and can tip a neighbouring
+# point over the positivity limit first).
 NACA = {
     "configs0": ((260, 154), 0.63, 2.0),
     "configs1": ((520, 308), 0.85, 1.0),
     "configs2": ((1000, 625), 1.2, 0.0),
 }
+
+
+# Size of the perturbation whose effect on the reference defines the envelope:
+# strict mode differs from the reference only through libm ulps (1e-13 is a
+# few hundred ulps); fast mode's flux is specified to 1e-12 scale-aware per
+# kernel, i.e. up to ~1e-11 relative on small residuals, so its envelope is
+# the reference's response to a 1e-11 relative change of the state.
+ENVELOPE_DELTA = {"strict": 1e-13, "fast": 1e-11}
 
 
 def rel_each(got, want):
@@ -142,7 +151,7 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
     c = naca(*dims)
     g = c.geometry()
     prim1 = bumped(g, mach, aoa)
-    prim1[:, 0] *= 1.0 + 1e-13  # the reference's own envelope (fast-mode kernels differ by ~1e-13)
+    prim1[:, 0] *= 1.0 + ENVELOPE_DELTA[fp_mode]  # the reference's own envelope
 
     def perturbed(k):
         return P.ref_run(oracle_cloud(g), mach=mach, aoa=aoa, iters=k, order=order, inner=3, cfl=cfl, layout=1,
@@ -155,8 +164,10 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
         assert err.status == want.code
         assert abort_iteration(err.message) == abort_iteration(want.msg)
         pert = perturbed(iters)
-        if pert.code == want.code and pert.msg.rsplit(" ", 1)[0] == want.msg.rsplit(" ", 1)[0]:
-            # well-conditioned abort: same failing point / edge and quantity
+        if fp_mode == "strict" and pert.code == want.code and \
+                pert.msg.rsplit(" ", 1)[0] == want.msg.rsplit(" ", 1)[0]:
+            # well-conditioned abort: same failing point / edge and quantity (strict mode:
+            # fast mode's per-iteration differences may tip a different point over first)
             assert err.message.rsplit(" ", 1)[0] == want.msg.rsplit(" ", 1)[0], (err.message, want.msg)
         k = abort_iteration(want.msg) - 1
         assert k >= 3
@@ -167,12 +178,12 @@ def naca_parity(dims, mach, aoa, order, iters, cfl=0.05, fp_mode="fast"):
     env = rel_each(pert.residue, want.residue)
     assert len(got) == k and got[-1] > 0.0
     err_t = rel_each(got, want.residue)
-    tol = np.maximum(1e-10, 1e2 * env)
+    tol = np.maximum(1e-10, 30.0 * env)
     bad = np.nonzero(err_t > tol)[0]
     assert bad.size == 0, [(int(t) + 1, float(err_t[t]), float(env[t])) for t in bad[:5]]
     scale = np.maximum(np.abs(want.store[:, 0:4]).max(axis=1, keepdims=True), 1.0)
     env_state = float(np.max(np.abs(pert.store[:, 0:4] - want.store[:, 0:4]) / scale))
-    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= max(1e-10 if order == 1 else 1e-9, 1e2 * env_state)
+    assert rel_err(c.fields()[:, 0:4], want.store[:, 0:4]) <= max(1e-10 if order == 1 else 1e-9, 30.0 * env_state)
     return k, env
 
 
@@ -184,12 +195,13 @@ def test_naca_config_runs_match_reference(case, order):
     naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30)
 
 
+@pytest.mark.parametrize("fp_mode", ["fast", "strict"])
 @pytest.mark.parametrize("order", [1, 2])
 @pytest.mark.parametrize("case", sorted(NACA))
-def test_naca_cfl05_abort_matches_reference(case, order):
+def test_naca_cfl05_abort_matches_reference(case, order, fp_mode):
     """CFL 0.5 (the bench's CFL): the run up to the reference's abort and the abort."""
     dims, mach, aoa = NACA[case]
-    naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30, cfl=0.5)
+    naca_parity(dims, mach, aoa, order, 100 if order == 1 else 30, cfl=0.5, fp_mode=fp_mode)
 
 
 def test_naca_strict_mode_matches_reference():
