@@ -1,6 +1,6 @@
 """A/B timing of library builds (kernel variants) on one cloud (profiling aid).
 
-  python scripts/ab_kernels.py [--naca 4000x2500] [--reps 3] lib1.so lib2.so ...
+  python scripts/ab_kernels.py [--naca 4000x2500] [--reps 3] lib1.so lib2.so:VAR=value,VAR2=v ...
 Each build runs in its own process (LSKUM_B200_LIB): a free-stream session on
 the NACA cloud, 10 warm-up iterations, then per rep: 20 cold-L2 steps with
 kernel events (first sweep, flux) and 40 back-to-back iterations.  Prints one
@@ -25,7 +25,7 @@ for _ in range(20):
     a, b = s.event_ms()
     sw.append(a); fl.append(b)
 ms = s.iterate(40)
-print(json.dumps({"lib": os.environ.get("LSKUM_B200_LIB"), "n": c.n, "sweep_ms": statistics.median(sw),
+print(json.dumps({"lib": os.environ.get("LSKUM_B200_LIB"), "env": {k: v for k, v in os.environ.items() if k.startswith("LSKUM_") and k != "LSKUM_B200_LIB"}, "n": c.n, "sweep_ms": statistics.median(sw),
                   "flux_ms": statistics.median(fl), "step_ms_events": statistics.median(st),
                   "iter_ms": ms / 40, "kernels": [(k, round(v * 1e3 / max(n, 1), 4)) for k, v, n in s.kernels()]}))
 '''
@@ -40,8 +40,12 @@ a = ap.parse_args()
 nw, nr = (int(v) for v in a.naca.split("x"))
 code = CHILD % {"root": ROOT, "nw": nw, "nr": nr, "order": a.order, "fp": a.fp}
 for rep in range(a.reps):
-    for lib in a.libs:
+    for spec in a.libs:
+        lib, _, extra = spec.partition(":")
         env = dict(os.environ, LSKUM_B200_LIB=os.path.abspath(lib))
+        for kv in filter(None, extra.split(",")):
+            k, v = kv.split("=", 1)
+            env[k] = v
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
-        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else json.dumps({"lib": lib, "err": out.stderr[-500:]})
+        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else json.dumps({"lib": spec, "err": out.stderr[-500:]})
         print(line, flush=True)
