@@ -308,39 +308,21 @@ int resident_blocks(K kern, int slot) {
 }
 
 // The unrolled 8-point sweep in blocks of NT threads (MB resident per SM).
-template <bool S, int MB, int NT, int MODE = 0>
-void sweep8_launch_m(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                     unsigned long long* it0, int sweep, cudaStream_t st, D4* g0) {
+template <bool S, int MB, int NT>
+void sweep8_launch(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                   unsigned long long* it0, int sweep, cudaStream_t st) {
   static int resident[64] = {};  // per instantiation and device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!resident[dev & 63]) {
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep2<S, MB, 8, NT, MODE>, NT, 0), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep2<S, MB, 8, NT>, NT, 0), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int npts = g.list ? g.nlist : g.n;
   const int grid = std::max(1, std::min((2 * npts + NT - 1) / NT, resident[dev & 63]));
-  launch_pdl(k_sweep2<S, MB, 8, NT, MODE>, grid, NT, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep, g0);
-}
-template <bool S, int MB, int NT>
-void sweep8_launch(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                   unsigned long long* it0, int sweep, cudaStream_t st, int mode = 0, D4* g0 = nullptr) {
-  if constexpr (!S) {
-    if (mode == 1) return sweep8_launch_m<S, MB, NT, 1>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, g0);
-    if (mode == 2) return sweep8_launch_m<S, MB, NT, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, g0);
-  }
-  sweep8_launch_m<S, MB, NT, 0>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, nullptr);
-}
-
-// Split sweeps (k_sweep2 MODE 1/2; LSKUM_SPLIT_SWEEP=0 disables).
-bool split_sweeps_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("LSKUM_SPLIT_SWEEP");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
+  launch_pdl(k_sweep2<S, MB, 8, NT>, grid, NT, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
 }
 
 // 128-thread blocks for the unrolled sweep (default; LSKUM_SWEEP_BLOCK=256:
@@ -355,34 +337,32 @@ bool sweep_small_blocks() {
 
 template <bool S, int MB>
 void sweep_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                    unsigned long long* it0, int sweep, cudaStream_t st, int mode, D4* g0) {
+                    unsigned long long* it0, int sweep, cudaStream_t st) {
   const int slot = (S ? 4 : 0) + MB - 2;
   if (sweep_lanes() == 2 && g.kfix == 8 && sweep_unrolled()) {
-    if (sweep_small_blocks()) sweep8_launch<S, 2 * MB, 128>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, mode, g0);
-    else sweep8_launch<S, MB, 256>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, mode, g0);
+    if (sweep_small_blocks()) sweep8_launch<S, 2 * MB, 128>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep8_launch<S, MB, 256>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   } else if (sweep_lanes() == 2) {
     const int npts = g.list ? g.nlist : g.n;
     const int grid = std::max(1, std::min((2 * npts + 255) / 256, resident_blocks(k_sweep2<S, MB>, slot)));
-    launch_pdl(k_sweep2<S, MB, 0>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep,
-               static_cast<D4*>(nullptr));
+    launch_pdl(k_sweep2<S, MB, 0>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
   } else {
     const int grid = std::max(1, std::min((g.n + 255) / 256, resident_blocks(k_sweep<S, MB>, slot)));
     launch_pdl(k_sweep<S, MB>, grid, 256, 0, st, g, q, dq_in, dq_out, gas, ctl, it0, sweep);
   }
 }
 
-// mode: 0 fused sweep; 1/2 split sweeps (fast mode, 8-point stencils), see k_sweep2.
 void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                  unsigned long long* it0, int sweep, cudaStream_t st, int mode = 0, D4* g0 = nullptr) {
+                  unsigned long long* it0, int sweep, cudaStream_t st) {
   const int mb = sweep_min_blocks(sweep_lanes() == 2 && g.kfix == 8 && sweep_unrolled());
   if (strict) {
-    if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, 0, nullptr);
-    else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, 0, nullptr);
-    else sweep_launch_t<true, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, 0, nullptr);
+    if (mb == 2) sweep_launch_t<true, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else if (mb == 4) sweep_launch_t<true, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep_launch_t<true, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   } else {
-    if (mb == 2) sweep_launch_t<false, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, mode, g0);
-    else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, mode, g0);
-    else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st, mode, g0);
+    if (mb == 2) sweep_launch_t<false, 2>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
+    else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   }
 }
 
@@ -1250,8 +1230,6 @@ class Domain {
     strict_ = fp_mode == 1;
     chunk_ = std::max(1, chunk);
     if (!strict_ && flux_weighted()) ensure_weights();
-    if (!strict_ && split_sweeps_enabled() && order == 2 && inner >= 2 && kfix_ == 8 && !g0_.get())
-      g0_.alloc(2 * static_cast<std::size_t>(std::max(1, n_)), st_);  // not inside a graph capture
     if (!strict_ && order == 1 && point_flux_enabled() && !pf_.get()) {  // not inside a graph capture
       pf_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
       pfvalid_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
@@ -1375,15 +1353,8 @@ class Domain {
     Geo g = geo();
     g.list = list;
     g.nlist = nlist;
-    const int mode = split_sweeps() ? (s == 0 ? 1 : 2) : 0;
     sweep_launch(strict_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
-                 s == 0 ? it0_.get() : nullptr, s, st_, mode, g0_.get());
-  }
-  // Split sweeps (k_sweep2 MODE 1/2): fast mode, uniform 8-point stencils, the
-  // unrolled two-lane sweep, at least two sweeps per iteration.
-  bool split_sweeps() const {
-    return !strict_ && split_sweeps_enabled() && order_ == 2 && inner_ >= 2 && kfix_ == 8 && sweep_lanes() == 2 &&
-           sweep_unrolled() && g0_.get() != nullptr;
+                 s == 0 ? it0_.get() : nullptr, s, st_);
   }
   bool subsets_supported() const {
     return !strict_ && weights_ && kmax_ <= 8 && kfix_ == 8 && flux_staged() && sweep_lanes() == 2 &&
@@ -1869,7 +1840,6 @@ class Domain {
   double* mag_out_ = nullptr;
   DBuf<long long> psz_;
   DBuf<unsigned long long> acc_;
-  DBuf<D4> g0_;  // split sweeps: the q part of each point's least-squares gradient
   AccTab acc_tab_{};
   int acc_ndom_ = 1;
   DBuf<D4> prim_, q_[2], dq_[2], res_;

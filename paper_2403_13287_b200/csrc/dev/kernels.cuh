@@ -349,20 +349,10 @@ __device__ __forceinline__ int4 ld_i4(const int* p) {
   return v;
 }
 
-// MODE (fast mode, K = 8 only): the least-squares right-hand side splits into
-// a part from q, b0 = sum dx (qn - qi), which the n_inner sweeps of one
-// iteration share (q only changes in k_update), and a part from the
-// derivatives, b1 = -1/2 sum dx (dx (qxn - qxi) + dy (qyn - qyi)).  MODE 1 (the
-// iteration's first sweep) stores g0 = M b0 per point (M: the 2x2 solve) next
-// to its output M (b0 + b1); MODE 2 (the later sweeps) reads g0 and gathers
-// only the neighbours' xy and derivatives — no neighbour q — and writes
-// g0 + M b1: 29% fewer gathered bytes per sweep.  MODE 0: the fused sums.
-template <bool S, int MB, int K = 0, int NT = 256, int MODE = 0>
+template <bool S, int MB, int K = 0, int NT = 256>
 __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__ q,
                                                     const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
-                                                    Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep,
-                                                    D4* __restrict__ g0buf = nullptr) {
-  static_assert(MODE == 0 || (!S && K == 8), "split sweeps: fast mode, uniform 8-point stencils");
+                                                    Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
   pdl_enter();
   using A = Ar<S>;
   __shared__ int s_skip;
@@ -379,12 +369,11 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
     const int i = visit_point(g, static_cast<int>(t >> 1));
     const double* xyd = reinterpret_cast<const double*>(g.xy);  // read-only path (geometry is constant)
     const double2 pi = ld2(xyd + 2 * i);
-    const double2 qi = MODE == 2 ? make_double2(0.0, 0.0) : ld2(qd + 4 * i);
+    const double2 qi = ld2(qd + 4 * i);
     double2 qxi, qyi;
     ld4d(dd + 8 * i, qxi, qyi);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
-    double cx0 = 0.0, cx1 = 0.0, cy0 = 0.0, cy1 = 0.0;  // MODE 1/2: derivative part
     int e0, k;
     int nbk[K > 0 ? K : 1];
     if constexpr (K == 8) {
@@ -402,28 +391,12 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
       const int nb = K > 0 ? nbk[j] : g.nbr[e0 + j];
       const double2 pn = ld2(xyd + 2 * nb);
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const double2 qn = MODE == 2 ? make_double2(0.0, 0.0) : ld2(qd + 4 * nb);
+      const double2 qn = ld2(qd + 4 * nb);
       double2 qxn, qyn;
       ld4d(dd + 8 * nb, qxn, qyn);
       sxx = A::add(sxx, A::mul(dx, dx));
       sxy = A::add(sxy, A::mul(dx, dy));
       syy = A::add(syy, A::mul(dy, dy));
-      if constexpr (MODE != 0) {
-        const double c0 = fma(dx, qxn.x - qxi.x, dy * (qyn.x - qyi.x));
-        const double c1 = fma(dx, qxn.y - qxi.y, dy * (qyn.y - qyi.y));
-        cx0 = fma(dx, c0, cx0);
-        cy0 = fma(dy, c0, cy0);
-        cx1 = fma(dx, c1, cx1);
-        cy1 = fma(dy, c1, cy1);
-        if constexpr (MODE == 1) {
-          const double d0 = qn.x - qi.x, d1 = qn.y - qi.y;
-          bx0 = fma(dx, d0, bx0);
-          by0 = fma(dy, d0, by0);
-          bx1 = fma(dx, d1, bx1);
-          by1 = fma(dy, d1, by1);
-        }
-        continue;
-      }
       double df0, df1;
       if constexpr (S) {
         df0 = X::sub(corrected<true>(qn.x, qxn.x, qyn.x, dx, dy), corrected<true>(qi.x, qxi.x, qyi.x, dx, dy));
@@ -447,26 +420,12 @@ __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__
         fx.y = A::sub(A::mul(syy, bx1), A::mul(sxy, by1)) / det;
         fy.x = A::sub(A::mul(sxx, by0), A::mul(sxy, bx0)) / det;
         fy.y = A::sub(A::mul(sxx, by1), A::mul(sxy, bx1)) / det;
-      } else if constexpr (MODE == 0) {
+      } else {
         const double r = 1.0 / det;
         fx.x = (syy * bx0 - sxy * by0) * r;
         fx.y = (syy * bx1 - sxy * by1) * r;
         fy.x = (sxx * by0 - sxy * bx0) * r;
         fy.y = (sxx * by1 - sxy * bx1) * r;
-      } else {
-        const double r = 1.0 / det, rc = -0.5 * r;
-        D4 base;  // g0 = M b0 of this lane's components {qx, qx, qy, qy}
-        if constexpr (MODE == 1) {
-          base = D4{(syy * bx0 - sxy * by0) * r, (syy * bx1 - sxy * by1) * r, (sxx * by0 - sxy * bx0) * r,
-                    (sxx * by1 - sxy * bx1) * r};
-          st4(g0buf + 2 * static_cast<long long>(i) + h, base);
-        } else {
-          base = ld4(g0buf + 2 * static_cast<long long>(i) + h);
-        }
-        fx.x = fma(syy * cx0 - sxy * cy0, rc, base.a);
-        fx.y = fma(syy * cx1 - sxy * cy1, rc, base.b);
-        fy.x = fma(sxx * cy0 - sxy * cx0, rc, base.c);
-        fy.y = fma(sxx * cy1 - sxy * cx1, rc, base.d);
       }
       double* o = reinterpret_cast<double*>(dq_out) + 8 * static_cast<long long>(i) + 4 * h;
       st4(reinterpret_cast<D4*>(o), D4{fx.x, fx.y, fy.x, fy.y});
