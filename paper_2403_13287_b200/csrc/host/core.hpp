@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -80,6 +81,52 @@ struct NoInitAlloc : std::allocator<T> {
   }
 };
 
+// Storage of a field store.  Large stores (>= 64 MB) come from pinned host
+// memory when the engine registered an allocator (store_pinned_hooks(), set by
+// engine.cu; a process-wide pool keeps freed blocks for the next store of the
+// same size), so the copy-back DMAs straight into the store instead of through
+// staging and a host copy.  Falls back to ordinary memory (no device,
+// LSKUM_PINNED_STORE=0).  Contents are not initialised.
+struct StoreHooks {
+  void* (*alloc)(std::size_t bytes) = nullptr;    // null on failure
+  void (*release)(void* p, std::size_t bytes) = nullptr;
+};
+StoreHooks& store_hooks();
+
+class StoreBuffer {
+ public:
+  StoreBuffer() = default;
+  explicit StoreBuffer(std::size_t count) { allocate(count); }
+  StoreBuffer(const StoreBuffer& o) : StoreBuffer(o.n_) {
+    if (n_) std::memcpy(p_, o.p_, n_ * sizeof(double));
+  }
+  StoreBuffer(StoreBuffer&& o) noexcept : p_(o.p_), n_(o.n_), pinned_(o.pinned_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+    o.pinned_ = false;
+  }
+  StoreBuffer& operator=(StoreBuffer o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(pinned_, o.pinned_);
+    return *this;
+  }
+  ~StoreBuffer() { release(); }
+  double* data() { return p_; }
+  const double* data() const { return p_; }
+  std::size_t size() const { return n_; }
+  bool pinned() const { return pinned_; }
+  double& operator[](std::size_t i) { return p_[i]; }
+  double operator[](std::size_t i) const { return p_[i]; }
+
+ private:
+  void allocate(std::size_t count);
+  void release();
+  double* p_ = nullptr;
+  std::size_t n_ = 0;
+  bool pinned_ = false;
+};
+
 class FieldBlock {
  public:
   FieldBlock() = default;
@@ -95,6 +142,8 @@ class FieldBlock {
   }
   double* raw() { return data_.data(); }
   const double* raw() const { return data_.data(); }
+  // The store lives in pinned host memory (device copies may target it directly).
+  bool pinned() const { return data_.pinned(); }
 
   // Point-major (AoS) export/import regardless of the layout.
   void export_aos(double* out) const;
@@ -108,7 +157,7 @@ class FieldBlock {
   std::int32_t n_ = 0;
   // Allocated without value-initialisation; the constructor zero-fills it in
   // parallel (first touch spread over threads: hundreds of MB at 10M+ points).
-  std::vector<double, NoInitAlloc<double>> data_;
+  StoreBuffer data_;
 };
 
 // Bitwise comparison over every (point, slot) (reference layout.cpp:29-45).

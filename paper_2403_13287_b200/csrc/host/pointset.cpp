@@ -44,9 +44,38 @@ std::string fmt_f(double v) {
   return buf;
 }
 
+StoreHooks& store_hooks() {
+  static StoreHooks h;
+  return h;
+}
+
+void StoreBuffer::allocate(std::size_t count) {
+  n_ = count;
+  if (!count) return;
+  const std::size_t bytes = count * sizeof(double);
+  static const bool allow = [] {
+    const char* e = std::getenv("LSKUM_PINNED_STORE");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (allow && bytes >= (std::size_t{64} << 20) && store_hooks().alloc) {
+    p_ = static_cast<double*>(store_hooks().alloc(bytes));
+    pinned_ = p_ != nullptr;
+  }
+  if (!p_) p_ = static_cast<double*>(::operator new(bytes));
+}
+
+void StoreBuffer::release() {
+  if (!p_) return;
+  if (pinned_) store_hooks().release(p_, n_ * sizeof(double));
+  else ::operator delete(p_);
+  p_ = nullptr;
+  n_ = 0;
+  pinned_ = false;
+}
+
 FieldBlock::FieldBlock(Layout layout, std::int32_t n) : layout_(layout), n_(n) {
   if (n <= 0) raise(Status::argument, "field store needs n_points > 0, got " + std::to_string(n));
-  data_.resize(static_cast<std::size_t>(n) * slot::count);
+  data_ = StoreBuffer(static_cast<std::size_t>(n) * slot::count);
   double* d = data_.data();
   parallel_slices(static_cast<std::int64_t>(data_.size()),
                   [d](std::int64_t lo, std::int64_t hi) { std::fill(d + lo, d + hi, 0.0); }, 1 << 18);
