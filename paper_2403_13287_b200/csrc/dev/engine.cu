@@ -911,16 +911,22 @@ class Domain {
     const int tasks = std::max(1, std::min(host_threads(), static_cast<int>(nl >> 14)));
     const std::int64_t k0 = n ? gv.off[1] - gv.off[0] : 0;
     std::vector<std::int64_t> t_kmax(static_cast<std::size_t>(tasks), 1);
-    std::vector<char> t_uniform(static_cast<std::size_t>(tasks), 1);
+    std::vector<char> t_uniform(static_cast<std::size_t>(tasks), 1), t_walls(static_cast<std::size_t>(tasks), 0),
+        t_parts(static_cast<std::size_t>(tasks), 0);
     parallel_tasks(tasks, [&](int t) {
       auto part_of = [&](std::size_t len, int k) { return len * static_cast<std::size_t>(k) / tasks; };
       const std::size_t lo = part_of(nl, t), hi = part_of(nl, t + 1), c = hi - lo;
       stream_pairs(reinterpret_cast<double*>(hxy + lo), gv.x + lo, gv.y + lo, c);
       stream_pairs(reinterpret_cast<double*>(hnrm + lo), gv.nx + lo, gv.ny + lo, c);
+      char walls = 0, parts = 0;
       for (std::size_t i = lo; i < hi; ++i) {
         hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
         hpart[i] = gv.part ? gv.part[i] : 0;
+        walls |= hkind[i] == KIND_WALL;
+        parts |= hpart[i] != 0;
       }
+      t_walls[t] = walls;
+      t_parts[t] = parts;
       flush_lines(hkind + lo, c);
       flush_lines(hpart + lo, c * sizeof(std::uint16_t));
       const std::size_t olo = part_of(n, t), ohi = part_of(n, t + 1);
@@ -968,10 +974,20 @@ class Domain {
     trace_sync(st_, "domain: geometry buffers allocated");
     ck(cudaMemcpyAsync(xy_.get(), hxy, b_xy, cudaMemcpyHostToDevice, st_), "H2D xy");
     trace_sync(st_, "domain: xy copied");
-    ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
+    // normals are only read for wall points, partition ids only on the failure
+    // path: clouds without walls / with one partition skip those transfers
+    const bool any_wall = std::any_of(t_walls.begin(), t_walls.end(), [](char c) { return c != 0; });
+    const bool any_part = std::any_of(t_parts.begin(), t_parts.end(), [](char c) { return c != 0; });
+    if (any_wall) ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
+    else ck(cudaMemsetAsync(nrm_.get(), 0, b_xy, st_), "zero nrm");
     ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
-    ck(cudaMemcpyAsync(part_.get(), hpart, nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_), "H2D part");
-    part_host_.assign(hpart, hpart + nl);
+    if (any_part) {
+      ck(cudaMemcpyAsync(part_.get(), hpart, nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_), "H2D part");
+      part_host_.assign(hpart, hpart + nl);
+    } else {
+      ck(cudaMemsetAsync(part_.get(), 0, nl * sizeof(std::uint16_t), st_), "zero part");
+      part_host_.clear();  // empty = all partition ids 0
+    }
     ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
     trace_sync(st_, "domain: nrm kind part off copied");
     if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
@@ -1360,15 +1376,21 @@ class Domain {
       clear_graphs();
     }
     const std::size_t nl = static_cast<std::size_t>(n_loc_);
+    if (!part && part_host_.empty()) return;  // one partition before and now (the common case)
     std::vector<std::uint16_t> hp(nl, 0);
     if (part)
       for (std::size_t i = 0; i < nl; ++i) hp[i] = part[gid_host_.empty() ? i : static_cast<std::size_t>(gid_host_[i])];
-    if (hp != part_host_) {
+    const bool zero = std::all_of(hp.begin(), hp.end(), [](std::uint16_t v) { return v == 0; });
+    if (zero && part_host_.empty()) return;
+    if (zero) {
+      part_host_.clear();
+      ck(cudaMemsetAsync(part_.get(), 0, nl * sizeof(std::uint16_t), st_), "zero part");
+    } else if (hp != part_host_) {
       part_host_ = hp;
       ck(cudaMemcpyAsync(part_.get(), part_host_.data(), nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_),
          "H2D part");
-      ck(cudaStreamSynchronize(st_), "part");
     }
+    ck(cudaStreamSynchronize(st_), "part");
   }
 
   // Geometry-only split-stencil weights for the fast flux kernel (once per
