@@ -137,6 +137,11 @@ int lskum_b200_session_kernel_stats(const lskum_b200_session* s, int index, doub
 /* Kernel launches per iteration and the CUDA stream (cudaStream_t as integer). */
 int lskum_b200_session_info(const lskum_b200_session* s, int* launches_per_iter,
                             uint64_t* stream);
+/* Tiled derivative sweep (engine tiles.cuh): tiles whose stencil union is
+ * staged in shared memory, and all tiles, summed over the session's domains
+ * (0/0: the run has no tile plan — first order, non-uniform stencils or
+ * LSKUM_SWEEP_TILE=0). */
+int lskum_b200_session_tiles(const lskum_b200_session* s, int* staged, int* total);
 int lskum_b200_session_download(lskum_b200_session* s);
 /* CUDA-event milliseconds of the first derivative sweep and of the flux
  * kernel of the latest lskum_b200_session_step_flushed(kernel_events = 1)

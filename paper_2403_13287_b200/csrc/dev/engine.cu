@@ -26,6 +26,7 @@
 
 #include "../engine.hpp"
 #include "kernels.cuh"
+#include "tiles.cuh"
 #include "../host/par.hpp"
 
 namespace lskb {
@@ -421,6 +422,60 @@ void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* d
   }
 }
 
+// Tiled sweep (tiles.cuh) for uniform 8-point stencils.  LSKUM_SWEEP_TILE
+// selects the tile shape: 128 (default) = tiles of 128 points, 256-thread
+// blocks, 2 resident per SM, each with 2 stages of up to 480 staged points
+// (2 x 55.9 KB); 64 = tiles of 64 points, 128-thread blocks, 4 per SM, 2
+// stages of up to 216 points (2 x 25.3 KB); 0 = untiled sweep.  A ring
+// cloud's tile stages ~3 x (TP + 4) points (its row and the rows above and below).
+template <int TP>
+struct TileShape;
+template <>
+struct TileShape<128> {
+  static constexpr int MB = 2, smax = 480;
+};
+template <>
+struct TileShape<64> {
+  static constexpr int MB = 4, smax = 216;
+};
+int sweep_tile_p() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_SWEEP_TILE");
+    if (!e) return 128;
+    const int t = std::atoi(e);
+    return t == 0 ? 0 : (t == 64 ? 64 : 128);
+  }();
+  return v;
+}
+
+template <bool S, int TP>
+void sweep_tile_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl, int sweep,
+                         const TilePlan* plan, const std::uint16_t* slot, int ntiles, cudaStream_t st) {
+  constexpr int MB = TileShape<TP>::MB, smax = TileShape<TP>::smax;
+  constexpr std::size_t smem = 2 * tile_stage_bytes(TP, smax);
+  auto kern = k_sweep_tile<S, TP, MB>;
+  static int resident[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!resident[dev & 63]) {
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+       "cudaFuncSetAttribute(k_sweep_tile)");
+    int per_sm = 0, sms = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * TP, smem), "occupancy");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    resident[dev & 63] = std::max(1, per_sm) * sms;
+  }
+  const int grid = std::max(1, std::min(ntiles, resident[dev & 63]));
+  launch_pdl(kern, grid, 2 * TP, smem, st, g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, smax, ntiles);
+}
+
+template <bool S>
+void sweep_tile_launch(int tp, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
+                       int sweep, const TilePlan* plan, const std::uint16_t* slot, int ntiles, cudaStream_t st) {
+  if (tp == 64) sweep_tile_launch_t<S, 64>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, st);
+  else sweep_tile_launch_t<S, 128>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, st);
+}
+
 // Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per
 // SM (LSKUM_FLUX_MINB = 2 | 3, default 2: 128 registers, no spills).
 int flux_min_blocks() {
@@ -608,8 +663,8 @@ __global__ void k_diagnose(Geo g, const D4* q, const D4* dq, const D4* prim, con
   const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
   const D4 qi = q[i], qn = q[nb];
   D4 qxi, qyi, qxn, qyn;
-  dq_load(dq, i, qxi, qyi);
-  dq_load(dq, nb, qxn, qyn);
+  dq_load(dq, g.nloc, i, qxi, qyi);
+  dq_load(dq, g.nloc, nb, qxn, qyn);
   double ti[4], tn[4];
   for (int c = 0; c < 4; ++c) {
     ti[c] = corrected<S>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
@@ -668,12 +723,12 @@ __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter
 
 // Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
 // major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
-__global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, const D4* res,
-                              const double* dt, const int* gid, double* out) {
+__global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, long long dq_ps,
+                              const D4* res, const double* dt, const int* gid, double* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int p = gid ? gid[i] : i;  // position in the store
     D4 qx, qy;
-    dq_load(dq, i, qx, qy);
+    dq_load(dq, dq_ps, i, qx, qy);
     const D4 v[5] = {prim[i], q[i], qx, qy, res[i]};
     double r[21];
 #pragma unroll
@@ -753,16 +808,16 @@ __global__ void k_screen(Geo g, double tol, ScreenOut* out, int* defective, int 
   atomicMin(&out->min_size, fc);
 }
 
-// Derivative records <-> the reference's scratch layout [qx0..3, qy0..3]:
-// to_records = 1: plain -> records, 0: records -> plain.
-__global__ void k_dq_layout(const D4* in, D4* out, long long n, int to_records) {
+// Derivative planes (plane stride ps) <-> the reference's scratch layout
+// [qx0..3, qy0..3] per point: to_records = 1: plain -> planes, 0: planes -> plain.
+__global__ void k_dq_layout(const D4* in, D4* out, long long n, long long ps, int to_records) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   if (to_records) {
-    dq_store(out, i, ld4(in + 2 * i), ld4(in + 2 * i + 1));
+    dq_store(out, ps, i, ld4(in + 2 * i), ld4(in + 2 * i + 1));
   } else {
     D4 qx, qy;
-    dq_load(in, i, qx, qy);
+    dq_load(in, ps, i, qx, qy);
     st4(out + 2 * i, qx);
     st4(out + 2 * i + 1, qy);
   }
@@ -1058,6 +1113,7 @@ class Domain {
     g.gid = gid_.get();
     g.n = n_;
     g.kfix = kfix_;
+    g.nloc = n_loc_;
     return g;
   }
 
@@ -1186,17 +1242,17 @@ class Domain {
       const int p = static_cast<int>(i);
       hp[i] = D4{f.at(p, slot::prim), f.at(p, slot::prim + 1), f.at(p, slot::prim + 2), f.at(p, slot::prim + 3)};
       hp[n + i] = D4{f.at(p, slot::q), f.at(p, slot::q + 1), f.at(p, slot::q + 2), f.at(p, slot::q + 3)};
-      // derivative records per component pair (dq_load/dq_store layout)
-      hp[2 * n + 2 * i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qy), f.at(p, slot::qy + 1)};
-      hp[2 * n + 2 * i + 1] =
-          D4{f.at(p, slot::qx + 2), f.at(p, slot::qx + 3), f.at(p, slot::qy + 2), f.at(p, slot::qy + 3)};
+      // derivative planes (dq_load/dq_store layout): qx records, then qy records
+      hp[2 * n + i] = D4{f.at(p, slot::qx), f.at(p, slot::qx + 1), f.at(p, slot::qx + 2), f.at(p, slot::qx + 3)};
+      hp[3 * n + i] = D4{f.at(p, slot::qy), f.at(p, slot::qy + 1), f.at(p, slot::qy + 2), f.at(p, slot::qy + 3)};
       hp[4 * n + i] =
           D4{f.at(p, slot::res), f.at(p, slot::res + 1), f.at(p, slot::res + 2), f.at(p, slot::res + 3)};
       reinterpret_cast<double*>(hp + 5 * n)[i] = f.at(p, slot::dt);
     }
     ck(cudaMemcpyAsync(prim_.get(), hp, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D prim");
     ck(cudaMemcpyAsync(q_[0].get(), hp + n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D q");
-    ck(cudaMemcpyAsync(dq_[0].get(), hp + 2 * n, 2 * n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D dq");
+    ck(cudaMemcpyAsync(dq_[0].get(), hp + 2 * n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D qx");
+    ck(cudaMemcpyAsync(dq_[0].get() + n_loc_, hp + 3 * n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D qy");
     ck(cudaMemcpyAsync(res_.get(), hp + 4 * n, n * sizeof(D4), cudaMemcpyHostToDevice, st_), "H2D res");
     ck(cudaMemcpyAsync(dt_.get(), hp + 5 * n, n * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D dt");
     ck(cudaStreamSynchronize(st_), "upload");
@@ -1209,7 +1265,8 @@ class Domain {
       // the domain is a permutation of the whole cloud), one D2H into the store
       DBuf<double> packed(21 * n, st_);
       k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
-          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, res_.get(), dt_.get(),
+          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(),
+          dt_.get(),
           static_cast<const int*>(gid_.get()), packed.get());
       ck(cudaGetLastError(), "k_pack_fields");
       trace_sync(st_, "download: packed");
@@ -1264,7 +1321,8 @@ class Domain {
     D4* hp = h.data();
     ck(cudaMemcpyAsync(hp, prim_.get(), n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H prim");
     if (with_q) ck(cudaMemcpyAsync(hp + n, qsrc, n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H q");
-    ck(cudaMemcpyAsync(hp + 2 * n, dqsrc, 2 * n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H dq");
+    ck(cudaMemcpyAsync(hp + 2 * n, dqsrc, n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H qx");
+    ck(cudaMemcpyAsync(hp + 3 * n, dqsrc + n_loc_, n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H qy");
     ck(cudaMemcpyAsync(hp + 4 * n, res_.get(), n * sizeof(D4), cudaMemcpyDeviceToHost, st_), "D2H res");
     ck(cudaMemcpyAsync(hp + 5 * n, dt_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, st_), "D2H dt");
     ck(cudaStreamSynchronize(st_), "download");
@@ -1283,9 +1341,8 @@ class Domain {
         f.at(p, slot::q + 2) = q.c;
         f.at(p, slot::q + 3) = q.d;
       }
-      const D4& r0 = hp[2 * n + 2 * i];
-      const D4& r1 = hp[2 * n + 2 * i + 1];
-      const D4 qx{r0.a, r0.b, r1.a, r1.b}, qy{r0.c, r0.d, r1.c, r1.d};
+      const D4& qx = hp[2 * n + i];
+      const D4& qy = hp[3 * n + i];
       const D4& r = hp[4 * n + i];
       for (int c = 0; c < 4; ++c) {
         f.at(p, slot::qx + c) = comp(qx, c);
@@ -1308,6 +1365,7 @@ class Domain {
     strict_ = fp_mode == 1;
     chunk_ = std::max(1, chunk);
     if (!strict_ && flux_weighted()) ensure_weights();
+    if (order == 2) ensure_tiles();
     if (!strict_ && order == 1 && point_flux_enabled() && !pf_.get()) {  // not inside a graph capture
       pf_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
       pfvalid_.alloc(static_cast<std::size_t>(std::max(1, n_loc_)), st_);
@@ -1437,9 +1495,41 @@ class Domain {
     Geo g = geo();
     g.list = list;
     g.nlist = nlist;
+    if (!list && tiles_) {
+      if (strict_)
+        sweep_tile_launch<true>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
+                                tplan_.get(), tslot_.get(), ntiles_, st_);
+      else
+        sweep_tile_launch<false>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
+                                 tplan_.get(), tslot_.get(), ntiles_, st_);
+      return;
+    }
     sweep_launch(strict_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
                  s == 0 ? it0_.get() : nullptr, s, st_);
   }
+  // Tile plan of the tiled sweep (geometry only, once per domain; uniform
+  // 8-point stencils).  Returns the number of tiles that are staged.
+  int ensure_tiles() {
+    if (tiles_ || kfix_ != 8 || n_ <= 0 || sweep_tile_p() == 0) return tiles_staged_;
+    tile_p_ = sweep_tile_p();
+    ntiles_ = (n_ + tile_p_ - 1) / tile_p_;
+    tplan_.alloc(static_cast<std::size_t>(ntiles_), st_);
+    tslot_.alloc(static_cast<std::size_t>(n_) * 8, st_);
+    if (tile_p_ == 64)
+      k_tile_plan<64><<<ntiles_, 64, 0, st_>>>(geo(), TileShape<64>::smax, tplan_.get(), tslot_.get());
+    else
+      k_tile_plan<128><<<ntiles_, 128, 0, st_>>>(geo(), TileShape<128>::smax, tplan_.get(), tslot_.get());
+    ck(cudaGetLastError(), "k_tile_plan");
+    std::vector<TilePlan> h(static_cast<std::size_t>(ntiles_));
+    ck(cudaMemcpyAsync(h.data(), tplan_.get(), h.size() * sizeof(TilePlan), cudaMemcpyDeviceToHost, st_), "D2H tiles");
+    ck(cudaStreamSynchronize(st_), "tile plan");
+    tiles_staged_ = static_cast<int>(std::count_if(h.begin(), h.end(), [](const TilePlan& t) { return t.nint > 0; }));
+    trace("engine: tile plan");
+    tiles_ = true;
+    return tiles_staged_;
+  }
+  int tiles_staged() const { return tiles_staged_; }
+  int tiles_total() const { return ntiles_; }
   bool subsets_supported() const {
     return !strict_ && weights_ && kmax_ <= 8 && kfix_ == 8 && flux_staged() && sweep_lanes() == 2 &&
            sweep_unrolled();
@@ -1504,14 +1594,15 @@ class Domain {
                static_cast<const long long*>(psz_.get()), d1_, n_res_, hist_.get(), it0_.get(), it1_.get(),
                ctl_.get());
   }
-  // Halo gather of `recs` records per point from the owners' buffers, as
-  // part of stage `sub` of the iteration (0: q; 1+s: derivatives of sweep s).
-  void launch_halo(D4* dst, int recs, const int* hdom, const int* hidx, const PeerTab& src, int sub,
+  // Halo gather of `planes` record planes per point (q: 1, dq: 2) from the
+  // owners' buffers, as part of stage `sub` of the iteration (0: q; 1+s:
+  // derivatives of sweep s).
+  void launch_halo(D4* dst, int planes, const int* hdom, const int* hidx, const PeerTab& src, int sub,
                    bool skip_first = false) {
     const int nh = n_loc_ - n_;
     if (nh <= 0) return;
-    k_halo<<<std::min((nh * recs + 255) / 256, 4096), 256, 0, st_>>>(dst, recs, n_, nh, hdom, hidx, src,
-                                                                       ctl_.get(), sub, skip_first ? 1 : 0);
+    k_halo<<<std::min((nh * planes + 255) / 256, 4096), 256, 0, st_>>>(dst, n_loc_, planes, n_, nh, hdom, hidx,
+                                                                         src, ctl_.get(), sub, skip_first ? 1 : 0);
   }
 
   // One iteration starting at parity (a, b); `timed` brackets the first sweep
@@ -1929,6 +2020,10 @@ class Domain {
   DBuf<D4> prim_, q_[2], dq_[2], res_;
   std::int64_t nnz_ = 0;
   DBuf<double2> w1_, w2_;       // least-squares weights of the split stencils (fast mode)
+  DBuf<TilePlan> tplan_;        // tile plan of the tiled sweep (tiles.cuh)
+  DBuf<std::uint16_t> tslot_;
+  int ntiles_ = 0, tiles_staged_ = 0, tile_p_ = 128;
+  bool tiles_ = false;
   DBuf<PointFlux> pf_;           // first order: split fluxes per point (owned + halo)
   DBuf<std::uint8_t> psign_;     // first order: half-stencil signs / zero offset per pair
   DBuf<std::uint8_t> pfvalid_;
@@ -2239,6 +2334,12 @@ class MultiRun {
   }
 
   Domain& root() { return *dom_[0]; }
+  void tiles(int* staged, int* total) const {
+    for (const auto& d : dom_) {
+      *staged += d->tiles_staged();
+      *total += d->tiles_total();
+    }
+  }
   int launches_per_iter() const {
     return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 3) + (spec_.fp_mode == 1 ? 2 : 1);
   }
@@ -2334,12 +2435,18 @@ class MultiRun {
   void wait(int d, cudaEvent_t e) { ck(cudaStreamWaitEvent(dom_[d]->stream(), e, 0), "StreamWaitEvent"); }
   PeerTab peers_q(int a) const {
     PeerTab tb{};
-    for (int o = 0; o < P_; ++o) tb.base[o] = dom_[o]->q_buf(a);
+    for (int o = 0; o < P_; ++o) {
+      tb.base[o] = dom_[o]->q_buf(a);
+      tb.ps[o] = dom_[o]->n_loc();
+    }
     return tb;
   }
   PeerTab peers_dq(int b) const {
     PeerTab tb{};
-    for (int o = 0; o < P_; ++o) tb.base[o] = dom_[o]->dq_buf(b);
+    for (int o = 0; o < P_; ++o) {
+      tb.base[o] = dom_[o]->dq_buf(b);
+      tb.ps[o] = dom_[o]->n_loc();
+    }
     return tb;
   }
 
@@ -2472,7 +2579,7 @@ __global__ void k_wait(WaitList w, long long mult, long long add, Ctl* ctl, int 
 }
 
 struct RankBlob {
-  int rank = 0, world = 0, device = 0, pad = 0;
+  int rank = 0, world = 0, device = 0, nloc = 0;  // nloc: plane stride of the rank's dq buffers
   cudaIpcMemHandle_t q[2], dq[2], flags, sh, mag, acc;
 };
 
@@ -2547,6 +2654,7 @@ class RankRun {
     blob_.rank = rank;
     blob_.world = world;
     blob_.device = device;
+    blob_.nloc = dom_->n_loc();
     ck(cudaIpcGetMemHandle(&blob_.q[0], dom_->q_buf(0)), "IpcGetMemHandle q0");
     ck(cudaIpcGetMemHandle(&blob_.q[1], dom_->q_buf(1)), "IpcGetMemHandle q1");
     ck(cudaIpcGetMemHandle(&blob_.dq[0], dom_->dq_buf(0)), "IpcGetMemHandle dq0");
@@ -2582,6 +2690,7 @@ class RankRun {
         for (int k = 0; k < 2; ++k) {
           qp_[k].base[o] = dom_->q_buf(k);
           dqp_[k].base[o] = dom_->dq_buf(k);
+          qp_[k].ps[o] = dqp_[k].ps[o] = dom_->n_loc();
         }
         flag_[o] = flags_.get();
         continue;
@@ -2590,6 +2699,7 @@ class RankRun {
       for (int k = 0; k < 2; ++k) {
         qp_[k].base[o] = open(open_ipc<D4>(b.q[k]));
         dqp_[k].base[o] = open(open_ipc<D4>(b.dq[k]));
+        qp_[k].ps[o] = dqp_[k].ps[o] = b.nloc;
       }
       flag_[o] = open(open_ipc<unsigned long long>(b.flags));
       if (rank_ == 0) acc.p[o] = open(open_ipc<unsigned long long>(b.acc));
@@ -2956,6 +3066,15 @@ std::vector<KernelTime> session_kernels(const Session* s) { return s->head().ker
 int session_launches_per_iter(const Session* s) {
   return s->multi ? s->multi->launches_per_iter() : s->dom->launches_per_iter();
 }
+void session_tiles(const Session* s, int* staged, int* total) {
+  *staged = *total = 0;
+  if (s->multi) {
+    s->multi->tiles(staged, total);
+  } else {
+    *staged = s->dom->tiles_staged();
+    *total = s->dom->tiles_total();
+  }
+}
 std::uint64_t session_stream(const Session* s) { return reinterpret_cast<std::uint64_t>(s->head().stream()); }
 void session_download(Session* s) {
   if (s->multi) s->multi->download();
@@ -3052,7 +3171,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
     case Op::publish:  // scratch is the reference's [qx0..3, qy0..3] per point
       ck(cudaMemcpyAsync(d.dq_buf(1), scratch, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D scratch");
       k_dq_layout<<<static_cast<int>((nn + 255) / 256), 256, 0, st>>>(d.dq_buf(1), d.dq_buf(0),
-                                                                     static_cast<long long>(nn), 1);
+                                                                     static_cast<long long>(nn), g.nloc, 1);
       break;
     case Op::flux_fused:
     case Op::flux_direction: {
@@ -3084,7 +3203,7 @@ void engine_op(PointSet& ps, Op op, const OpSpec& spec, double* scratch) {
   if (op == Op::q_derivatives) {
     DBuf<D4> plain(2 * nn, st);
     k_dq_layout<<<static_cast<int>((nn + 255) / 256), 256, 0, st>>>(d.dq_buf(1), plain.get(),
-                                                                   static_cast<long long>(nn), 0);
+                                                                   static_cast<long long>(nn), g.nloc, 0);
     ck(cudaMemcpyAsync(scratch, plain.get(), nn * 8 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H scratch");
     ck(cudaStreamSynchronize(st), "scratch");
     return;  // the store itself is untouched (reference kernels.hpp:30-35)

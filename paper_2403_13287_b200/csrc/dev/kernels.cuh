@@ -115,6 +115,7 @@ struct Geo {
   const int* gid;  // local -> global point id (null: local ids are global)
   int n;           // owned points (kernels loop over these)
   int kfix;        // uniform stencil size (offsets are then i*kfix), 0 = use CSR offsets
+  long long nloc;  // owned + halo points: the plane stride of the dq buffers (dq_load)
   // Optional subset of the owned points (k_sweep2, k_flux_ws): when set, the
   // kernel visits points list[0..nlist) instead of 0..n — interior points
   // before the halo arrives, boundary points after.
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
     const double2 pi = g.xy[i];
     const D4 qi = ld4(q + i);
     D4 qxi, qyi;
-    dq_load(dq_in, i, qxi, qyi);
+    dq_load(dq_in, g.nloc, i, qxi, qyi);
     double sxx = 0.0, sxy = 0.0, syy = 0.0;
     double bx[4] = {0.0, 0.0, 0.0, 0.0}, by[4] = {0.0, 0.0, 0.0, 0.0};
     int e0, k;
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
       const D4 qn = ld4(q + nb);
       D4 qxn, qyn;
-      dq_load(dq_in, nb, qxn, qyn);
+      dq_load(dq_in, g.nloc, nb, qxn, qyn);
       sxx = A::add(sxx, A::mul(dx, dx));
       sxy = A::add(sxy, A::mul(dx, dy));
       syy = A::add(syy, A::mul(dy, dy));
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(256, MB) k_sweep(Geo g, const D4* __restrict__
       fy.b = A::sub(A::mul(sxx, by[1]), A::mul(sxy, bx[1])) / det;
       fy.c = A::sub(A::mul(sxx, by[2]), A::mul(sxy, bx[2])) / det;
       fy.d = A::sub(A::mul(sxx, by[3]), A::mul(sxy, bx[3])) / det;
-      dq_store(dq_out, i, fx, fy);
+      dq_store(dq_out, g.nloc, i, fx, fy);
     }
   }
   __syncthreads();
@@ -332,10 +333,6 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
-// One 32-byte load split into its two 16-byte halves.
-__device__ __forceinline__ void ld4d(const double* p, double2& lo, double2& hi) {
-  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y) : "l"(p));
-}
 __device__ __forceinline__ void st2(double* p, double2 v) {
   asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
@@ -349,86 +346,139 @@ __device__ __forceinline__ int4 ld_i4(const int* p) {
   return v;
 }
 
+// Global-memory neighbour source of the two-lane sweep: lane h reads its
+// halves {2h, 2h+1} of q, qx and qy (bases offset by 2h doubles).
+struct GlobalSrc {
+  const double* xy;
+  const double* q;
+  const double* qx;
+  const double* qy;
+  __device__ __forceinline__ void get(int s, double2& p, double2& qv, double2& x, double2& y) const {
+    p = ld2(xy + 2 * s);
+    qv = ld2(q + 4 * s);
+    x = ld2(qx + 4 * s);
+    y = ld2(qy + 4 * s);
+  }
+};
+
+// Sweep arithmetic of one (point, neighbour) term and of the solve.  S = true:
+// the reference's sequence, every product and sum rounded; S = false: the
+// same sums with explicit FMAs (fixed contraction, so every kernel that uses
+// these helpers produces bitwise the same derivatives).
+template <bool S>
+__device__ __forceinline__ void sweep_term(double2 pi, double2 qi, double2 qxi, double2 qyi, double2 pn, double2 qn,
+                                           double2 qxn, double2 qyn, double& sxx, double& sxy, double& syy,
+                                           double& bx0, double& bx1, double& by0, double& by1) {
+  const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+  if constexpr (S) {
+    sxx = X::add(sxx, X::mul(dx, dx));
+    sxy = X::add(sxy, X::mul(dx, dy));
+    syy = X::add(syy, X::mul(dy, dy));
+    const double df0 = X::sub(corrected<true>(qn.x, qxn.x, qyn.x, dx, dy), corrected<true>(qi.x, qxi.x, qyi.x, dx, dy));
+    const double df1 = X::sub(corrected<true>(qn.y, qxn.y, qyn.y, dx, dy), corrected<true>(qi.y, qxi.y, qyi.y, dx, dy));
+    bx0 = X::add(bx0, X::mul(dx, df0));
+    by0 = X::add(by0, X::mul(dy, df0));
+    bx1 = X::add(bx1, X::mul(dx, df1));
+    by1 = X::add(by1, X::mul(dy, df1));
+  } else {
+    sxx = fma(dx, dx, sxx);
+    sxy = fma(dx, dy, sxy);
+    syy = fma(dy, dy, syy);
+    const double df0 = fma(-0.5, fma(dx, __dsub_rn(qxn.x, qxi.x), __dmul_rn(dy, __dsub_rn(qyn.x, qyi.x))),
+                           __dsub_rn(qn.x, qi.x));
+    const double df1 = fma(-0.5, fma(dx, __dsub_rn(qxn.y, qxi.y), __dmul_rn(dy, __dsub_rn(qyn.y, qyi.y))),
+                           __dsub_rn(qn.y, qi.y));
+    bx0 = fma(dx, df0, bx0);
+    by0 = fma(dy, df0, by0);
+    bx1 = fma(dx, df1, bx1);
+    by1 = fma(dy, df1, by1);
+  }
+}
+
+// Solve and store (lane h writes its halves of the qx and qy planes); false
+// when the stencil is singular (the caller raises).
+template <bool S>
+__device__ __forceinline__ bool sweep_solve(double sxx, double sxy, double syy, double bx0, double bx1, double by0,
+                                            double by1, double det_tol, D4* __restrict__ dq_out, long long ps, int i,
+                                            int h) {
+  using A = Ar<S>;
+  double det;
+  double2 fx, fy;
+  if constexpr (S) {
+    det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
+    if (!(det > det_tol)) return false;
+    fx.x = A::sub(A::mul(syy, bx0), A::mul(sxy, by0)) / det;
+    fx.y = A::sub(A::mul(syy, bx1), A::mul(sxy, by1)) / det;
+    fy.x = A::sub(A::mul(sxx, by0), A::mul(sxy, bx0)) / det;
+    fy.y = A::sub(A::mul(sxx, by1), A::mul(sxy, bx1)) / det;
+  } else {
+    det = fma(sxx, syy, -__dmul_rn(sxy, sxy));
+    if (!(det > det_tol)) return false;
+    const double r = 1.0 / det;
+    fx.x = __dmul_rn(fma(syy, bx0, -__dmul_rn(sxy, by0)), r);
+    fx.y = __dmul_rn(fma(syy, bx1, -__dmul_rn(sxy, by1)), r);
+    fy.x = __dmul_rn(fma(sxx, by0, -__dmul_rn(sxy, bx0)), r);
+    fy.y = __dmul_rn(fma(sxx, by1, -__dmul_rn(sxy, bx1)), r);
+  }
+  st2(reinterpret_cast<double*>(dq_out + i) + 2 * h, fx);
+  st2(reinterpret_cast<double*>(dq_out + ps + i) + 2 * h, fy);
+  return true;
+}
+
+// One point of the two-lane sweep over a uniform 8-point stencil; nbr[j]
+// indexes the source (global id, or a staged slot in tiles.cuh).
+template <bool S, class Src>
+__device__ __forceinline__ void sweep_point8(const Src& src, int self, const int (&nbr)[8], const Geo& g, int i, int h,
+                                             D4* __restrict__ dq_out, const Gas& gas, Ctl* ctl, int sweep) {
+  double2 pi, qi, qxi, qyi;
+  src.get(self, pi, qi, qxi, qyi);
+  double sxx = 0.0, sxy = 0.0, syy = 0.0, bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double2 pn, qn, qxn, qyn;
+    src.get(nbr[j], pn, qn, qxn, qyn);
+    sweep_term<S>(pi, qi, qxi, qyi, pn, qn, qxn, qyn, sxx, sxy, syy, bx0, bx1, by0, by1);
+  }
+  if (!sweep_solve<S>(sxx, sxy, syy, bx0, bx1, by0, by1, gas.det_tol, dq_out, g.nloc, i, h) && h == 0)
+    raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0), 1 + sweep);
+}
+
 template <bool S, int MB, int K = 0, int NT = 256>
 __global__ void __launch_bounds__(NT, MB) k_sweep2(Geo g, const D4* __restrict__ q,
                                                     const D4* __restrict__ dq_in, D4* __restrict__ dq_out,
                                                     Gas gas, Ctl* ctl, unsigned long long* iter_t0, int sweep) {
   pdl_enter();
-  using A = Ar<S>;
   __shared__ int s_skip;
   ktimer_begin(ctl, kt_sweep(sweep));
   if (threadIdx.x == 0) s_skip = skip_stage(ctl, 1 + sweep);
   __syncthreads();
   const int h = threadIdx.x & 1;
-  const double* qd = reinterpret_cast<const double*>(q) + 2 * h;
-  const double* dd = reinterpret_cast<const double*>(dq_in) + 4 * h;  // {qx, qy} of this lane's pair
+  const GlobalSrc src{reinterpret_cast<const double*>(g.xy), reinterpret_cast<const double*>(q) + 2 * h,
+                      reinterpret_cast<const double*>(dq_in) + 2 * h,
+                      reinterpret_cast<const double*>(dq_in + g.nloc) + 2 * h};
   const long long n2 = 2ll * visit_count(g);
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   for (; !s_skip && t < n2; t += stride) {
     const int i = visit_point(g, static_cast<int>(t >> 1));
-    const double* xyd = reinterpret_cast<const double*>(g.xy);  // read-only path (geometry is constant)
-    const double2 pi = ld2(xyd + 2 * i);
-    const double2 qi = ld2(qd + 4 * i);
-    double2 qxi, qyi;
-    ld4d(dd + 8 * i, qxi, qyi);
-    double sxx = 0.0, sxy = 0.0, syy = 0.0;
-    double bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
-    int e0, k;
-    int nbk[K > 0 ? K : 1];
     if constexpr (K == 8) {
       // ids in two 16-byte loads (loading them a point ahead measured 2% slower)
-      e0 = 8 * i;
-      k = 8;
-      const int4 na0 = ld_i4(g.nbr + e0), na1 = ld_i4(g.nbr + e0 + 4);
-      nbk[0] = na0.x, nbk[1] = na0.y, nbk[2] = na0.z, nbk[3] = na0.w;
-      nbk[4] = na1.x, nbk[5] = na1.y, nbk[6] = na1.z, nbk[7] = na1.w;
+      const int4 na0 = ld_i4(g.nbr + 8ll * i), na1 = ld_i4(g.nbr + 8ll * i + 4);
+      const int nbr[8] = {na0.x, na0.y, na0.z, na0.w, na1.x, na1.y, na1.z, na1.w};
+      sweep_point8<S>(src, i, nbr, g, i, h, dq_out, gas, ctl, sweep);
     } else {
+      double2 pi, qi, qxi, qyi;
+      src.get(i, pi, qi, qxi, qyi);
+      double sxx = 0.0, sxy = 0.0, syy = 0.0, bx0 = 0.0, bx1 = 0.0, by0 = 0.0, by1 = 0.0;
+      int e0, k;
       stencil_of(g, i, e0, k);
-    }
-#pragma unroll
-    for (int j = 0; j < (K > 0 ? K : k); ++j) {
-      const int nb = K > 0 ? nbk[j] : g.nbr[e0 + j];
-      const double2 pn = ld2(xyd + 2 * nb);
-      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-      const double2 qn = ld2(qd + 4 * nb);
-      double2 qxn, qyn;
-      ld4d(dd + 8 * nb, qxn, qyn);
-      sxx = A::add(sxx, A::mul(dx, dx));
-      sxy = A::add(sxy, A::mul(dx, dy));
-      syy = A::add(syy, A::mul(dy, dy));
-      double df0, df1;
-      if constexpr (S) {
-        df0 = X::sub(corrected<true>(qn.x, qxn.x, qyn.x, dx, dy), corrected<true>(qi.x, qxi.x, qyi.x, dx, dy));
-        df1 = X::sub(corrected<true>(qn.y, qxn.y, qyn.y, dx, dy), corrected<true>(qi.y, qxi.y, qyi.y, dx, dy));
-      } else {
-        df0 = fma(-0.5, fma(dx, qxn.x - qxi.x, dy * (qyn.x - qyi.x)), qn.x - qi.x);
-        df1 = fma(-0.5, fma(dx, qxn.y - qxi.y, dy * (qyn.y - qyi.y)), qn.y - qi.y);
+      for (int j = 0; j < k; ++j) {
+        double2 pn, qn, qxn, qyn;
+        src.get(g.nbr[e0 + j], pn, qn, qxn, qyn);
+        sweep_term<S>(pi, qi, qxi, qyi, pn, qn, qxn, qyn, sxx, sxy, syy, bx0, bx1, by0, by1);
       }
-      bx0 = A::add(bx0, A::mul(dx, df0));
-      by0 = A::add(by0, A::mul(dy, df0));
-      bx1 = A::add(bx1, A::mul(dx, df1));
-      by1 = A::add(by1, A::mul(dy, df1));
-    }
-    const double det = A::sub(A::mul(sxx, syy), A::mul(sxy, sxy));
-    if (!(det > gas.det_tol)) {
-      if (h == 0) raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0), 1 + sweep);
-    } else {
-      double2 fx, fy;
-      if constexpr (S) {
-        fx.x = A::sub(A::mul(syy, bx0), A::mul(sxy, by0)) / det;
-        fx.y = A::sub(A::mul(syy, bx1), A::mul(sxy, by1)) / det;
-        fy.x = A::sub(A::mul(sxx, by0), A::mul(sxy, bx0)) / det;
-        fy.y = A::sub(A::mul(sxx, by1), A::mul(sxy, bx1)) / det;
-      } else {
-        const double r = 1.0 / det;
-        fx.x = (syy * bx0 - sxy * by0) * r;
-        fx.y = (syy * bx1 - sxy * by1) * r;
-        fy.x = (sxx * by0 - sxy * bx0) * r;
-        fy.y = (sxx * by1 - sxy * bx1) * r;
-      }
-      double* o = reinterpret_cast<double*>(dq_out) + 8 * static_cast<long long>(i) + 4 * h;
-      st4(reinterpret_cast<D4*>(o), D4{fx.x, fx.y, fy.x, fy.y});
+      if (!sweep_solve<S>(sxx, sxy, syy, bx0, bx1, by0, by1, gas.det_tol, dq_out, g.nloc, i, h) && h == 0)
+        raise_err(ctl, err_key(PH_SWEEP, g.part[i], gidx(g, i), 0, 0), 1 + sweep);
     }
   }
   __syncthreads();
@@ -515,7 +565,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
     const double2 pi = g.xy[ic];
     const D4 qi = ld4(a.q + ic);
     D4 qxi, qyi;
-    dq_load(a.dq, ic, qxi, qyi);
+    dq_load(a.dq, g.nloc, ic, qxi, qyi);
     for (int jb = 0; jb < kwarp; jb += W) {
       const int j = jb + lane;
       const bool act = live && j < k;
@@ -524,7 +574,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
       const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
       const D4 qn = ld4(a.q + nb);
       D4 qxn, qyn;
-      dq_load(a.dq, nb, qxn, qyn);
+      dq_load(a.dq, g.nloc, nb, qxn, qyn);
       double ti[4], tn[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -827,7 +877,7 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
     const double2 pi = g.xy[ic];
     const D4 qi = ld4(a.q + ic);
     D4 qxi, qyi;
-    dq_load(a.dq, ic, qxi, qyi);
+    dq_load(a.dq, g.nloc, ic, qxi, qyi);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int jb = 0; jb < kwarp; jb += 8) {
       const int j = jb + lane;
@@ -836,7 +886,7 @@ __global__ void __launch_bounds__(256, MB) k_flux_w(FluxArgs a, const double2* _
       const double2 w = act ? w1[e0 + j] : make_double2(0.0, 0.0);
       const D4 qn = ld4(a.q + nb);
       D4 qxn, qyn;
-      dq_load(a.dq, nb, qxn, qyn);
+      dq_load(a.dq, g.nloc, nb, qxn, qyn);
       flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 ? w2 + (e0 + j) : nullptr,
                      acc);
     }
@@ -1022,18 +1072,20 @@ __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1
   cp_async16(f + 0 * 512, g.xy + x.nb, true);
   cp_async16(f + 1 * 512, w1 + x.e, x.act);  // zero-filled for inactive lanes
   const char* qn = reinterpret_cast<const char*>(a.q + x.nb);
-  const char* dn = reinterpret_cast<const char*>(a.dq + 2 * x.nb);
+  const char* xn = reinterpret_cast<const char*>(a.dq + x.nb);           // qx plane
+  const char* yn = reinterpret_cast<const char*>(a.dq + g.nloc + x.nb);  // qy plane
   cp_async16(f + 2 * 512, qn, true);
   cp_async16(f + 3 * 512, qn + 16, true);
-  cp_async16(f + 4 * 512, dn, true);
-  cp_async16(f + 5 * 512, dn + 16, true);
-  cp_async16(f + 6 * 512, dn + 32, true);
-  cp_async16(f + 7 * 512, dn + 48, true);
-  if (lane < 7) {  // own record of the lane group's point: xy, q (2), qx (2), qy (2)
+  cp_async16(f + 4 * 512, xn, true);
+  cp_async16(f + 5 * 512, yn, true);
+  cp_async16(f + 6 * 512, xn + 16, true);
+  cp_async16(f + 7 * 512, yn + 16, true);
+  if (lane < 7) {  // own record of the lane group's point: xy, q (2), qx01 qy01 qx23 qy23
     char* o = st + kFluxStageChunks * 512 + (sub * 7 + lane) * 16;
+    const int c = lane - 3;
     const char* src = lane == 0 ? reinterpret_cast<const char*>(g.xy + x.ic)
                       : lane < 3 ? reinterpret_cast<const char*>(a.q + x.ic) + (lane - 1) * 16
-                                 : reinterpret_cast<const char*>(a.dq + 2 * x.ic) + (lane - 3) * 16;
+                                 : reinterpret_cast<const char*>(a.dq + ((c & 1) ? g.nloc : 0) + x.ic) + (c >> 1) * 16;
     cp_async16(o, src, true);
   }
 }
@@ -1321,23 +1373,27 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
 
 // ---------------------------------------------------------------------------
 // Halo exchange: ghost slot h of this domain (local index n_own + h) pulls its
-// `recs` 32-byte records from the owning domain's buffer, read directly over
-// peer memory (NVLink/NVSwitch when the domains sit on different GPUs).
+// records from the owning domain's buffer — `planes` planes of 32-byte
+// records (q: 1; dq: the qx and qy planes, dq_load), plane r of point p at
+// base + r * ps + p — read directly over peer memory (NVLink/NVSwitch when the
+// domains sit on different GPUs).
 constexpr int kMaxDomains = 16;
 struct PeerTab {
   const D4* base[kMaxDomains];
+  long long ps[kMaxDomains];  // plane stride (the owner's local point count)
 };
 
 // skip_first: the gather is a no-op in iteration 0 (the q halo then comes from
 // the domain's own first q_variables).
-__global__ void k_halo(D4* dst, int recs, int n_own, int n_halo, const int* hdom, const int* hidx,
-                       PeerTab src, const Ctl* ctl, int sub, int skip_first) {
+__global__ void k_halo(D4* dst, long long dst_ps, int planes, int n_own, int n_halo, const int* hdom,
+                       const int* hidx, PeerTab src, const Ctl* ctl, int sub, int skip_first) {
   if (skip_first && iter_of(ctl) == 0) return;
   if (skip_stage(ctl, sub)) return;  // keep the failing stage's buffers intact
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_halo * recs; t += gridDim.x * blockDim.x) {
-    const int h = t / recs, r = t - h * recs;
-    const D4* s = src.base[hdom[h]] + static_cast<size_t>(hidx[h]) * recs + r;
-    st4(dst + static_cast<size_t>(n_own + h) * recs + r, ld4_rw(s));
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_halo * planes; t += gridDim.x * blockDim.x) {
+    const int r = t / n_halo, h = t - r * n_halo;
+    const int d = hdom[h];
+    const D4* s = src.base[d] + r * src.ps[d] + hidx[h];
+    st4(dst + r * dst_ps + n_own + h, ld4_rw(s));
   }
 }
 

@@ -82,6 +82,7 @@ double session_iterate(Session* s, int n);  // returns device ms; throws Fault
 std::vector<double> session_residues(const Session* s);
 std::vector<KernelTime> session_kernels(const Session* s);
 int session_launches_per_iter(const Session* s);
+void session_tiles(const Session* s, int* staged, int* total);  // tiled-sweep plan over all domains
 std::uint64_t session_stream(const Session* s);
 void session_download(Session* s);
 void session_event_ms(const Session* s, double* sweep_ms, double* flux_ms);

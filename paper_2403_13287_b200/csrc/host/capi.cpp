@@ -557,6 +557,12 @@ int lskum_b200_session_info(const lskum_b200_session* s, int* launches_per_iter,
   return LSKUM_OK;
 }
 
+int lskum_b200_session_tiles(const lskum_b200_session* s, int* staged, int* total) {
+  NONNULL(s, staged, total);
+  lskb::session_tiles(s->session, staged, total);
+  return LSKUM_OK;
+}
+
 int lskum_b200_session_download(lskum_b200_session* s) {
   NONNULL(s);
   return guard([&] { lskb::session_download(s->session); });
