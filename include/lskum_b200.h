@@ -188,8 +188,9 @@ int lskum_b200_rank_flush_l2(lskum_b200_rank* r);
 void lskum_b200_rank_destroy(lskum_b200_rank* r);
 
 /* ---- verification hook ----
- * Evaluates CUDA libdevice erf (fn 0) / exp (fn 1) into ref[] and the engine's
- * constant-table replicas used by the flux kernel into ours[] (must be bitwise equal). */
+ * Evaluates CUDA libdevice erf (fn 0, 2) / exp (fn 1) into ref[] and into ours[]
+ * the engine's constant-table replicas used by the flux kernel (fn 0, 1: must be
+ * bitwise equal) or fp_mode fast's polynomial erf (fn 2: a few ulps). */
 int lskum_b200_math_selftest(int fn, const double* in, int64_t n, double* ref, double* ours);
 
 #ifdef __cplusplus

@@ -593,7 +593,7 @@ int lskum_b200_fp64_peak(int device, double* tflops) {
 
 int lskum_b200_math_selftest(int fn, const double* in, int64_t n, double* ref, double* ours) {
   if (n > 0 && (!in || !ref || !ours)) return fail(LSKUM_ERR_ARGUMENT, "null argument");
-  if (fn != 0 && fn != 1) return fail(LSKUM_ERR_ARGUMENT, "fn must be 0 (erf) or 1 (exp)");
+  if (fn < 0 || fn > 2) return fail(LSKUM_ERR_ARGUMENT, "fn must be 0 (erf), 1 (exp) or 2 (fast-mode erf)");
   return guard([&] { lskb::engine_math_selftest(fn, in, n, ref, ours); });
 }
 
