@@ -474,7 +474,11 @@ def run_b200_arm(a):
         res.close()
         e2e_cloud.close()
         nnz = cloud.nnz
-        h2d = n * (16 + 16 + 1 + 2) + 4 * (n + 1) + 4 * nnz  # xy, normals, kind, part, offsets, ids
+        # what lskum_run moves H2D for this cloud (engine Domain: straight from the
+        # cloud's pinned arrays): x and y, kinds, stencil ids; uniform stencils'
+        # offsets are generated on the device, normals only sent for wall points
+        # (none here), partition ids only when non-zero (one partition)
+        h2d = n * (8 + 8 + 1) + 4 * nnz
         d2h = n * 21 * 8 + 8 * a.steps                       # 21-slot store + residue history
         out["e2e"] = {"value": n * a.steps / e2e_wall, "unit": UNIT,
                       "h2d_bytes_per_step": int(h2d / a.steps), "d2h_bytes_per_step": int(d2h / a.steps),

@@ -723,9 +723,10 @@ __global__ void k_set_diag(Ctl* ctl, int diag_iter) { ctl->diag_iter = diag_iter
 
 // Writes the 21-slot field store in the host FieldBlock's layout (AoS: point
 // major; SoA: slot major), so the copy-back is one contiguous D2H transfer.
-__global__ void k_pack_fields(int n, int soa, const D4* prim, const D4* q, const D4* dq, long long dq_ps,
-                              const D4* res, const double* dt, const int* gid, double* out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// Points [lo, hi) of n.
+__global__ void k_pack_fields(int n, int lo, int hi, int soa, const D4* prim, const D4* q, const D4* dq,
+                              long long dq_ps, const D4* res, const double* dt, const int* gid, double* out) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
     const int p = gid ? gid[i] : i;  // position in the store
     D4 qx, qy;
     dq_load(dq, dq_ps, i, qx, qy);
@@ -925,6 +926,30 @@ Gas make_gas(double gamma, double cfl, double det_tol) {
   return g;
 }
 
+// Geometry upload from a cloud whose arrays live in pinned host memory
+// (HostAlloc): the coordinates arrive as two planes and are interleaved here;
+// uniform stencils get their offsets generated, others narrowed to int32.
+__global__ void k_interleave(const double* a, const double* b, double2* out, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = make_double2(a[i], b[i]);
+}
+__global__ void k_off_fill(int* off, long long n, int k, const std::int64_t* src) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    off[i] = src ? static_cast<int>(src[i]) : static_cast<int>(i * k);
+}
+
+bool pinned_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 class Domain {
  public:
   // ipc: buffers that peers read (q, dq, the shared word, the residue array)
@@ -951,18 +976,9 @@ class Domain {
     const std::size_t b_xy = nl * sizeof(double2), b_off = (n + 1) * sizeof(int), b_nbr = nnz * sizeof(int);
     const std::size_t b_gid = gv.gid ? nl * sizeof(int) : 0;
     trace("domain: pool");
-    char* hs = static_cast<char*>(t_staging.get(2 * b_xy + 3 * nl + b_off + b_nbr + b_gid + 64));
-    trace("domain: staging buffer");
-    double2* hxy = reinterpret_cast<double2*>(hs);
-    double2* hnrm = hxy + nl;
-    std::uint16_t* hpart = reinterpret_cast<std::uint16_t*>(hnrm + nl);
-    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hpart + nl);
-    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 3 * nl + 15) & ~std::size_t{15}));
-    int* hnbr = hoff + n + 1;
-    int* hgid = hnbr + nnz;
-    // One pass over the cloud on the host threads: stencil-size scan (kmax,
-    // uniform size kfix) and staging.  Staging uses streaming stores / flushed
-    // lines, so the DMA below runs at PCIe rate (hostcopy.cpp).
+    // Pass 1 on the host threads (reads only): stencil sizes (kmax, uniform
+    // size kfix), wall points (normals are only read for them) and non-zero
+    // partition ids (only read on the failure path).
     const int tasks = std::max(1, std::min(host_threads(), static_cast<int>(nl >> 14)));
     const std::int64_t k0 = n ? gv.off[1] - gv.off[0] : 0;
     std::vector<std::int64_t> t_kmax(static_cast<std::size_t>(tasks), 1);
@@ -970,20 +986,13 @@ class Domain {
         t_parts(static_cast<std::size_t>(tasks), 0);
     parallel_tasks(tasks, [&](int t) {
       auto part_of = [&](std::size_t len, int k) { return len * static_cast<std::size_t>(k) / tasks; };
-      const std::size_t lo = part_of(nl, t), hi = part_of(nl, t + 1), c = hi - lo;
-      stream_pairs(reinterpret_cast<double*>(hxy + lo), gv.x + lo, gv.y + lo, c);
-      stream_pairs(reinterpret_cast<double*>(hnrm + lo), gv.nx + lo, gv.ny + lo, c);
+      const std::size_t lo = part_of(nl, t), hi = part_of(nl, t + 1);
       char walls = 0, parts = 0;
-      for (std::size_t i = lo; i < hi; ++i) {
-        hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
-        hpart[i] = gv.part ? gv.part[i] : 0;
-        walls |= hkind[i] == KIND_WALL;
-        parts |= hpart[i] != 0;
-      }
+      for (std::size_t i = lo; i < hi; ++i) walls |= static_cast<std::uint8_t>(gv.kind[i]) == KIND_WALL;
+      if (gv.part)
+        for (std::size_t i = lo; i < hi; ++i) parts |= gv.part[i] != 0;
       t_walls[t] = walls;
       t_parts[t] = parts;
-      flush_lines(hkind + lo, c);
-      flush_lines(hpart + lo, c * sizeof(std::uint16_t));
       const std::size_t olo = part_of(n, t), ohi = part_of(n, t + 1);
       std::int64_t km = 1;
       bool uni = true;
@@ -991,14 +1000,9 @@ class Domain {
         const std::int64_t e0 = gv.off[i], k = gv.off[i + 1] - e0;
         km = std::max(km, k);
         uni = uni && k == k0 && e0 == static_cast<std::int64_t>(i) * k0;
-        hoff[i] = static_cast<int>(e0);
       }
-      if (t == tasks - 1) hoff[n] = static_cast<int>(gv.off[n]);
-      flush_lines(hoff + olo, (ohi - olo + (t == tasks - 1)) * sizeof(int));
       t_kmax[t] = km;
       t_uniform[t] = uni;
-      const std::size_t blo = part_of(b_nbr, t), bhi = part_of(b_nbr, t + 1);
-      stream_copy(reinterpret_cast<char*>(hnbr) + blo, reinterpret_cast<const char*>(gv.nbr) + blo, bhi - blo);
     });
     std::int64_t km = 1;
     bool uniform = true;
@@ -1013,12 +1017,9 @@ class Domain {
     W_ = flux_width(kmax_);
     smem_ = flux_smem_bytes(W_, kmax_);
     stride_ = flux_stride(kmax_);
-    if (gv.gid) {
-      std::memcpy(hgid, gv.gid, b_gid);
-      flush_lines(hgid, b_gid);
-      gid_host_.assign(gv.gid, gv.gid + nl);
-    }
-    trace("domain: staged");
+    const bool any_wall = std::any_of(t_walls.begin(), t_walls.end(), [](char c) { return c != 0; });
+    const bool any_part = std::any_of(t_parts.begin(), t_parts.end(), [](char c) { return c != 0; });
+    trace("domain: scanned");
     xy_.alloc(nl, st_);
     nrm_.alloc(nl, st_);
     kind_.alloc(nl, st_);
@@ -1026,27 +1027,103 @@ class Domain {
     off_.alloc(n + 1, st_);
     nbr_.alloc(std::max<std::size_t>(1, nnz), st_);
     mind_.alloc(n, st_);
-    trace_sync(st_, "domain: geometry buffers allocated");
-    ck(cudaMemcpyAsync(xy_.get(), hxy, b_xy, cudaMemcpyHostToDevice, st_), "H2D xy");
-    trace_sync(st_, "domain: xy copied");
-    // normals are only read for wall points, partition ids only on the failure
-    // path: clouds without walls / with one partition skip those transfers
-    const bool any_wall = std::any_of(t_walls.begin(), t_walls.end(), [](char c) { return c != 0; });
-    const bool any_part = std::any_of(t_parts.begin(), t_parts.end(), [](char c) { return c != 0; });
-    if (any_wall) ck(cudaMemcpyAsync(nrm_.get(), hnrm, b_xy, cudaMemcpyHostToDevice, st_), "H2D nrm");
-    else ck(cudaMemsetAsync(nrm_.get(), 0, b_xy, st_), "zero nrm");
-    ck(cudaMemcpyAsync(kind_.get(), hkind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
-    if (any_part) {
-      ck(cudaMemcpyAsync(part_.get(), hpart, nl * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_), "H2D part");
-      part_host_.assign(hpart, hpart + nl);
-    } else {
+    if (!any_wall) ck(cudaMemsetAsync(nrm_.get(), 0, b_xy, st_), "zero nrm");
+    if (!any_part) {
       ck(cudaMemsetAsync(part_.get(), 0, nl * sizeof(std::uint16_t), st_), "zero part");
       part_host_.clear();  // empty = all partition ids 0
     }
-    ck(cudaMemcpyAsync(off_.get(), hoff, b_off, cudaMemcpyHostToDevice, st_), "H2D off");
-    trace_sync(st_, "domain: nrm kind part off copied");
-    if (nnz) ck(cudaMemcpyAsync(nbr_.get(), hnbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
-    trace_sync(st_, "domain: nbr copied");
+    // Pass 2a: a single-domain cloud whose arrays are pinned (HostAlloc) is
+    // copied straight from them — no staging.
+    const bool direct = n == nl && !gv.gid && pinned_host(gv.x) && pinned_host(gv.y) && pinned_host(gv.kind) &&
+                        (kfix_ > 0 || pinned_host(gv.off)) && (nnz == 0 || pinned_host(gv.nbr)) &&
+                        (!any_wall || (pinned_host(gv.nx) && pinned_host(gv.ny))) && !any_part;
+    if (direct) {
+      const int blocks = static_cast<int>(std::min<std::size_t>(4096, (nl + 255) / 256));
+      DBuf<double> tx(std::max<std::size_t>(1, nl), st_), ty(std::max<std::size_t>(1, nl), st_);
+      auto planes = [&](const double* a, const double* b, double2* out, const char* what) {
+        ck(cudaMemcpyAsync(tx.get(), a, nl * sizeof(double), cudaMemcpyHostToDevice, st_), what);
+        ck(cudaMemcpyAsync(ty.get(), b, nl * sizeof(double), cudaMemcpyHostToDevice, st_), what);
+        k_interleave<<<blocks, 256, 0, st_>>>(tx.get(), ty.get(), out, static_cast<long long>(nl));
+        ck(cudaGetLastError(), "k_interleave");
+      };
+      planes(gv.x, gv.y, xy_.get(), "H2D x/y");
+      if (nnz) ck(cudaMemcpyAsync(nbr_.get(), gv.nbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
+      ck(cudaMemcpyAsync(kind_.get(), gv.kind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
+      DBuf<std::int64_t> toff(kfix_ > 0 ? 1 : n + 1, st_);
+      if (kfix_ == 0)
+        ck(cudaMemcpyAsync(toff.get(), gv.off, (n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, st_), "H2D off");
+      k_off_fill<<<blocks, 256, 0, st_>>>(off_.get(), static_cast<long long>(n), kfix_, kfix_ > 0 ? nullptr : toff.get());
+      ck(cudaGetLastError(), "k_off_fill");
+      if (any_wall) {
+        ck(cudaStreamSynchronize(st_), "geometry planes");  // tx/ty are reused
+        planes(gv.nx, gv.ny, nrm_.get(), "H2D nx/ny");
+      }
+      ck(cudaStreamSynchronize(st_), "geometry upload");  // temporaries go back to the pool
+      trace("domain: direct copies done");
+    }
+    // Pass 2: stage the geometry into pinned memory in point chunks (streaming
+    // stores / flushed lines, so the DMA runs at PCIe rate, hostcopy.cpp) and
+    // queue each chunk's copies as soon as it is staged — staging chunk c + 1
+    // overlaps the DMA of chunk c.
+    char* hs = direct ? nullptr : static_cast<char*>(t_staging.get(2 * b_xy + 3 * nl + b_off + b_nbr + b_gid + 64));
+    double2* hxy = reinterpret_cast<double2*>(hs);
+    double2* hnrm = hxy + nl;
+    std::uint16_t* hpart = reinterpret_cast<std::uint16_t*>(hnrm + nl);
+    std::uint8_t* hkind = reinterpret_cast<std::uint8_t*>(hpart + nl);
+    int* hoff = reinterpret_cast<int*>(hs + ((2 * b_xy + 3 * nl + 15) & ~std::size_t{15}));
+    int* hnbr = hoff + n + 1;
+    int* hgid = hnbr + nnz;
+    const int chunks = direct ? 0 : static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(8, nl >> 20)));
+    for (int c = 0; c < chunks; ++c) {
+      const std::size_t lo = nl * c / chunks, hi = nl * (c + 1) / chunks;
+      const std::size_t olo = std::min(lo, n), ohi = std::min(hi, n);
+      const std::size_t elo = olo < n ? static_cast<std::size_t>(gv.off[olo]) : nnz;
+      const std::size_t ehi = static_cast<std::size_t>(gv.off[ohi]);
+      parallel_slices(static_cast<std::int64_t>(hi - lo), [&](std::int64_t a, std::int64_t b) {
+        const std::size_t plo = lo + a, phi = lo + b, cnt = phi - plo;
+        stream_pairs(reinterpret_cast<double*>(hxy + plo), gv.x + plo, gv.y + plo, cnt);
+        if (any_wall) stream_pairs(reinterpret_cast<double*>(hnrm + plo), gv.nx + plo, gv.ny + plo, cnt);
+        for (std::size_t i = plo; i < phi; ++i) hkind[i] = static_cast<std::uint8_t>(gv.kind[i]);
+        flush_lines(hkind + plo, cnt);
+        if (any_part) {
+          for (std::size_t i = plo; i < phi; ++i) hpart[i] = gv.part[i];
+          flush_lines(hpart + plo, cnt * sizeof(std::uint16_t));
+        }
+        const std::size_t qlo = std::min(plo, n), qhi = std::min(phi, n);
+        for (std::size_t i = qlo; i < qhi; ++i) hoff[i] = static_cast<int>(gv.off[i]);
+        if (qhi > qlo) flush_lines(hoff + qlo, (qhi - qlo) * sizeof(int));
+        if (qhi > qlo) {
+          const std::size_t blo = static_cast<std::size_t>(gv.off[qlo]) * sizeof(int),
+                            bhi = static_cast<std::size_t>(gv.off[qhi]) * sizeof(int);
+          stream_copy(reinterpret_cast<char*>(hnbr) + blo, reinterpret_cast<const char*>(gv.nbr) + blo, bhi - blo);
+        }
+      }, 1 << 14);
+      if (c == chunks - 1) {
+        hoff[n] = static_cast<int>(gv.off[n]);
+        flush_lines(hoff + n, sizeof(int));
+      }
+      const std::size_t cnt = hi - lo;
+      ck(cudaMemcpyAsync(xy_.get() + lo, hxy + lo, cnt * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D xy");
+      if (any_wall)
+        ck(cudaMemcpyAsync(nrm_.get() + lo, hnrm + lo, cnt * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D nrm");
+      ck(cudaMemcpyAsync(kind_.get() + lo, hkind + lo, cnt, cudaMemcpyHostToDevice, st_), "H2D kind");
+      if (any_part)
+        ck(cudaMemcpyAsync(part_.get() + lo, hpart + lo, cnt * sizeof(std::uint16_t), cudaMemcpyHostToDevice, st_),
+           "H2D part");
+      const std::size_t offn = ohi - olo + (c == chunks - 1 ? 1 : 0);
+      if (offn)
+        ck(cudaMemcpyAsync(off_.get() + olo, hoff + olo, offn * sizeof(int), cudaMemcpyHostToDevice, st_), "H2D off");
+      if (ehi > elo)
+        ck(cudaMemcpyAsync(nbr_.get() + elo, hnbr + elo, (ehi - elo) * sizeof(int), cudaMemcpyHostToDevice, st_),
+           "H2D nbr");
+    }
+    if (any_part) part_host_.assign(hpart, hpart + nl);
+    trace("domain: staged, copies queued");
+    if (gv.gid) {
+      std::memcpy(hgid, gv.gid, b_gid);
+      flush_lines(hgid, b_gid);
+      gid_host_.assign(gv.gid, gv.gid + nl);
+    }
     if (gv.gid) {
       gid_.alloc(nl, st_);
       ck(cudaMemcpyAsync(gid_.get(), hgid, b_gid, cudaMemcpyHostToDevice, st_), "H2D gid");
@@ -1264,19 +1341,54 @@ class Domain {
       // pack on the device in the host layout (scattered to cloud order when
       // the domain is a permutation of the whole cloud), one D2H into the store
       DBuf<double> packed(21 * n, st_);
-      k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
-          n_, f.layout() == Layout::soa ? 1 : 0, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(),
-          dt_.get(),
-          static_cast<const int*>(gid_.get()), packed.get());
-      ck(cudaGetLastError(), "k_pack_fields");
-      trace_sync(st_, "download: packed");
-      if (f.pinned()) {  // the store is pinned: one DMA straight into it
-        ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
-           "D2H fields");
+      const bool soa = f.layout() == Layout::soa;
+      auto pack = [&](int lo, int hi) {
+        k_pack_fields<<<std::max(1, std::min<int>((hi - lo + 255) / 256, 4096)), 256, 0, st_>>>(
+            n_, lo, hi, soa ? 1 : 0, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(), dt_.get(),
+            static_cast<const int*>(gid_.get()), packed.get());
+        ck(cudaGetLastError(), "k_pack_fields");
+      };
+      if (f.pinned()) {  // the store is pinned: DMA straight into it
+        if (gid_host_.empty()) {
+          // cloud order: pack and copy in point chunks, so the packing of
+          // chunk c + 1 overlaps the transfer of chunk c (SoA: 21 rows of the
+          // chunk's points, one 2-D copy)
+          // (the copies run on a second stream, each after its chunk's packing)
+          const int chunks = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(8, n >> 20)));
+          cudaStream_t cs = nullptr;
+          ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+          std::vector<cudaEvent_t> packed_ev(static_cast<std::size_t>(chunks));
+          for (auto& e : packed_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+          cudaError_t err = cudaSuccess;
+          for (int c = 0; c < chunks && err == cudaSuccess; ++c) {
+            const int lo = static_cast<int>(n * c / chunks), hi = static_cast<int>(n * (c + 1) / chunks);
+            pack(lo, hi);
+            err = cudaEventRecord(packed_ev[c], st_);
+            if (err == cudaSuccess) err = cudaStreamWaitEvent(cs, packed_ev[c], 0);
+            if (err != cudaSuccess) break;
+            if (soa)
+              err = cudaMemcpy2DAsync(f.raw() + lo, n * sizeof(double), packed.get() + lo, n * sizeof(double),
+                                      (hi - lo) * sizeof(double), 21, cudaMemcpyDeviceToHost, cs);
+            else
+              err = cudaMemcpyAsync(f.raw() + 21ll * lo, packed.get() + 21ll * lo, 21ll * (hi - lo) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, cs);
+          }
+          const cudaError_t serr = cudaStreamSynchronize(cs);
+          for (auto& e : packed_ev) cudaEventDestroy(e);
+          cudaStreamDestroy(cs);
+          ck(err, "D2H fields");
+          ck(serr, "download (copy stream)");
+        } else {
+          pack(0, n_);
+          ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
+             "D2H fields");
+        }
         ck(cudaStreamSynchronize(st_), "download");
         trace("download: stored (pinned store)");
         return;
       }
+      pack(0, n_);
+      trace_sync(st_, "download: packed");
       // through pinned staging (full-rate D2H) in chunks; host threads copy
       // each chunk into the store as soon as its transfer completes
       const std::size_t count = 21 * n, bytes = count * sizeof(double);

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(TP) k_tile_plan(Geo g, int smax, TilePlan* pla
   } tmp;
   __shared__ int s_last[TP];
   __shared__ int s_start[kTileIv], s_end[kTileIv], s_soff[kTileIv];
-  __shared__ int s_nint, s_ok;
+  __shared__ int s_nint, s_ok, s_lo, s_hi;
   const int t = blockIdx.x;
   const int i0 = t * TP;
   const int i = i0 + static_cast<int>(threadIdx.x);
@@ -68,7 +68,26 @@ __global__ void __launch_bounds__(TP) k_tile_plan(Geo g, int smax, TilePlan* pla
   keys[0] = ic;
 #pragma unroll
   for (int j = 0; j < 8; ++j) keys[1 + j] = g.nbr[8ll * ic + j];
-  Sort(tmp.sort).Sort(keys);  // blocked: thread t holds ranks 9t .. 9t+8
+  // sort the offsets from the tile's smallest id on only as many bits as the
+  // id window needs (2 radix passes instead of 4 for a ring-ordered cloud)
+  if (threadIdx.x == 0) {
+    s_lo = 0x7FFFFFFF;
+    s_hi = 0;
+  }
+  __syncthreads();
+  int lo = keys[0], hi = keys[0];
+#pragma unroll
+  for (int j = 1; j < 9; ++j) lo = min(lo, keys[j]), hi = max(hi, keys[j]);
+  atomicMin(&s_lo, lo);
+  atomicMax(&s_hi, hi);
+  __syncthreads();
+  const int base_id = s_lo;
+  const int bits = 32 - __clz(static_cast<unsigned>(s_hi - base_id) | 1u);
+#pragma unroll
+  for (int j = 0; j < 9; ++j) keys[j] -= base_id;
+  Sort(tmp.sort).Sort(keys, 0, bits);  // blocked: thread t holds ranks 9t .. 9t+8
+#pragma unroll
+  for (int j = 0; j < 9; ++j) keys[j] += base_id;
   s_last[threadIdx.x] = keys[8];
   __syncthreads();
   // interval starts: the first key, and every key more than kTileGap + 1 above its predecessor

@@ -32,7 +32,7 @@ void split(const PointSet& ps, std::vector<std::int32_t>& ids, int parts, std::v
     ylo = std::min(ylo, ps.y[i]);
     yhi = std::max(yhi, ps.y[i]);
   }
-  const std::vector<double>& key = (xhi - xlo) >= (yhi - ylo) ? ps.x : ps.y;
+  const HVec<double>& key = (xhi - xlo) >= (yhi - ylo) ? ps.x : ps.y;
   std::sort(ids.begin(), ids.end(), [&key](std::int32_t a, std::int32_t b) {
     return key[a] < key[b] || (key[a] == key[b] && a < b);
   });

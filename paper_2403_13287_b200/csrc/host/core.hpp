@@ -93,6 +93,52 @@ struct StoreHooks {
 };
 StoreHooks& store_hooks();
 
+// Allocator of a cloud's per-point arrays (coordinates, normals, kinds,
+// stencil offsets and ids): blocks of 32 MB and more come from pinned host
+// memory through store_hooks() (the engine's pool), so the geometry upload
+// DMAs straight from the cloud's own arrays instead of through staging;
+// smaller blocks, and every block when no device is present, from the heap.
+// The pinned/heap decision is a function of the block size alone, so
+// deallocate() takes the same path as allocate() did.
+template <class T>
+struct HostAlloc {
+  using value_type = T;
+  HostAlloc() = default;
+  template <class U>
+  HostAlloc(const HostAlloc<U>&) noexcept {}
+  static constexpr std::size_t kPinnedMin = std::size_t{32} << 20;
+  T* allocate(std::size_t n) {
+    const std::size_t bytes = n * sizeof(T);
+    if (bytes >= kPinnedMin && store_hooks().alloc) {
+      // a pinned block carries a 64-byte header: 1 = pinned, so a heap
+      // fallback of the same size is released to the heap
+      char* p = static_cast<char*>(store_hooks().alloc(bytes + 64));
+      if (p) {
+        *reinterpret_cast<std::uint64_t*>(p) = 1;
+        return reinterpret_cast<T*>(p + 64);
+      }
+      char* h = static_cast<char*>(::operator new(bytes + 64));
+      *reinterpret_cast<std::uint64_t*>(h) = 0;
+      return reinterpret_cast<T*>(h + 64);
+    }
+    return static_cast<T*>(::operator new(bytes));
+  }
+  void deallocate(T* p, std::size_t n) noexcept {
+    const std::size_t bytes = n * sizeof(T);
+    if (bytes >= kPinnedMin && store_hooks().alloc) {
+      char* b = reinterpret_cast<char*>(p) - 64;
+      if (*reinterpret_cast<std::uint64_t*>(b) == 1) store_hooks().release(b, bytes + 64);
+      else ::operator delete(b);
+      return;
+    }
+    ::operator delete(p);
+  }
+  template <class U>
+  bool operator==(const HostAlloc<U>&) const noexcept { return true; }
+};
+template <class T>
+using HVec = std::vector<T, HostAlloc<T>>;
+
 class StoreBuffer {
  public:
   StoreBuffer() = default;
@@ -169,10 +215,10 @@ struct Screening;
 struct Locality;
 
 struct PointSet {
-  std::vector<double> x, y, nx, ny;
-  std::vector<Kind> kind;
-  std::vector<std::int64_t> off{0};  // n+1
-  std::vector<std::int32_t> nbr;     // ascending ids per point
+  HVec<double> x, y, nx, ny;
+  HVec<Kind> kind;
+  HVec<std::int64_t> off{0};  // n+1
+  HVec<std::int32_t> nbr;     // ascending ids per point
   FieldBlock fields;
 
   std::int32_t n() const { return static_cast<std::int32_t>(x.size()); }

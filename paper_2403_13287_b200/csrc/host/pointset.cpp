@@ -197,8 +197,8 @@ PointSet assemble(std::vector<PointRow> rows, std::vector<std::int64_t> off,
       ps.kind[i] = rows[i].kind;
     }
   }, 1 << 16);
-  ps.off = std::move(off);
-  ps.nbr = std::move(nbr);
+  ps.off.assign(off.begin(), off.end());  // into the cloud's (pinned when large) arrays
+  ps.nbr.assign(nbr.begin(), nbr.end());
   ps.fields = FieldBlock(Layout::aos, n);
   return ps;
 }
