@@ -350,7 +350,8 @@ def rooflines(L, counts, n, n_flux, k, order, inner, step_ms, sweep_ms, flux_ms,
             "flops_source": f"ncu dynamic 2*DFMA+DADD+DMUL = {flops_pt:.0f} per point "
                             "(profiles/flux_ncu_counts.json)" if flops_pt else None,
             "launch_ms": flux_ms}
-    hbmr = {"bound": "hbm", "kernel": "k_sweep2 (derivative sweep)", "achieved": sweep_gbs, "peak": hbm,
+    hbmr = {"bound": "hbm", "kernel": "k_sweep_tile (derivative sweep: stencil unions of 128-point tiles staged in "
+                                      "shared memory by TMA bulk copies)", "achieved": sweep_gbs, "peak": hbm,
             "unit": "GB/s", "frac": sweep_gbs / hbm if sweep_gbs else None,
             "algorithmic_bytes_per_point": sweep_bytes(k), "launch_ms": sweep_ms, "peak_source": hbm_kind,
             "iteration_achieved_gbs_per_gpu": iter_gbs, "iteration_frac": iter_gbs / hbm,

@@ -1034,7 +1034,9 @@ class Domain {
     }
     // Pass 2a: a single-domain cloud whose arrays are pinned (HostAlloc) is
     // copied straight from them — no staging.
-    const bool direct = n == nl && !gv.gid && pinned_host(gv.x) && pinned_host(gv.y) && pinned_host(gv.kind) &&
+    // (kinds, 1 B per point, may sit below HostAlloc's pinned threshold: they
+    // go through a small staging copy)
+    const bool direct = n == nl && !gv.gid && pinned_host(gv.x) && pinned_host(gv.y) &&
                         (kfix_ > 0 || pinned_host(gv.off)) && (nnz == 0 || pinned_host(gv.nbr)) &&
                         (!any_wall || (pinned_host(gv.nx) && pinned_host(gv.ny))) && !any_part;
     if (direct) {
@@ -1048,7 +1050,13 @@ class Domain {
       };
       planes(gv.x, gv.y, xy_.get(), "H2D x/y");
       if (nnz) ck(cudaMemcpyAsync(nbr_.get(), gv.nbr, b_nbr, cudaMemcpyHostToDevice, st_), "H2D nbr");
-      ck(cudaMemcpyAsync(kind_.get(), gv.kind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
+      if (pinned_host(gv.kind)) {
+        ck(cudaMemcpyAsync(kind_.get(), gv.kind, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
+      } else {
+        std::uint8_t* hk = static_cast<std::uint8_t*>(t_staging.get(nl));
+        stream_copy(hk, gv.kind, nl);
+        ck(cudaMemcpyAsync(kind_.get(), hk, nl, cudaMemcpyHostToDevice, st_), "H2D kind");
+      }
       DBuf<std::int64_t> toff(kfix_ > 0 ? 1 : n + 1, st_);
       if (kfix_ == 0)
         ck(cudaMemcpyAsync(toff.get(), gv.off, (n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, st_), "H2D off");
@@ -1161,9 +1169,12 @@ class Domain {
     hsh_.alloc(1);
     trace("domain: allocated, copies queued");
     trace_sync(st_, "domain: copies done");
-    k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get());
+    DBuf<unsigned long long> zc(1, st_);
+    ck(cudaMemsetAsync(zc.get(), 0, sizeof(unsigned long long), st_), "memset");
+    k_min_dist<<<(n_ + 255) / 256, 256, 0, st_>>>(geo(), mind_.get(), zc.get());
     ck(cudaGetLastError(), "k_min_dist");
     k_ctl_init<<<1, 1, 0, st_>>>(ctl_.get(), shared_, 1, -1, 0, update_blocks());
+    ck(cudaMemcpyAsync(&zero_pairs_, zc.get(), sizeof zero_pairs_, cudaMemcpyDeviceToHost, st_), "D2H zero pairs");
     ck(cudaStreamSynchronize(st_), "geometry upload");
   }
 
@@ -1237,11 +1248,14 @@ class Domain {
     ScreenOut init{0, 0, 0, 0x7FFFFFFF, 0};
     ck(cudaMemcpyAsync(so.get(), &init, sizeof init, cudaMemcpyHostToDevice, st_), "H2D screen");
     DBuf<unsigned long long> keys(static_cast<std::size_t>(n), st_), sorted(static_cast<std::size_t>(n), st_);
+    trace_sync(st_, "screen: buffers");
     k_screen_keys<<<(n + 255) / 256, 256, 0, st_>>>(n, mind_.get(), keys.get(), so.get());
     std::size_t tmp_bytes = 0;
     ck(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort size");
     DBuf<char> tmp(std::max<std::size_t>(1, tmp_bytes), st_);
+    trace_sync(st_, "screen: keys");
     ck(cub::DeviceRadixSort::SortKeys(tmp.get(), tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort");
+    trace_sync(st_, "screen: sorted");
     ScreenOut head{};
     ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
     ck(cudaStreamSynchronize(st_), "screen keys");
@@ -1568,20 +1582,13 @@ class Domain {
   void ensure_weights() {
     if (weights_) return;
     const int blocks = (n_ + 255) / 256;
-    DBuf<unsigned long long> zc(1, st_);
-    ck(cudaMemsetAsync(zc.get(), 0, sizeof(unsigned long long), st_), "memset");
-    k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, nullptr, nullptr, nullptr, zc.get(),
-                                                          nullptr);
-    unsigned long long zeros = 0;
-    ck(cudaMemcpyAsync(&zeros, zc.get(), sizeof zeros, cudaMemcpyDeviceToHost, st_), "D2H zero pairs");
-    ck(cudaStreamSynchronize(st_), "weights count");
     const std::size_t nnz = static_cast<std::size_t>(std::max<std::int64_t>(1, nnz_));
     w1_.alloc(nnz, st_);
     psign_.alloc(nnz, st_);
-    if (zeros) w2_.alloc(nnz, st_);
+    if (zero_pairs_) w2_.alloc(nnz, st_);  // counted by k_min_dist
     sing_.alloc(static_cast<std::size_t>(std::max(1, n_)), st_);
     k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, w1_.get(), w2_.get(), sing_.get(),
-                                                          zc.get(), psign_.get());
+                                                          psign_.get());
     ck(cudaGetLastError(), "k_flux_weights");
     ck(cudaStreamSynchronize(st_), "weights");
     weights_ = true;
@@ -2135,6 +2142,7 @@ class Domain {
   DBuf<TilePlan> tplan_;        // tile plan of the tiled sweep (tiles.cuh)
   DBuf<std::uint16_t> tslot_;
   int ntiles_ = 0, tiles_staged_ = 0, tile_p_ = 128;
+  unsigned long long zero_pairs_ = 0;  // pairs with dx == 0 or dy == 0 (non-outer points)
   bool tiles_ = false;
   DBuf<PointFlux> pf_;           // first order: split fluxes per point (owned + halo)
   DBuf<std::uint8_t> psign_;     // first order: half-stencil signs / zero offset per pair

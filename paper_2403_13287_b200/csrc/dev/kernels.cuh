@@ -229,18 +229,29 @@ __device__ __forceinline__ unsigned long long ktimer_fold_warp(Ctl* ctl) {
 // ---------------------------------------------------------------------------
 // Geometry: nearest-neighbour distance per point (the min over the stencil in
 // local_timestep_kernel, kernels.cpp:170-175) — constant for a run.
-__global__ void k_min_dist(Geo g, double* mind) {
+// Also counts the pairs of non-outer points with a zero offset (dx == 0 or
+// dy == 0): they belong to both half stencils of that axis, and the fast flux
+// only allocates and reads their second weight table (w2) when there are any.
+__global__ void k_min_dist(Geo g, double* mind, unsigned long long* zero_pairs) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  const double2 pi = g.xy[i];
-  double best = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-  for (int e = g.off[i]; e < g.off[i + 1]; ++e) {
-    const double2 pn = g.xy[g.nbr[e]];
-    const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
-    const double d = sqrt(X::add(X::mul(dx, dx), X::mul(dy, dy)));
-    best = d < best ? d : best;  // std::min(best, d)
+  unsigned z = 0;
+  if (i < g.n) {
+    const double2 pi = g.xy[i];
+    double best = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+    for (int e = g.off[i]; e < g.off[i + 1]; ++e) {
+      const double2 pn = g.xy[g.nbr[e]];
+      const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+      const double d = sqrt(X::add(X::mul(dx, dx), X::mul(dy, dy)));
+      best = d < best ? d : best;  // std::min(best, d)
+      z += (dx == 0.0 || dy == 0.0) ? 1u : 0u;
+    }
+    mind[i] = best;
+    if (g.kind[i] == KIND_OUTER) z = 0;
   }
-  mind[i] = best;
+  if (__any_sync(0xFFFFFFFFu, z != 0)) {
+    const unsigned sum = __reduce_add_sync(0xFFFFFFFFu, z);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(zero_pairs, static_cast<unsigned long long>(sum));
+  }
 }
 
 // q_variables over all points (kernels.cpp:68-80); used for the first
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(W * flux_points_per_block(W), MB) k_flux(FluxA
 // psign[e] (first order): bit 0 = the pair's x half is Gx- (dx > 0), bit 1 =
 // its y half is Gy- (dy > 0), bit 2 = a zero offset (both halves).
 __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, std::uint8_t* sing,
-                               unsigned long long* zero_pairs, std::uint8_t* psign) {
+                               std::uint8_t* psign) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   int e0, k;
@@ -719,15 +730,6 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
     return;
   }
   const double2 pi = g.xy[i];
-  if (!w1) {  // counting pass
-    unsigned long long z = 0;
-    for (int j = 0; j < k; ++j) {
-      const double2 pn = g.xy[g.nbr[e0 + j]];
-      z += (X::sub(pn.x, pi.x) == 0.0 || X::sub(pn.y, pi.y) == 0.0) ? 1 : 0;
-    }
-    if (z) atomicAdd(zero_pairs, z);
-    return;
-  }
   double sxx[4] = {0.0, 0.0, 0.0, 0.0}, sxy[4] = {0.0, 0.0, 0.0, 0.0}, syy[4] = {0.0, 0.0, 0.0, 0.0};
   for (int j = 0; j < k; ++j) {
     const double2 pn = g.xy[g.nbr[e0 + j]];
@@ -810,7 +812,7 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = fma(wy, X::sub(gn[c], gi[c]), acc[c]);
   // a zero offset belongs to both half stencils: add the minus direction
-  // (w2e null: the stencil table has no zero offset — k_flux_weights' count)
+  // (w2e null: the stencil table has no zero offset — k_min_dist's count)
   if (w2e != nullptr && __any_sync(kFull, store && (dx == 0.0 || dy == 0.0))) {
     const double2 v = (store && (dx == 0.0 || dy == 0.0)) ? *w2e : make_double2(0.0, 0.0);
     split_flux_fast<0>(fi, at[0], true, epi, kki, gi);
@@ -1115,6 +1117,11 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
     cp_async_commit();
     StageRaw nxt = stage_load(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
     int buf = 0;
+#ifdef LSKUM_FLUX_DEFER_REDUCE
+    double pacc[4] = {0.0, 0.0, 0.0, 0.0};
+    int prev_i = 0;
+    bool prev_live = false, have_prev = false;
+#endif
     for (; grp < groups; grp += nwarps, buf ^= 1) {
       const bool more = grp + nwarps < groups;
       const StageIdx nx = stage_index(g, nxt, lane);
@@ -1137,17 +1144,38 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
       if (cur.live && lane == 0 && cur.sing != 0xFF)
         raise_err(a.ctl, flux_key(a.ctl, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
+#ifdef LSKUM_FLUX_DEFER_REDUCE
+      // the previous group's reduction and store, independent of this group's
+      // math: the shuffles fill issue slots between its FP64 chains
+      if (have_prev) {
+        const double r = reduce8(pacc, lane);
+        if (prev_live) store_res8(a.res, prev_i, r, lane);
+      }
+#endif
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
                      D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
                      D4{y01.x, y01.y, y23.x, y23.y}, w, w2 ? w2 + cur.e : nullptr, acc);
+#ifdef LSKUM_FLUX_DEFER_REDUCE
+      for (int c = 0; c < 4; ++c) pacc[c] = acc[c];
+      prev_i = cur.i;
+      prev_live = cur.live;
+      have_prev = true;
+#else
       const double r = reduce8(acc, lane);
       if (cur.live) store_res8(a.res, cur.i, r, lane);
+#endif
       __syncwarp();  // the stage is refilled two groups on
       cur = nx;
       nxt = nxt2;
     }
+#ifdef LSKUM_FLUX_DEFER_REDUCE
+    if (have_prev) {
+      const double r = reduce8(pacc, lane);
+      if (prev_live) store_res8(a.res, prev_i, r, lane);
+    }
+#endif
     cp_async_wait<0>();
   }
   __syncthreads();

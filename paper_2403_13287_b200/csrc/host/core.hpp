@@ -92,6 +92,8 @@ struct StoreHooks {
   void (*release)(void* p, std::size_t bytes) = nullptr;
 };
 StoreHooks& store_hooks();
+// Clouds keep their large arrays in pinned memory (LSKUM_PINNED_CLOUD=0: heap).
+bool pinned_clouds();
 
 // Allocator of a cloud's per-point arrays (coordinates, normals, kinds,
 // stencil offsets and ids): blocks of 32 MB and more come from pinned host
@@ -107,9 +109,10 @@ struct HostAlloc {
   template <class U>
   HostAlloc(const HostAlloc<U>&) noexcept {}
   static constexpr std::size_t kPinnedMin = std::size_t{32} << 20;
+  static bool pinned_block(std::size_t bytes) { return bytes >= kPinnedMin && store_hooks().alloc && pinned_clouds(); }
   T* allocate(std::size_t n) {
     const std::size_t bytes = n * sizeof(T);
-    if (bytes >= kPinnedMin && store_hooks().alloc) {
+    if (pinned_block(bytes)) {
       // a pinned block carries a 64-byte header: 1 = pinned, so a heap
       // fallback of the same size is released to the heap
       char* p = static_cast<char*>(store_hooks().alloc(bytes + 64));
@@ -125,7 +128,7 @@ struct HostAlloc {
   }
   void deallocate(T* p, std::size_t n) noexcept {
     const std::size_t bytes = n * sizeof(T);
-    if (bytes >= kPinnedMin && store_hooks().alloc) {
+    if (pinned_block(bytes)) {
       char* b = reinterpret_cast<char*>(p) - 64;
       if (*reinterpret_cast<std::uint64_t*>(b) == 1) store_hooks().release(b, bytes + 64);
       else ::operator delete(b);

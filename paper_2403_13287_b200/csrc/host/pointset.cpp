@@ -49,6 +49,14 @@ StoreHooks& store_hooks() {
   return h;
 }
 
+bool pinned_clouds() {
+  static const bool on = [] {
+    const char* e = std::getenv("LSKUM_PINNED_CLOUD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 void StoreBuffer::allocate(std::size_t count) {
   n_ = count;
   if (!count) return;

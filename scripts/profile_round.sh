@@ -8,7 +8,7 @@ tag=${1:-r02}
 mkdir -p gpurun_out
 timeout 1200 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/${tag}_bench_reference.json 2> gpurun_out/${tag}_bench_reference.err
-bash scripts/ncu_kernels.sh ${tag} k_flux_ws k_sweep2 k_update
+bash scripts/ncu_kernels.sh ${tag} k_flux_ws k_sweep_tile k_update
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-sizes \
     --no-e2e > gpurun_out/${tag}_b_ncu.log 2>&1
