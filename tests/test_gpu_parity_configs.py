@@ -11,6 +11,7 @@ BASELINE.json's configs name:
   configs[1] NACA 0012 520x308  (160,160 points)  M 0.85 AoA 1   orders 1 and 2 (+ strict mode)
   configs[2] NACA 0012 1000x625 (625,000 points)  M 1.2  AoA 0   orders 1 and 2
   configs[3] NACA 0012 4000x2500 (10M points)     M 0.85 AoA 1   order 2
+  configs[4] NACA 0012 8000x5000 (40M points)     M 0.85 AoA 1   order 2 (3 iterations: the bench cloud)
 
 The state is the free stream plus a +5% Gaussian density/pressure bump above
 the section (the reference's tests/support.hpp:45-56 bump, centred at
@@ -219,6 +220,14 @@ def test_configs3_10m_matches_reference():
     its 8x2 block shape, sweep/update/residue at full size)."""
     k, env = naca_parity((4000, 2500), 0.85, 1.0, 2, 5)
     assert k == 5
+
+
+def test_configs4_40m_matches_reference():
+    """configs[4]: the 40M-point cloud of the bench headline, 3 second-order
+    iterations against the reference itself (tiled sweep, k_flux_ws 8x2,
+    direct geometry upload and chunked copy-back at full size)."""
+    k, env = naca_parity((8000, 5000), 0.85, 1.0, 2, 3)
+    assert k == 3
 
 
 # ---- the SURVEY 8(d) rectangle stand-ins at the config sizes (stable at order 1) ----
