@@ -564,24 +564,42 @@ int flux_ws_shape(int n) {
 
 // The staged flux kernel, instantiated for gamma = 1.4 (2/(gamma-1) = 5 at
 // compile time: -2.8% flux time at 10M points) and for any gamma.
-template <int MB, int NW, int HP>
-void flux_ws_launch_hp(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                       cudaStream_t st) {
+// Uniform 8-point stencils over all owned points: the k_flux_ws instantiation
+// with compile-time stencil offsets (LSKUM_FLUX_U8=0 disables it).
+bool flux_u8() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_FLUX_U8");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+template <int MB, int NW, int HP, bool U8>
+void flux_ws_launch_k(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                      cudaStream_t st) {
   constexpr std::size_t smem = static_cast<std::size_t>(2 * NW) * kFluxStageBytes;
+  auto kern = k_flux_ws<MB, NW, HP, U8>;
   static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!resident[dev & 63]) {
-    ck(cudaFuncSetAttribute(k_flux_ws<MB, NW, HP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
        "cudaFuncSetAttribute(k_flux_ws)");
     int per_sm = 0, sms = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_flux_ws<MB, NW, HP>, NW * 32, smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem), "occupancy");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int groups = ((a.g.list ? a.g.nlist : a.g.n) + 3) / 4;
   const int blocks = std::max(1, std::min((groups + NW - 1) / NW, resident[dev & 63]));
-  launch_pdl(k_flux_ws<MB, NW, HP>, blocks, NW * 32, smem, st, a, w1, w2, sing);
+  launch_pdl(kern, blocks, NW * 32, smem, st, a, w1, w2, sing);
+}
+
+template <int MB, int NW, int HP>
+void flux_ws_launch_hp(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                       cudaStream_t st) {
+  if (a.g.kfix == 8 && !a.g.list && flux_u8()) flux_ws_launch_k<MB, NW, HP, true>(a, w1, w2, sing, st);
+  else flux_ws_launch_k<MB, NW, HP, false>(a, w1, w2, sing, st);
 }
 
 template <int MB, int NW>

@@ -1040,15 +1040,24 @@ struct StageRaw {
   int i, kind, nbr, e, k, sing;
 };
 
+// U8: uniform 8-point stencils and every owned point visited (no subset
+// list): the stencil offsets and the visit list are compile-time, so the
+// loop keeps fewer kernel parameters live.
+template <bool U8 = false>
 __device__ __forceinline__ StageRaw stage_load(const Geo& g, const std::uint8_t* sing, int grp, int lane,
                                                int sub) {
   StageRaw r;
-  r.i = visit_point(g, grp * 4 + sub);
+  r.i = U8 ? grp * 4 + sub : visit_point(g, grp * 4 + sub);
   const int ic = r.i < g.n ? r.i : g.n - 1;
   r.kind = g.kind[ic];
   r.sing = lane == 0 ? sing[ic] : 0xFF;  // first singular split direction (k_flux_weights)
   int e0 = 0, k = 0;
-  stencil_of(g, ic, e0, k);
+  if constexpr (U8) {
+    e0 = 8 * ic;
+    k = 8;
+  } else {
+    stencil_of(g, ic, e0, k);
+  }
   r.e = e0 + lane;
   r.k = k;
   r.nbr = (r.i < g.n && lane < k) ? g.nbr[r.e] : ic;
@@ -1092,7 +1101,7 @@ __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1
   }
 }
 
-template <int MB, int NW = kFluxWarps, int HP = -1>
+template <int MB, int NW = kFluxWarps, int HP = -1, bool U8 = false>
 __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
                                                      const double2* __restrict__ w2,
                                                      const std::uint8_t* __restrict__ sing) {
@@ -1108,26 +1117,21 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
   const int warp = threadIdx.x >> 5;
   char* const stage0 = fsm + (2 * warp) * kFluxStageBytes;  // stage b at stage0 + b * kFluxStageBytes
   const Geo& g = a.g;
-  const int groups = (visit_count(g) + 3) >> 2;
+  const int groups = ((U8 ? g.n : visit_count(g)) + 3) >> 2;
   const int nwarps = gridDim.x * NW;
   int grp = blockIdx.x * NW + warp;
   if (!s_skip && grp < groups) {
-    StageIdx cur = stage_index(g, stage_load(g, sing, grp, lane, sub), lane);
+    StageIdx cur = stage_index(g, stage_load<U8>(g, sing, grp, lane, sub), lane);
     stage_issue(a, w1, cur, stage0, lane32, lane, sub);
     cp_async_commit();
-    StageRaw nxt = stage_load(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
+    StageRaw nxt = stage_load<U8>(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
     int buf = 0;
-#ifdef LSKUM_FLUX_DEFER_REDUCE
-    double pacc[4] = {0.0, 0.0, 0.0, 0.0};
-    int prev_i = 0;
-    bool prev_live = false, have_prev = false;
-#endif
     for (; grp < groups; grp += nwarps, buf ^= 1) {
       const bool more = grp + nwarps < groups;
       const StageIdx nx = stage_index(g, nxt, lane);
       if (more) stage_issue(a, w1, nx, stage0 + (buf ^ 1) * kFluxStageBytes, lane32, lane, sub);
       cp_async_commit();
-      const StageRaw nxt2 = stage_load(g, sing, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
+      const StageRaw nxt2 = stage_load<U8>(g, sing, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
       cp_async_wait<1>();
       __syncwarp();
       const char* st = stage0 + buf * kFluxStageBytes;
@@ -1144,38 +1148,17 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
       if (cur.live && lane == 0 && cur.sing != 0xFF)
         raise_err(a.ctl, flux_key(a.ctl, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
-#ifdef LSKUM_FLUX_DEFER_REDUCE
-      // the previous group's reduction and store, independent of this group's
-      // math: the shuffles fill issue slots between its FP64 chains
-      if (have_prev) {
-        const double r = reduce8(pacc, lane);
-        if (prev_live) store_res8(a.res, prev_i, r, lane);
-      }
-#endif
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
                      D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
                      D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
                      D4{y01.x, y01.y, y23.x, y23.y}, w, w2 ? w2 + cur.e : nullptr, acc);
-#ifdef LSKUM_FLUX_DEFER_REDUCE
-      for (int c = 0; c < 4; ++c) pacc[c] = acc[c];
-      prev_i = cur.i;
-      prev_live = cur.live;
-      have_prev = true;
-#else
       const double r = reduce8(acc, lane);
       if (cur.live) store_res8(a.res, cur.i, r, lane);
-#endif
       __syncwarp();  // the stage is refilled two groups on
       cur = nx;
       nxt = nxt2;
     }
-#ifdef LSKUM_FLUX_DEFER_REDUCE
-    if (have_prev) {
-      const double r = reduce8(pacc, lane);
-      if (prev_live) store_res8(a.res, prev_i, r, lane);
-    }
-#endif
     cp_async_wait<0>();
   }
   __syncthreads();
