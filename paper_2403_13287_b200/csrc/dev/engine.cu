@@ -61,9 +61,14 @@ bool graph_upload() {
 }
 
 // LSKUM_TRACE only: waits for the stream so the trace line times its work.
+// (LSKUM_TRACE_NOSYNC=1: host timestamps only, the pipeline left as it runs)
 void trace_sync(cudaStream_t st, const char* what) {
   if (!tracing()) return;
-  cudaStreamSynchronize(st);
+  static const bool nosync = [] {
+    const char* e = std::getenv("LSKUM_TRACE_NOSYNC");
+    return e && std::atoi(e) == 1;
+  }();
+  if (!nosync) cudaStreamSynchronize(st);
   trace(what);
 }
 
@@ -204,10 +209,12 @@ class Staging {
 };
 thread_local Staging t_staging;
 
-// Pinned host memory for large field stores (StoreBuffer, host/core.hpp): the
-// copy-back DMAs straight into the cloud's store.  Freed blocks are kept for
-// the next store of the same size (a cloud handle per run, as lskum_run users
-// and the bench create them, then costs no page pinning).
+// Pinned host memory for large field stores (StoreBuffer) and large cloud
+// arrays (HostAlloc, host/core.hpp): the copy-back DMAs straight into the
+// cloud's store and the geometry upload straight from its arrays.  Freed
+// blocks are kept for the next store / cloud of the same sizes (a cloud handle
+// per run, as lskum_run users and the bench create them, then costs no page
+// pinning).
 class StorePool {
  public:
   static void* alloc(std::size_t bytes) {
@@ -233,11 +240,18 @@ class StorePool {
     }
     return p;
   }
+  // Freed blocks stay cached (most recent last) up to kKeepBytes, so the next
+  // cloud / store of the same sizes reuses them instead of pinning anew
+  // (cudaHostAlloc runs at ~1-2 GB/s); the oldest go back to the system.
+  static constexpr std::size_t kKeepBytes = std::size_t{24} << 30;
   static void release(void* p, std::size_t bytes) {
     std::lock_guard<std::mutex> g(mu());
     auto& f = free_blocks();
     f.emplace_back(p, bytes);
-    while (f.size() > 2) {  // keep the two most recent blocks
+    std::size_t total = 0;
+    for (const auto& b : f) total += b.second;
+    while (total > kKeepBytes && f.size() > 1) {
+      total -= f.front().second;
       cudaFreeHost(f.front().first);
       f.erase(f.begin());
     }
@@ -420,6 +434,18 @@ void sweep_launch(bool strict, const Geo& g, const D4* q, const D4* dq_in, D4* d
     else if (mb == 4) sweep_launch_t<false, 4>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
     else sweep_launch_t<false, 3>(g, q, dq_in, dq_out, gas, ctl, it0, sweep, st);
   }
+}
+
+// LSKUM_ZERO_COPY=1: the copy-back writes a pinned store directly from the
+// pack kernel (no 21-slot device pack buffer: 6.7 GB at 40M points) instead of
+// packing on the device and copying in chunks.  Off by default: the copy
+// engines are faster (40M: 127 ms zero copy vs 119 ms packed + DMA).
+bool zero_copy_store() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_ZERO_COPY");
+    return (e && std::atoi(e) == 1) ? 1 : 0;
+  }();
+  return v != 0;
 }
 
 // Tiled sweep (tiles.cuh) for uniform 8-point stencils.  LSKUM_SWEEP_TILE
@@ -768,6 +794,45 @@ __global__ void k_pack_fields(int n, int lo, int hi, int soa, const D4* prim, co
   }
 }
 
+// The 21-slot store in the AoS layout written straight into pinned host memory
+// (zero copy, no device pack buffer): a block gathers its 256 points' records
+// in shared memory, then writes them as one contiguous run of 16-byte stores,
+// so the writes reach the host as full PCIe transactions.
+constexpr int kPackPts = 256;
+__global__ void __launch_bounds__(kPackPts) k_pack_aos_host(int n, const D4* prim, const D4* q, const D4* dq,
+                                                            long long dq_ps, const D4* res, const double* dt,
+                                                            double* out) {
+  __shared__ __align__(16) double tile[kPackPts * 21];
+  for (long long p0 = static_cast<long long>(blockIdx.x) * kPackPts; p0 < n;
+       p0 += static_cast<long long>(gridDim.x) * kPackPts) {
+    const long long i = p0 + threadIdx.x;
+    if (i < n) {
+      D4 qx, qy;
+      dq_load(dq, dq_ps, i, qx, qy);
+      const D4 v[5] = {prim[i], q[i], qx, qy, res[i]};
+      double* r = tile + threadIdx.x * 21;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        r[4 * k] = v[k].a;
+        r[4 * k + 1] = v[k].b;
+        r[4 * k + 2] = v[k].c;
+        r[4 * k + 3] = v[k].d;
+      }
+      r[20] = dt[i];
+    }
+    __syncthreads();
+    const int pts = n - p0 < kPackPts ? static_cast<int>(n - p0) : kPackPts;
+    const int chunks = pts * 21 * 8 / 16;  // whole 16-byte chunks
+    const double2* src = reinterpret_cast<const double2*>(tile);
+    double2* o = reinterpret_cast<double2*>(out + p0 * 21);
+    for (int c = threadIdx.x; c < chunks; c += kPackPts) o[c] = src[c];
+    if ((pts * 21) & 1) {  // an odd trailing double
+      if (threadIdx.x == 0) out[p0 * 21 + pts * 21 - 1] = tile[pts * 21 - 1];
+    }
+    __syncthreads();
+  }
+}
+
 // Scatters the primitives (slots 0-3 of a FieldBlock in either layout) into D4 records.
 // ---- stencil screening on the device (reference validate_cloud,
 // cloud.cpp:252-321; host twin: host/screen.cpp).  Same sums in the same
@@ -1060,6 +1125,7 @@ class Domain {
     if (direct) {
       const int blocks = static_cast<int>(std::min<std::size_t>(4096, (nl + 255) / 256));
       DBuf<double> tx(std::max<std::size_t>(1, nl), st_), ty(std::max<std::size_t>(1, nl), st_);
+      trace("domain: direct temporaries");
       auto planes = [&](const double* a, const double* b, double2* out, const char* what) {
         ck(cudaMemcpyAsync(tx.get(), a, nl * sizeof(double), cudaMemcpyHostToDevice, st_), what);
         ck(cudaMemcpyAsync(ty.get(), b, nl * sizeof(double), cudaMemcpyHostToDevice, st_), what);
@@ -1084,6 +1150,7 @@ class Domain {
         ck(cudaStreamSynchronize(st_), "geometry planes");  // tx/ty are reused
         planes(gv.nx, gv.ny, nrm_.get(), "H2D nx/ny");
       }
+      trace("domain: direct copies queued");
       ck(cudaStreamSynchronize(st_), "geometry upload");  // temporaries go back to the pool
       trace("domain: direct copies done");
     }
@@ -1262,6 +1329,10 @@ class Domain {
     Screening out;
     const int n = n_;
     if (n <= 0) return out;
+    if (tracing()) {
+      cudaEventCreate(&ev_trace_);
+      cudaEventRecord(ev_trace_, st_);
+    }
     DBuf<ScreenOut> so(1, st_);
     ScreenOut init{0, 0, 0, 0x7FFFFFFF, 0};
     ck(cudaMemcpyAsync(so.get(), &init, sizeof init, cudaMemcpyHostToDevice, st_), "H2D screen");
@@ -1276,6 +1347,18 @@ class Domain {
     trace_sync(st_, "screen: sorted");
     ScreenOut head{};
     ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
+    if (tracing()) {  // device time of the work queued so far vs the host's wait
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st_);
+      cudaEventSynchronize(e);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev_trace_, e);
+      char buf[96];
+      std::snprintf(buf, sizeof buf, "screen: device work since upload %.2f ms", ms);
+      trace(buf);
+      cudaEventDestroy(e);
+    }
     ck(cudaStreamSynchronize(st_), "screen keys");
     if (head.n_finite > 0) {
       unsigned long long bits = 0;
@@ -1372,8 +1455,26 @@ class Domain {
     if (with_q && (gid_host_.empty() || (n_loc_ == n_ && static_cast<std::size_t>(f.size()) == n))) {
       // pack on the device in the host layout (scattered to cloud order when
       // the domain is a permutation of the whole cloud), one D2H into the store
-      DBuf<double> packed(21 * n, st_);
       const bool soa = f.layout() == Layout::soa;
+      void* hdev = nullptr;
+      if (f.pinned() && gid_host_.empty() && zero_copy_store() &&
+          cudaHostGetDevicePointer(&hdev, f.raw(), 0) == cudaSuccess && hdev) {
+        // pinned store in cloud order: the kernels write it directly (zero copy)
+        double* out = static_cast<double*>(hdev);
+        if (soa)  // 21 rows: consecutive points of a row are consecutive addresses
+          k_pack_fields<<<std::min<int>((n_ + 255) / 256, 4096), 256, 0, st_>>>(
+              n_, 0, n_, 1, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(), dt_.get(), nullptr,
+              out);
+        else
+          k_pack_aos_host<<<std::min<int>((n_ + kPackPts - 1) / kPackPts, 2048), kPackPts, 0, st_>>>(
+              n_, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(), dt_.get(), out);
+        ck(cudaGetLastError(), "k_pack (zero copy)");
+        ck(cudaStreamSynchronize(st_), "download");
+        trace("download: stored (zero copy)");
+        return;
+      }
+      cudaGetLastError();
+      DBuf<double> packed(21 * n, st_);
       auto pack = [&](int lo, int hi) {
         k_pack_fields<<<std::max(1, std::min<int>((hi - lo + 255) / 256, 4096)), 256, 0, st_>>>(
             n_, lo, hi, soa ? 1 : 0, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(), dt_.get(),
@@ -1405,6 +1506,7 @@ class Domain {
               err = cudaMemcpyAsync(f.raw() + 21ll * lo, packed.get() + 21ll * lo, 21ll * (hi - lo) * sizeof(double),
                                     cudaMemcpyDeviceToHost, cs);
           }
+          trace("download: chunks queued");
           const cudaError_t serr = cudaStreamSynchronize(cs);
           for (auto& e : packed_ev) cudaEventDestroy(e);
           cudaStreamDestroy(cs);
@@ -2161,6 +2263,7 @@ class Domain {
   DBuf<std::uint16_t> tslot_;
   int ntiles_ = 0, tiles_staged_ = 0, tile_p_ = 128;
   unsigned long long zero_pairs_ = 0;  // pairs with dx == 0 or dy == 0 (non-outer points)
+  cudaEvent_t ev_trace_ = nullptr;     // LSKUM_TRACE: device-time reference of the screening
   bool tiles_ = false;
   DBuf<PointFlux> pf_;           // first order: split fluxes per point (owned + halo)
   DBuf<std::uint8_t> psign_;     // first order: half-stencil signs / zero offset per pair

@@ -3,11 +3,12 @@
 Large clouds keep their per-point arrays in pinned host memory (HostAlloc,
 host/core.hpp) and the engine uploads them with DMAs straight from those
 arrays; with LSKUM_PINNED_CLOUD=0 (heap arrays) the same geometry goes through
-pinned staging in point chunks.  The copy-back packs and copies the 21-slot
-store in point chunks on two streams.  Whatever the path, the results must be
-bitwise the same: a 10M-point run (direct upload, chunked copy-back) is
-compared with the same run in a child process on heap arrays (staged upload),
-in both store layouts.
+pinned staging in point chunks.  The copy-back packs the 21-slot store on the
+device and copies it in point chunks on two streams; with LSKUM_ZERO_COPY=1 the
+pack kernel writes the pinned store directly.  Whatever the path, the results
+must be bitwise the same: a 10M-point run (direct upload, chunked copy-back) is
+compared with the same run in a child process on heap arrays (staged upload)
+with the zero-copy store, in both store layouts.
 """
 import os
 import subprocess
@@ -54,7 +55,7 @@ def test_direct_upload_and_chunked_copy_back_are_bitwise_the_staged_paths(layout
     res, f = case(layout)
     out = str(tmp_path / "heap")
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), layout=repr(layout), out=out)
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LSKUM_PINNED_CLOUD="0"),
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LSKUM_PINNED_CLOUD="0", LSKUM_ZERO_COPY="1"),
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     assert np.array_equal(res, np.load(out + "_res.npy"))
