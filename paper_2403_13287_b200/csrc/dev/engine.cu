@@ -476,7 +476,8 @@ int sweep_tile_p() {
 
 template <bool S, int TP>
 void sweep_tile_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl, int sweep,
-                         const TilePlan* plan, const std::uint16_t* slot, int ntiles, cudaStream_t st) {
+                         const TilePlan* plan, const std::uint16_t* slot, int ntiles, const int* tlist,
+                         cudaStream_t st) {
   constexpr int MB = TileShape<TP>::MB, smax = TileShape<TP>::smax;
   constexpr std::size_t smem = 2 * tile_stage_bytes(TP, smax);
   auto kern = k_sweep_tile<S, TP, MB>;
@@ -492,14 +493,15 @@ void sweep_tile_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out,
     resident[dev & 63] = std::max(1, per_sm) * sms;
   }
   const int grid = std::max(1, std::min(ntiles, resident[dev & 63]));
-  launch_pdl(kern, grid, 2 * TP, smem, st, g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, smax, ntiles);
+  launch_pdl(kern, grid, 2 * TP, smem, st, g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, smax, ntiles, tlist);
 }
 
 template <bool S>
 void sweep_tile_launch(int tp, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
-                       int sweep, const TilePlan* plan, const std::uint16_t* slot, int ntiles, cudaStream_t st) {
-  if (tp == 64) sweep_tile_launch_t<S, 64>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, st);
-  else sweep_tile_launch_t<S, 128>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, st);
+                       int sweep, const TilePlan* plan, const std::uint16_t* slot, int ntiles, const int* tlist,
+                       cudaStream_t st) {
+  if (tp == 64) sweep_tile_launch_t<S, 64>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+  else sweep_tile_launch_t<S, 128>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
 }
 
 // Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per
@@ -1735,17 +1737,24 @@ class Domain {
     g.list = list;
     g.nlist = nlist;
     if (!list && tiles_) {
-      if (strict_)
-        sweep_tile_launch<true>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
-                                tplan_.get(), tslot_.get(), ntiles_, st_);
-      else
-        sweep_tile_launch<false>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
-                                 tplan_.get(), tslot_.get(), ntiles_, st_);
+      launch_sweep_tiles(a, b, s, nullptr, ntiles_);
       return;
     }
     sweep_launch(strict_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(),
                  s == 0 ? it0_.get() : nullptr, s, st_);
   }
+  // Tiled sweep over the tiles tlist[0 .. ntl) (null: all ntl tiles).
+  void launch_sweep_tiles(int a, int b, int s, const int* tlist, int ntl) {
+    const Geo g = geo();
+    if (strict_)
+      sweep_tile_launch<true>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
+                              tplan_.get(), tslot_.get(), ntl, tlist, st_);
+    else
+      sweep_tile_launch<false>(tile_p_, g, q_[a].get(), dq_[b].get(), dq_[b ^ 1].get(), gas_, ctl_.get(), s,
+                               tplan_.get(), tslot_.get(), ntl, tlist, st_);
+  }
+  bool tiled() const { return tiles_; }
+  int tile_points() const { return tile_p_; }
   // Tile plan of the tiled sweep (geometry only, once per domain; uniform
   // 8-point stencils).  Returns the number of tiles that are staged.
   int ensure_tiles() {
@@ -2953,6 +2962,7 @@ class RankRun {
     dom_->upload(ps_.fields, false);
     dom_->set_split4(spec_.split4);
     if (rank_ != 0) dom_->reset_run(spec_.order, spec_.inner, spec_.fp_mode, spec_.chunk, false);
+    split_tiles();
     dom_->first_q();
     ck(cudaStreamSynchronize(dom_->stream()), "first q");
     dom_->refresh_ctl();
@@ -3084,6 +3094,36 @@ class RankRun {
     return exec;
   }
 
+  // With a tile plan the sweeps' interior work runs tiled: the tiles none of
+  // whose points reads a halo slot go to the tiled sweep (tile_in_) while the
+  // halo is in flight; the points of the other tiles (bd_tiles_, a superset
+  // of the boundary points) to the list sweep after it.
+  void split_tiles() {
+    if (!dom_->tiled() || tiles_split_) return;
+    const LocalGeom& g = geoms_[rank_];
+    const int tp = dom_->tile_points();
+    std::vector<int> tin, bpts;
+    for (std::int32_t t0 = 0; t0 < g.n_own; t0 += tp) {
+      const std::int32_t t1 = std::min<std::int32_t>(g.n_own, t0 + tp);
+      bool touches = false;
+      for (std::int32_t i = t0; i < t1 && !touches; ++i)
+        for (std::int64_t e = g.off[i]; e < g.off[i + 1] && !touches; ++e) touches = g.nbr[e] >= g.n_own;
+      if (touches)
+        for (std::int32_t i = t0; i < t1; ++i) bpts.push_back(i);
+      else
+        tin.push_back(t0 / tp);
+    }
+    n_tile_in_ = static_cast<int>(tin.size());
+    n_bd_tiles_ = static_cast<int>(bpts.size());
+    tile_in_.alloc(std::max<std::size_t>(1, tin.size()));
+    bd_tiles_.alloc(std::max<std::size_t>(1, bpts.size()));
+    if (!tin.empty())
+      ck(cudaMemcpy(tile_in_.get(), tin.data(), tin.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D tiles");
+    if (!bpts.empty())
+      ck(cudaMemcpy(bd_tiles_.get(), bpts.data(), bpts.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D tiles");
+    tiles_split_ = true;
+  }
+
   // Second order with halo latency hidden behind interior work: each sweep and
   // the flux run first over the interior points (no halo reads), then wait for
   // the owners, gather the halo of the previous stage and finish the boundary
@@ -3104,7 +3144,8 @@ class RankRun {
       const int b = (t * spec_.inner + s) & 1;
       wait_for(readers_, FL_DQH, inner, s - 1, 1 + s);
       if (timed && s == 0) d.record_ext(kev_[0]);
-      d.launch_sweep(a, b, s, in, n_interior_);
+      if (tiles_split_) d.launch_sweep_tiles(a, b, s, tile_in_.get(), n_tile_in_);
+      else d.launch_sweep(a, b, s, in, n_interior_);
       if (s == 0) {
         wait_for(src_, FL_UPD, 1, 0, 1);  // owners' q of iteration t
         d.launch_halo(d.q_buf(a), 1, hdom_.get(), hidx_.get(), qp_[a], 1, true);
@@ -3113,7 +3154,8 @@ class RankRun {
         d.launch_halo(d.dq_buf(b), 2, hdom_.get(), hidx_.get(), dqp_[b], 1 + s);
         signal(FL_DQH, inner, s);
       }
-      d.launch_sweep(a, b, s, bd, n_boundary_);
+      if (tiles_split_) d.launch_sweep(a, b, s, bd_tiles_.get(), n_bd_tiles_);
+      else d.launch_sweep(a, b, s, bd, n_boundary_);
       if (timed && s == 0) d.record_ext(kev_[1]);
       launches_ += 3;  // interior sweep, halo, boundary sweep
       signal(FL_SW, inner, s + 1);
@@ -3198,6 +3240,9 @@ class RankRun {
   DBuf<int> hdom_, hidx_;
   DBuf<int> interior_, boundary_;
   int n_interior_ = 0, n_boundary_ = 0;
+  DBuf<int> tile_in_, bd_tiles_;  // interior tiles / points of the other tiles (split_tiles)
+  int n_tile_in_ = 0, n_bd_tiles_ = 0;
+  bool tiles_split_ = false;
   DBuf<unsigned long long> flags_;
   PeerTab qp_[2]{}, dqp_[2]{};
   unsigned long long* flag_[kMaxDomains] = {};

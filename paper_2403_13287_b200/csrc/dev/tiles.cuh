@@ -204,7 +204,9 @@ template <bool S, int TP, int MB>
 __global__ void __launch_bounds__(2 * TP, MB)
     k_sweep_tile(Geo g, const D4* __restrict__ q, const D4* __restrict__ dq_in, D4* __restrict__ dq_out, Gas gas,
                  Ctl* ctl, int sweep, const TilePlan* __restrict__ plan, const std::uint16_t* __restrict__ slot,
-                 int smax, int ntiles) {
+                 int smax, int ntiles, const int* __restrict__ tlist) {
+  // tlist: visit only the tiles tlist[0 .. ntiles) (a rank's interior tiles);
+  // null: tiles 0 .. ntiles.  k below is the visit index, tile_at(k) the tile.
   constexpr int NS = 2;
   constexpr int NW = 2 * TP / 32;
   pdl_enter();
@@ -234,9 +236,11 @@ __global__ void __launch_bounds__(2 * TP, MB)
   auto qy_of = [&](int s) { return xy_of(s) + static_cast<std::size_t>(smax) * 80; };
   const D4* qyp = dq_in + g.nloc;
   const int grid = static_cast<int>(gridDim.x);
-  // Refill stage s with `tile` (one warp; pp = the tile's plan, in global or
-  // shared memory; lane r reads interval r).
-  auto issue = [&](int tile, int s, const TilePlan* pp) {
+  auto tile_at = [&](int k) { return tlist ? tlist[k] : k; };
+  // Refill stage s with the tile of visit k (one warp; pp = the tile's plan,
+  // in global or shared memory; lane r reads interval r).
+  auto issue = [&](int k, int s, const TilePlan* pp) {
+    const int tile = tile_at(k);
     const int nint = pp->nint, own = pp->own, staged = pp->staged;
     const TileIv v = lane < nint ? pp->iv[lane] : TileIv{0, 0};
     const int len = v.len;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(2 * TP, MB)
     }
     off -= len;
     const long long start = v.start;
-    const int next = tile + NS * grid;
+    const int next = k + NS * grid;
     const int npts = min(TP, g.n - tile * TP);
     __syncwarp();  // every lane has read the plan (it may live in the stage being refilled)
     if (lane == 0) {
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(2 * TP, MB)
       mbar_arrive_tx(&full[s], bytes);
     }
     __syncwarp();
-    if (lane == 0 && next < ntiles) bulk_g2s(stage(s), plan + next, 80u, &full[s]);
+    if (lane == 0 && next < ntiles) bulk_g2s(stage(s), plan + tile_at(next), 80u, &full[s]);
     if (lane == 1) bulk_g2s(slots_of(s), slot + 8ll * tile * TP, 16u * npts, &full[s]);
     if (len > 0) {
       bulk_g2s(xy_of(s) + off * 16, g.xy + start, len * 16u, &full[s]);
@@ -269,16 +273,17 @@ __global__ void __launch_bounds__(2 * TP, MB)
   const int warp = tid >> 5;
   if (run && warp == 0) {
     for (int s = 0; s < NS; ++s) {
-      const int tile = blockIdx.x + s * grid;
-      if (tile < ntiles) issue(tile, s, plan + tile);
+      const int k = blockIdx.x + s * grid;
+      if (k < ntiles) issue(k, s, plan + tile_at(k));
     }
   }
   const int p = tid >> 1, h = tid & 1;
   const GlobalSrc gsrc{reinterpret_cast<const double*>(g.xy), reinterpret_cast<const double*>(q) + 2 * h,
                        reinterpret_cast<const double*>(dq_in) + 2 * h, reinterpret_cast<const double*>(qyp) + 2 * h};
   int it = 0;
-  for (int tile = blockIdx.x; run && tile < ntiles; tile += grid, ++it) {
+  for (int k = blockIdx.x; run && k < ntiles; k += grid, ++it) {
     const int s = it & (NS - 1);
+    const int tile = tile_at(k);
     mbar_wait(&full[s], static_cast<unsigned>(it / NS) & 1u);
     const int2 th = cur[s];
     const int i = tile * TP + p;
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(2 * TP, MB)
       if (last) done[s] = 0;
     }
     last = __shfl_sync(0xFFFFFFFFu, last, 0);
-    const int next = tile + NS * grid;
+    const int next = k + NS * grid;
     if (last && next < ntiles) issue(next, s, reinterpret_cast<const TilePlan*>(stage(s)));
   }
   __syncthreads();
