@@ -474,13 +474,13 @@ int sweep_tile_p() {
   return v;
 }
 
-template <bool S, int TP>
+template <bool S, int TP, bool LIST>
 void sweep_tile_launch_t(const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl, int sweep,
                          const TilePlan* plan, const std::uint16_t* slot, int ntiles, const int* tlist,
                          cudaStream_t st) {
   constexpr int MB = TileShape<TP>::MB, smax = TileShape<TP>::smax;
   constexpr std::size_t smem = 2 * tile_stage_bytes(TP, smax);
-  auto kern = k_sweep_tile<S, TP, MB>;
+  auto kern = k_sweep_tile<S, TP, MB, LIST>;
   static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -500,8 +500,13 @@ template <bool S>
 void sweep_tile_launch(int tp, const Geo& g, const D4* q, const D4* dq_in, D4* dq_out, const Gas& gas, Ctl* ctl,
                        int sweep, const TilePlan* plan, const std::uint16_t* slot, int ntiles, const int* tlist,
                        cudaStream_t st) {
-  if (tp == 64) sweep_tile_launch_t<S, 64>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
-  else sweep_tile_launch_t<S, 128>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+  if (tp == 64) {
+    if (tlist) sweep_tile_launch_t<S, 64, true>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+    else sweep_tile_launch_t<S, 64, false>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+  } else {
+    if (tlist) sweep_tile_launch_t<S, 128, true>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+    else sweep_tile_launch_t<S, 128, false>(g, q, dq_in, dq_out, gas, ctl, sweep, plan, slot, ntiles, tlist, st);
+  }
 }
 
 // Register/occupancy trade-off of the W=8 kernel: minimum resident blocks per

@@ -200,7 +200,7 @@ __host__ __device__ constexpr std::size_t tile_stage_bytes(int tp, int smax) {
 // itself out (shared atomic); the last one refills the stage from the plan
 // record that came with it (lane r issues interval r's four copies), so no
 // block barrier sits in the loop and no refill waits on global memory.
-template <bool S, int TP, int MB>
+template <bool S, int TP, int MB, bool LIST = false>
 __global__ void __launch_bounds__(2 * TP, MB)
     k_sweep_tile(Geo g, const D4* __restrict__ q, const D4* __restrict__ dq_in, D4* __restrict__ dq_out, Gas gas,
                  Ctl* ctl, int sweep, const TilePlan* __restrict__ plan, const std::uint16_t* __restrict__ slot,
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(2 * TP, MB)
   auto qy_of = [&](int s) { return xy_of(s) + static_cast<std::size_t>(smax) * 80; };
   const D4* qyp = dq_in + g.nloc;
   const int grid = static_cast<int>(gridDim.x);
-  auto tile_at = [&](int k) { return tlist ? tlist[k] : k; };
+  auto tile_at = [&](int k) { return LIST ? tlist[k] : k; };
   // Refill stage s with the tile of visit k (one warp; pp = the tile's plan,
   // in global or shared memory; lane r reads interval r).
   auto issue = [&](int k, int s, const TilePlan* pp) {
