@@ -1388,7 +1388,7 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
 // records (q: 1; dq: the qx and qy planes, dq_load), plane r of point p at
 // base + r * ps + p — read directly over peer memory (NVLink/NVSwitch when the
 // domains sit on different GPUs).
-constexpr int kMaxDomains = 16;
+constexpr int kMaxDomains = 64;  // domains (GPUs / ranks) per run
 struct PeerTab {
   const D4* base[kMaxDomains];
   long long ps[kMaxDomains];  // plane stride (the owner's local point count)
