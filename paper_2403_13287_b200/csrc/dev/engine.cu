@@ -3389,6 +3389,121 @@ double session_step_flushed(Session* s, bool kernel_events) {
   return ms;
 }
 
+// ---- exact kNN queries on attach_knn's 2-d tree (host/synth.cpp): one thread
+// per point, in tree order (neighbouring threads walk similar paths).  The k
+// best by (d^2, id) are kept sorted in registers; a subtree is skipped only
+// when its box's lower bound exceeds the current k-th distance strictly, and
+// distances and bounds are formed with separately rounded products and sums
+// (no FMA) exactly as on the host — so the set is the host's, which is the
+// reference's build_stencils set (cloud.cpp:137-237).
+template <int K>
+__global__ void __launch_bounds__(128) k_knn(const KdNode* __restrict__ nodes, const KdPt* __restrict__ pts, int n,
+                                             std::int32_t* __restrict__ nbr) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const KdPt me = pts[t];
+  const double px = me.x, py = me.y;
+  double bd[K];
+  int bi[K];
+  int cnt = 0;
+  auto bound = [&](const KdNode& b) {
+    const double ex = px < b.x0 ? __dsub_rn(b.x0, px) : (px > b.x1 ? __dsub_rn(px, b.x1) : 0.0);
+    const double ey = py < b.y0 ? __dsub_rn(b.y0, py) : (py > b.y1 ? __dsub_rn(py, b.y1) : 0.0);
+    return __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+  };
+  int stack[96];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const KdNode b = nodes[stack[--sp]];
+    if (cnt == K && bound(b) > bd[K - 1]) continue;
+    if (b.left < 0) {
+      for (int e = b.lo; e < b.hi; ++e) {
+        const KdPt c = pts[e];
+        if (c.id == me.id) continue;
+        const double dx = __dsub_rn(c.x, px), dy = __dsub_rn(c.y, py);
+        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        if (cnt == K && !(d2 < bd[K - 1] || (d2 == bd[K - 1] && c.id < bi[K - 1]))) continue;
+        int j = cnt < K ? cnt++ : K - 1;  // insertion into the sorted list
+        while (j > 0 && (d2 < bd[j - 1] || (d2 == bd[j - 1] && c.id < bi[j - 1]))) {
+          bd[j] = bd[j - 1];
+          bi[j] = bi[j - 1];
+          --j;
+        }
+        bd[j] = d2;
+        bi[j] = c.id;
+      }
+      continue;
+    }
+    const double bl = bound(nodes[b.left]), br = bound(nodes[b.right]);
+    if (sp + 2 > 96) __trap();  // depth far beyond any median-split tree of 2^31 points
+    if (bl <= br) {  // nearer child last, so it is visited first
+      stack[sp++] = b.right;
+      stack[sp++] = b.left;
+    } else {
+      stack[sp++] = b.left;
+      stack[sp++] = b.right;
+    }
+  }
+  // ids ascending (the reference sorts each stencil)
+  for (int a = 1; a < K; ++a) {
+    const int v = bi[a];
+    int j = a;
+    while (j > 0 && bi[j - 1] > v) {
+      bi[j] = bi[j - 1];
+      --j;
+    }
+    bi[j] = v;
+  }
+  std::int32_t* out = nbr + static_cast<long long>(me.id) * K;
+  for (int j = 0; j < K; ++j) out[j] = bi[j];
+}
+
+template <int K>
+void knn_launch(const KdNode* nodes, const KdPt* pts, int n, std::int32_t* nbr, cudaStream_t st) {
+  k_knn<K><<<(n + 127) / 128, 128, 0, st>>>(nodes, pts, n, nbr);
+}
+
+bool engine_knn(const std::vector<KdNode>& nodes, const std::vector<KdPt>& pts, int k, std::int32_t* nbr) {
+  int count = 0;
+  const bool supported = (k >= 3 && k <= 8) || k == 12 || k == 16;
+  if (!supported || cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return false;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ensure_pool(dev);
+  const int n = static_cast<int>(pts.size());
+  cudaStream_t st = nullptr;
+  ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+  {
+    DBuf<KdNode> dn(nodes.size(), st);
+    DBuf<KdPt> dp(pts.size(), st);
+    DBuf<std::int32_t> dnbr(static_cast<std::size_t>(n) * k, st);
+    ck(cudaMemcpyAsync(dn.get(), nodes.data(), nodes.size() * sizeof(KdNode), cudaMemcpyHostToDevice, st), "H2D kd");
+    ck(cudaMemcpyAsync(dp.get(), pts.data(), pts.size() * sizeof(KdPt), cudaMemcpyHostToDevice, st), "H2D kd");
+    switch (k) {
+      case 3: knn_launch<3>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 4: knn_launch<4>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 5: knn_launch<5>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 6: knn_launch<6>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 7: knn_launch<7>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 8: knn_launch<8>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 12: knn_launch<12>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      case 16: knn_launch<16>(dn.get(), dp.get(), n, dnbr.get(), st); break;
+      default: break;
+    }
+    ck(cudaGetLastError(), "k_knn");
+    ck(cudaMemcpyAsync(nbr, dnbr.get(), static_cast<std::size_t>(n) * k * sizeof(std::int32_t), cudaMemcpyDeviceToHost,
+                       st),
+       "D2H knn");
+    ck(cudaStreamSynchronize(st), "knn");
+  }
+  cudaStreamDestroy(st);
+  return true;
+}
+
 __global__ void k_math_selftest(int fn, const double* in, long long n, double* ref, double* ours) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {

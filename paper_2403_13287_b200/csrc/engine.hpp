@@ -34,6 +34,11 @@ struct EngineSpec {
   bool* store_written = nullptr;
 };
 
+// Exact k nearest neighbours by (d^2, id) of every point, from attach_knn's
+// 2-d tree, on the GPU: nbr[p * k ..] = the ids, ascending.  False when no
+// device is usable or k is not one of 3..8, 12, 16 (the caller queries on the host).
+bool engine_knn(const std::vector<KdNode>& nodes, const std::vector<KdPt>& pts, int k, std::int32_t* nbr);
+
 // Stencil screening on the device into ps.screening (single-device runs; no-op
 // when the report is cached or gpus > 1).
 void engine_prescreen(PointSet& ps, const Settings& s);

@@ -269,6 +269,16 @@ PointSet make_naca0012(int n_wall, int n_rings, double r_outer, double jitter, s
                        bool frozen_wall);
 void attach_knn(PointSet& ps, int k);
 
+// 2-d tree of attach_knn (synth.cpp), also queried on the GPU (engine_knn).
+struct KdNode {
+  double x0, x1, y0, y1;              // bounding box of points [lo, hi)
+  std::int32_t lo, hi, left, right;   // leaf: left = right = -1
+};
+struct KdPt {
+  double x, y;
+  std::int32_t id, pad;
+};
+
 // ---- stencil screening (reference cloud.cpp:252-321) ----
 struct Screening {
   double h_ref = 0.0, det_tol = 0.0;

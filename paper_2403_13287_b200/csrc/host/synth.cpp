@@ -9,8 +9,10 @@
 // processed in parallel (the result is independent of the thread count).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <random>
 
+#include "../engine.hpp"
 #include "core.hpp"
 #include "par.hpp"
 
@@ -81,16 +83,10 @@ void attach_knn(PointSet& ps, int k) {
   // (an equal bound may still hold a tie with a smaller id); the bound is
   // computed with the same rounded operations as the point distances, which
   // are monotone, so it never exceeds the distance of a point inside.
-  struct Node {
-    double x0, x1, y0, y1;
-    std::int32_t lo, hi, left, right;
-  };
-  struct Pt {
-    double x, y;
-    std::int32_t id;
-  };
+  using Node = KdNode;
+  using Pt = KdPt;
   std::vector<Pt> pts(n);
-  for (std::int32_t i = 0; i < n; ++i) pts[i] = Pt{ps.x[i], ps.y[i], i};
+  for (std::int32_t i = 0; i < n; ++i) pts[i] = Pt{ps.x[i], ps.y[i], i, 0};
   constexpr std::int32_t kLeaf = 16;
   // Median split along the box's longer side; returns the split index or -1
   // for a leaf.  Writes the box of [lo, hi) into `nd`.
@@ -195,9 +191,18 @@ void attach_knn(PointSet& ps, int k) {
       nodes.push_back(nd);
     }
   }
+  trace("knn: tree built");
+  // the queries on the GPU when there is one (LSKUM_GPU_KNN=0: host)
+  static const bool gpu_knn = [] {
+    const char* e = std::getenv("LSKUM_GPU_KNN");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (gpu_knn && n >= (1 << 16) && k <= 16 && engine_knn(nodes, pts, k, ps.nbr.data())) {
+    trace("knn: queried (GPU)");
+    return;
+  }
   std::vector<std::int32_t> idx(n);
   for (std::int32_t i = 0; i < n; ++i) idx[i] = pts[i].id;
-  trace("knn: tree built");
   parallel_slices(n, [&](std::int64_t lo, std::int64_t hi) {
     std::vector<Cand> heap;
     std::vector<std::int32_t> stack;
