@@ -607,11 +607,22 @@ bool flux_u8() {
   return v != 0;
 }
 
-template <int MB, int NW, int HP, bool U8>
+// Rare-path deferral of the staged flux kernel (k_flux_ws<.., DEFER>, then
+// k_flux_redo over the points it listed); LSKUM_FLUX_DEFER=0 keeps the
+// fallback branches inside the staged kernel.
+bool flux_defer() {
+  static int v = [] {
+    const char* e = std::getenv("LSKUM_FLUX_DEFER");
+    return (e && std::atoi(e) == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+template <int MB, int NW, int HP, bool U8, bool DEFER>
 void flux_ws_launch_k(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                      cudaStream_t st) {
+                      const FluxRedo& rd, cudaStream_t st) {
   constexpr std::size_t smem = static_cast<std::size_t>(2 * NW) * kFluxStageBytes;
-  auto kern = k_flux_ws<MB, NW, HP, U8>;
+  auto kern = k_flux_ws<MB, NW, HP, U8, DEFER>;
   static int resident[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -625,34 +636,51 @@ void flux_ws_launch_k(const FluxArgs& a, const double2* w1, const double2* w2, c
   }
   const int groups = ((a.g.list ? a.g.nlist : a.g.n) + 3) / 4;
   const int blocks = std::max(1, std::min((groups + NW - 1) / NW, resident[dev & 63]));
-  launch_pdl(kern, blocks, NW * 32, smem, st, a, w1, w2, sing);
+  launch_pdl(kern, blocks, NW * 32, smem, st, a, w1, w2, sing, rd);
+  if constexpr (DEFER) {
+    // one warp step per 4096 points, at most two blocks per SM
+    const int steps = (a.g.n + kRedoPointsPer - 1) / kRedoPointsPer;
+    static int sms[64] = {};
+    if (!sms[dev & 63]) ck(cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev), "attr");
+    const int rblocks = std::max(1, std::min((steps + 7) / 8, 2 * sms[dev & 63]));
+    launch_pdl(k_flux_redo, rblocks, 256, 0, st, a, w1, w2, sing, rd);
+  }
+}
+
+template <int MB, int NW, int HP, bool U8>
+void flux_ws_launch_d(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
+                      const FluxRedo* rd, cudaStream_t st) {
+  if (rd) flux_ws_launch_k<MB, NW, HP, U8, true>(a, w1, w2, sing, *rd, st);
+  else flux_ws_launch_k<MB, NW, HP, U8, false>(a, w1, w2, sing, FluxRedo{nullptr}, st);
 }
 
 template <int MB, int NW, int HP>
 void flux_ws_launch_hp(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                       cudaStream_t st) {
-  if (a.g.kfix == 8 && !a.g.list && flux_u8()) flux_ws_launch_k<MB, NW, HP, true>(a, w1, w2, sing, st);
-  else flux_ws_launch_k<MB, NW, HP, false>(a, w1, w2, sing, st);
+                       const FluxRedo* rd, cudaStream_t st) {
+  if (a.g.kfix == 8 && !a.g.list && flux_u8()) flux_ws_launch_d<MB, NW, HP, true>(a, w1, w2, sing, rd, st);
+  else flux_ws_launch_d<MB, NW, HP, false>(a, w1, w2, sing, rd, st);
 }
 
 template <int MB, int NW>
 void flux_ws_launch(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                    cudaStream_t st) {
-  if (a.gas.half_pow == 5) flux_ws_launch_hp<MB, NW, 5>(a, w1, w2, sing, st);
-  else flux_ws_launch_hp<MB, NW, -1>(a, w1, w2, sing, st);
+                    const FluxRedo* rd, cudaStream_t st) {
+  if (a.gas.half_pow == 5) flux_ws_launch_hp<MB, NW, 5>(a, w1, w2, sing, rd, st);
+  else flux_ws_launch_hp<MB, NW, -1>(a, w1, w2, sing, rd, st);
 }
 
+// rd: the domain's redo list (null: no deferral).
 void flux_w_launch(const FluxArgs& a, int kmax, const double2* w1, const double2* w2, const std::uint8_t* sing,
-                   cudaStream_t st) {
+                   const FluxRedo* rd, cudaStream_t st) {
   const int groups = (a.g.n + 3) / 4;
   if (kmax <= 8 && flux_staged()) {
+    if (!flux_defer()) rd = nullptr;
     switch (flux_ws_shape(a.g.n)) {
-      case 83: flux_ws_launch<3, 8>(a, w1, w2, sing, st); break;
-      case 44: flux_ws_launch<4, 4>(a, w1, w2, sing, st); break;
-      case 45: flux_ws_launch<5, 4>(a, w1, w2, sing, st); break;
-      case 63: flux_ws_launch<3, 6>(a, w1, w2, sing, st); break;
-      case 82: flux_ws_launch<2, 8>(a, w1, w2, sing, st); break;
-      default: flux_ws_launch<4, 4>(a, w1, w2, sing, st); break;
+      case 83: flux_ws_launch<3, 8>(a, w1, w2, sing, rd, st); break;
+      case 44: flux_ws_launch<4, 4>(a, w1, w2, sing, rd, st); break;
+      case 45: flux_ws_launch<5, 4>(a, w1, w2, sing, rd, st); break;
+      case 63: flux_ws_launch<3, 6>(a, w1, w2, sing, rd, st); break;
+      case 82: flux_ws_launch<2, 8>(a, w1, w2, sing, rd, st); break;
+      default: flux_ws_launch<4, 4>(a, w1, w2, sing, rd, st); break;
     }
     return;
   }
@@ -1714,10 +1742,21 @@ class Domain {
     psign_.alloc(nnz, st_);
     if (zero_pairs_) w2_.alloc(nnz, st_);  // counted by k_min_dist
     sing_.alloc(static_cast<std::size_t>(std::max(1, n_)), st_);
+    const std::size_t nwords =
+        static_cast<std::size_t>((std::max(1, n_) + kRedoPointsPer - 1) / kRedoPointsPer) * kRedoWordsPer;
+    redo_bits_.alloc(nwords, st_);
+    ck(cudaMemsetAsync(redo_bits_.get(), 0, nwords * sizeof(unsigned), st_), "zero redo bits");
+    DBuf<unsigned> any(1, st_);
+    ck(cudaMemsetAsync(any.get(), 0, sizeof(unsigned), st_), "zero any_sing");
     k_flux_weights<<<std::max(1, blocks), 256, 0, st_>>>(geo(), gas_.det_tol, w1_.get(), w2_.get(), sing_.get(),
                                                           psign_.get());
     ck(cudaGetLastError(), "k_flux_weights");
+    k_flux_any_sing<<<std::max(1, blocks), 256, 0, st_>>>(geo(), sing_.get(), any.get());
+    ck(cudaGetLastError(), "k_flux_any_sing");
+    unsigned any_h = 0;
+    ck(cudaMemcpyAsync(&any_h, any.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, st_), "D2H any_sing");
     ck(cudaStreamSynchronize(st_), "weights");
+    any_sing_ = any_h != 0;
     weights_ = true;
   }
 
@@ -1814,7 +1853,8 @@ class Domain {
                  static_cast<const double2*>(w2_.get()), static_cast<const std::uint8_t*>(sing_.get()),
                  static_cast<const std::uint8_t*>(psign_.get()));
     } else if (!strict_ && weights_) {
-      flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), st_);
+      const FluxRedo rd{redo_bits_.get()};
+      flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), any_sing_ ? nullptr : &rd, st_);
     } else {
       flux_launch(W_, strict_, fa, smem_, st_);
     }
@@ -2283,6 +2323,8 @@ class Domain {
   DBuf<std::uint8_t> psign_;     // first order: half-stencil signs / zero offset per pair
   DBuf<std::uint8_t> pfvalid_;
   DBuf<std::uint8_t> sing_;     // first singular split direction per point
+  DBuf<unsigned> redo_bits_;       // flux points whose evaluation took a rare path (k_flux_redo)
+  bool any_sing_ = false;          // a live point has a singular split stencil: no deferral
   bool weights_ = false;
   DBuf<Ctl> ctl_;
   DBuf<Shared> sh_;

@@ -771,11 +771,15 @@ __global__ void k_flux_weights(Geo g, double det_tol, double2* w1, double2* w2, 
 // reconstructions, the x and y split fluxes of each side (the pair's half
 // stencils), acc += w . dG.  Warp-convergent (inactive lanes evaluate their
 // own point with zero offsets and add nothing).
-template <int HP = -1>
+// DEFER: the rare branches (erf argument above 1.5, exponential range, an
+// invalid state: act && !ok) leave the instruction stream; the lane sets redo
+// instead and the caller has the point recomputed by k_flux_redo, which runs
+// this function without DEFER (same arithmetic, so the same bits).
+template <int HP = -1, bool DEFER = false>
 __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, bool act, double2 pi,
                                                const D4& qi, const D4& qxi, const D4& qyi, double2 pn,
                                                const D4& qn, const D4& qxn, const D4& qyn, double2 w,
-                                               const double2* w2e, double (&acc)[4]) {
+                                               const double2* w2e, double (&acc)[4], bool* redo = nullptr) {
   constexpr unsigned kFull = 0xFFFFFFFFu;
   const Geo& g = a.g;
   const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
@@ -791,10 +795,13 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
     tn[3] = -1.0;
   }
   FluxState fi, fn;
-  ok = reconstruct2<false, HP>(ti, tn, a.gas, fi, fn) && ok;
-  if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
+  bool rd = false;
+  ok = reconstruct2<false, HP, DEFER>(ti, tn, a.gas, fi, fn, rd) && ok;
+  if constexpr (DEFER) rd |= act && !ok;
+  else if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
   AxisTerms at[4];
-  axis_terms4<false>(fi, fn, at);
+  axis_terms4<false, DEFER>(fi, fn, at, rd);
+  if constexpr (DEFER) *redo |= rd;
   const bool store = act && ok;
   const double wx = store ? w.x : 0.0, wy = store ? w.y : 0.0;
   // dG = gn - gi is an explicitly rounded subtraction: a contracted
@@ -1043,14 +1050,15 @@ struct StageRaw {
 // U8: uniform 8-point stencils and every owned point visited (no subset
 // list): the stencil offsets and the visit list are compile-time, so the
 // loop keeps fewer kernel parameters live.
-template <bool U8 = false>
+template <bool U8 = false, bool DEFER = false>
 __device__ __forceinline__ StageRaw stage_load(const Geo& g, const std::uint8_t* sing, int grp, int lane,
                                                int sub) {
   StageRaw r;
   r.i = U8 ? grp * 4 + sub : visit_point(g, grp * 4 + sub);
   const int ic = r.i < g.n ? r.i : g.n - 1;
   r.kind = g.kind[ic];
-  r.sing = lane == 0 ? sing[ic] : 0xFF;  // first singular split direction (k_flux_weights)
+  // first singular split direction (k_flux_weights); DEFER: flagged for the redo once per domain
+  r.sing = (!DEFER && lane == 0) ? sing[ic] : 0xFF;
   int e0 = 0, k = 0;
   if constexpr (U8) {
     e0 = 8 * ic;
@@ -1076,8 +1084,21 @@ __device__ __forceinline__ StageIdx stage_index(const Geo& g, const StageRaw& r,
   return x;
 }
 
+// Lanes 0-6 of a point's lane group stage its own record: xy, q (2 halves),
+// qx01 qy01 qx23 qy23 — chunk `lane` is at own_base + ic * own_stride.
+struct OwnSrc {
+  const char* base;
+  long long stride;
+};
+__device__ __forceinline__ OwnSrc own_src(const FluxArgs& a, int lane) {
+  const int c = lane - 3;
+  if (lane == 0) return OwnSrc{reinterpret_cast<const char*>(a.g.xy), 16};
+  if (lane < 3) return OwnSrc{reinterpret_cast<const char*>(a.q) + (lane - 1) * 16, 32};
+  return OwnSrc{reinterpret_cast<const char*>(a.dq + ((c & 1) ? a.g.nloc : 0)) + (c >> 1) * 16, 32};
+}
+
 __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1, const StageIdx& x,
-                                            char* st, int lane32, int lane, int sub) {
+                                            char* st, int lane32, int lane, int sub, const OwnSrc& own) {
   const Geo& g = a.g;
   char* f = st + lane32 * 16;
   cp_async16(f + 0 * 512, g.xy + x.nb, true);
@@ -1091,20 +1112,25 @@ __device__ __forceinline__ void stage_issue(const FluxArgs& a, const double2* w1
   cp_async16(f + 5 * 512, yn, true);
   cp_async16(f + 6 * 512, xn + 16, true);
   cp_async16(f + 7 * 512, yn + 16, true);
-  if (lane < 7) {  // own record of the lane group's point: xy, q (2), qx01 qy01 qx23 qy23
-    char* o = st + kFluxStageChunks * 512 + (sub * 7 + lane) * 16;
-    const int c = lane - 3;
-    const char* src = lane == 0 ? reinterpret_cast<const char*>(g.xy + x.ic)
-                      : lane < 3 ? reinterpret_cast<const char*>(a.q + x.ic) + (lane - 1) * 16
-                                 : reinterpret_cast<const char*>(a.dq + ((c & 1) ? g.nloc : 0) + x.ic) + (c >> 1) * 16;
-    cp_async16(o, src, true);
-  }
+  if (lane < 7) cp_async16(st + kFluxStageChunks * 512 + (sub * 7 + lane) * 16, own.base + x.ic * own.stride, true);
 }
 
-template <int MB, int NW = kFluxWarps, int HP = -1, bool U8 = false>
+// Rare-path deferral (DEFER): a lane whose pair took a rare path flags its
+// point (bit i of the bit set); k_flux_redo recomputes the flagged points with
+// the fallbacks in place and clears the bits.  The singular-split check is not
+// made (a domain with a live singular point — a run that fails in its first
+// flux pass — runs without DEFER, k_flux_any_sing).  bits: kRedoWordsPer *
+// ceil(n / kRedoPointsPer) zero-initialised words (the redo scans uint4 per lane).
+constexpr int kRedoPointsPer = 4096;  // points per warp step of the redo scan
+constexpr int kRedoWordsPer = kRedoPointsPer / 32;
+struct FluxRedo {
+  unsigned* bits;
+};
+
+template <int MB, int NW = kFluxWarps, int HP = -1, bool U8 = false, bool DEFER = false>
 __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const double2* __restrict__ w1,
                                                      const double2* __restrict__ w2,
-                                                     const std::uint8_t* __restrict__ sing) {
+                                                     const std::uint8_t* __restrict__ sing, FluxRedo rd) {
   pdl_enter();
   extern __shared__ __align__(16) char fsm[];
   __shared__ int s_skip;
@@ -1117,21 +1143,23 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
   const int warp = threadIdx.x >> 5;
   char* const stage0 = fsm + (2 * warp) * kFluxStageBytes;  // stage b at stage0 + b * kFluxStageBytes
   const Geo& g = a.g;
+  const OwnSrc own = own_src(a, lane);
   const int groups = ((U8 ? g.n : visit_count(g)) + 3) >> 2;
   const int nwarps = gridDim.x * NW;
   int grp = blockIdx.x * NW + warp;
   if (!s_skip && grp < groups) {
-    StageIdx cur = stage_index(g, stage_load<U8>(g, sing, grp, lane, sub), lane);
-    stage_issue(a, w1, cur, stage0, lane32, lane, sub);
+    StageIdx cur = stage_index(g, stage_load<U8, DEFER>(g, sing, grp, lane, sub), lane);
+    stage_issue(a, w1, cur, stage0, lane32, lane, sub, own);
     cp_async_commit();
-    StageRaw nxt = stage_load<U8>(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
+    StageRaw nxt = stage_load<U8, DEFER>(g, sing, grp + nwarps < groups ? grp + nwarps : grp, lane, sub);
     int buf = 0;
     for (; grp < groups; grp += nwarps, buf ^= 1) {
       const bool more = grp + nwarps < groups;
       const StageIdx nx = stage_index(g, nxt, lane);
-      if (more) stage_issue(a, w1, nx, stage0 + (buf ^ 1) * kFluxStageBytes, lane32, lane, sub);
+      if (more) stage_issue(a, w1, nx, stage0 + (buf ^ 1) * kFluxStageBytes, lane32, lane, sub, own);
       cp_async_commit();
-      const StageRaw nxt2 = stage_load<U8>(g, sing, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
+      const StageRaw nxt2 =
+          stage_load<U8, DEFER>(g, sing, grp + 2 * nwarps < groups ? grp + 2 * nwarps : grp, lane, sub);
       cp_async_wait<1>();
       __syncwarp();
       const char* st = stage0 + buf * kFluxStageBytes;
@@ -1146,15 +1174,17 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
       const double2 oq01 = *reinterpret_cast<const double2*>(o + 16), oq23 = *reinterpret_cast<const double2*>(o + 32);
       const double2 ox01 = *reinterpret_cast<const double2*>(o + 48), oy01 = *reinterpret_cast<const double2*>(o + 64);
       const double2 ox23 = *reinterpret_cast<const double2*>(o + 80), oy23 = *reinterpret_cast<const double2*>(o + 96);
-      if (cur.live && lane == 0 && cur.sing != 0xFF)
+      if (!DEFER && cur.live && lane == 0 && cur.sing != 0xFF)
         raise_err(a.ctl, flux_key(a.ctl, g.part[cur.i], gidx(g, cur.i), cur.sing, kSolveSlot), sub_flux(a.ctl));
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      flux_pair_fast<HP>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
-                     D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
-                     D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
-                     D4{y01.x, y01.y, y23.x, y23.y}, w, w2 ? w2 + cur.e : nullptr, acc);
+      bool redo = false;
+      flux_pair_fast<HP, DEFER>(a, cur.i, lane, cur.act, pi, D4{oq01.x, oq01.y, oq23.x, oq23.y},
+                                D4{ox01.x, ox01.y, ox23.x, ox23.y}, D4{oy01.x, oy01.y, oy23.x, oy23.y}, pn,
+                                D4{q01.x, q01.y, q23.x, q23.y}, D4{x01.x, x01.y, x23.x, x23.y},
+                                D4{y01.x, y01.y, y23.x, y23.y}, w, w2 ? w2 + cur.e : nullptr, acc, &redo);
       const double r = reduce8(acc, lane);
       if (cur.live) store_res8(a.res, cur.i, r, lane);
+      if (DEFER && redo && cur.live) atomicOr(rd.bits + (cur.i >> 5), 1u << (cur.i & 31));
       __syncwarp();  // the stage is refilled two groups on
       cur = nx;
       nxt = nxt2;
@@ -1163,6 +1193,84 @@ __global__ void __launch_bounds__(NW * 32, MB) k_flux_ws(FluxArgs a, const doubl
   }
   __syncthreads();
   ktimer_end(a.ctl, KT_FLUX);
+}
+
+// Any live point with a singular split stencil (once per domain, after k_flux_weights).
+__global__ void k_flux_any_sing(Geo g, const std::uint8_t* __restrict__ sing, unsigned* __restrict__ any) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < g.n && g.kind[i] != KIND_OUTER && sing[i] != 0xFFu) atomicOr(any, 1u);
+}
+
+// The flagged points of a DEFER flux pass, evaluated as k_flux_w does (global
+// loads, fallbacks and failure checks in place: the bits k_flux_ws without
+// DEFER stores).  A warp step scans 4096 flags (a uint4 of bits per lane);
+// flagged points are evaluated four at a time, one per 8-lane group.
+__device__ __forceinline__ void flux_point_redo(const FluxArgs& a, const double2* w1, const double2* w2,
+                                                const std::uint8_t* sing, int i, int lane) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  const Geo& g = a.g;
+  const int ic = i >= 0 ? i : 0;
+  const bool live = i >= 0 && g.kind[ic] != KIND_OUTER;
+  int k = 0, e0 = 0;
+  if (live) stencil_of(g, i, e0, k);
+  const int kwarp = __reduce_max_sync(kFull, k);
+  if (live && lane == 0) {
+    const unsigned sd = sing[i];
+    if (sd != 0xFFu) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), sd, kSolveSlot), sub_flux(a.ctl));
+  }
+  const double2 pi = g.xy[ic];
+  const D4 qi = ld4(a.q + ic);
+  D4 qxi, qyi;
+  dq_load(a.dq, g.nloc, ic, qxi, qyi);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int jb = 0; jb < kwarp; jb += 8) {
+    const int j = jb + lane;
+    const bool act = live && j < k;
+    const int nb = act ? g.nbr[e0 + j] : ic;
+    const double2 w = act ? w1[e0 + j] : make_double2(0.0, 0.0);
+    const D4 qn = ld4(a.q + nb);
+    D4 qxn, qyn;
+    dq_load(a.dq, g.nloc, nb, qxn, qyn);
+    flux_pair_fast(a, i, j, act, pi, qi, qxi, qyi, g.xy[nb], qn, qxn, qyn, w, w2 ? w2 + (e0 + j) : nullptr, acc);
+  }
+  const double r = reduce8(acc, lane);
+  if (live) store_res8(a.res, i, r, lane);
+}
+
+__global__ void __launch_bounds__(256, 2) k_flux_redo(FluxArgs a, const double2* __restrict__ w1,
+                                                      const double2* __restrict__ w2,
+                                                      const std::uint8_t* __restrict__ sing, FluxRedo rd) {
+  pdl_enter();
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  const int lane32 = threadIdx.x & 31;
+  const int lane = threadIdx.x & 7;
+  const int sub = lane32 >> 3;
+  const int n = a.g.n;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRedoPointsPer; base < n;
+       base += nwarps * kRedoPointsPer) {
+    uint4* wp = reinterpret_cast<uint4*>(rd.bits + base / 32) + lane32;
+    const uint4 v = *wp;
+    const bool mine = (v.x | v.y | v.z | v.w) != 0u;
+    unsigned m = __ballot_sync(kFull, mine);
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        unsigned w = __shfl_sync(kFull, c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w, q);
+        const int wbase = base + q * 128 + c * 32;
+        while (w) {  // warp-uniform: group `sub` takes the sub-th lowest flagged point
+          unsigned t = w;
+          for (int s2 = 0; s2 < sub; ++s2) t &= t - 1;
+          const int i = t ? wbase + __ffs(t) - 1 : -1;
+          for (int s2 = 0; s2 < 4; ++s2) w &= w - 1;
+          flux_point_redo(a, w1, w2, sing, i < n ? i : -1, lane);
+        }
+      }
+    }
+    if (mine) *wp = make_uint4(0u, 0u, 0u, 0u);
+  }
 }
 
 // Local time step + forward-Euler update + wall slip + next q-variables +
