@@ -1680,10 +1680,15 @@ class Domain {
     refresh_ctl();
   }
 
-  int launches_per_iter() const {
+  // Kernels of one launch_flux: the point fluxes + gather (order 1), or the
+  // staged kernel + the redo pass of its rare-path points (DEFER), or one.
+  int flux_launches() const {
     const bool pf = !strict_ && weights_ && order_ == 1 && point_flux_enabled() && pf_.get() && kmax_ <= 8;
-    return (order_ == 2 ? inner_ : 0) + (pf ? 2 : 1) + 1 + (strict_ ? 2 : 1);
+    if (pf) return 2;
+    const bool redo = !strict_ && weights_ && kmax_ <= 8 && flux_staged() && flux_defer() && !any_sing_;
+    return redo ? 2 : 1;
   }
+  int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + flux_launches() + 1 + (strict_ ? 2 : 1); }
 
   // Grid of k_update (persistent: at most the resident blocks); fixed per
   // domain, since the iteration index is derived from its completed blocks.
@@ -2638,7 +2643,8 @@ class MultiRun {
     }
   }
   int launches_per_iter() const {
-    return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 3) + (spec_.fp_mode == 1 ? 2 : 1);
+    return P_ * ((spec_.order == 2 ? 2 * spec_.inner : 0) + 2 + dom_[0]->flux_launches()) +
+           (spec_.fp_mode == 1 ? 2 : 1);
   }
 
   // Enqueues n more iterations (stopping early on an error); returns the
@@ -3218,7 +3224,7 @@ class RankRun {
     if (timed) d.record_ext(kev_[3]);
     wait_for(std::vector<int>{0}, FL_RES, 1, 0, spi_ - 2);  // root's residue(t-1) has read the summands
     d.launch_update(a);  // the device iteration index is t + 1 from here on
-    launches_ += 4;      // interior flux, halo, boundary flux, update
+    launches_ += 2 + 2 * d.flux_launches();  // interior flux, halo, boundary flux, update
     signal(FL_UPD, 1, 0);
     if (rank_ == 0) {
       std::vector<int> all;
@@ -3265,7 +3271,7 @@ class RankRun {
     d.launch_flux(a, bfin, spec_.order != 2);
     if (timed) d.record_ext(kev_[3]);
     d.launch_update(a);  // the device iteration index is t + 1 from here on
-    launches_ += 2;      // flux + update
+    launches_ += 1 + d.flux_launches();  // flux + update
     signal(FL_UPD, 1, 0);
     if (rank_ == 0) {
       std::vector<int> all;

@@ -150,7 +150,8 @@ def test_session_pieces_equal_one_run(bump_cloud_arrays):
         s.download()
         names = [k[0] for k in s.kernels()]
         assert names[:2] == ["q_variables", "q_derivatives"] and "flux_residual" in names
-        assert s.info()["launches_per_iter"] == 6  # 3 sweeps, flux, update, exact residue
+        # 3 sweeps, flux (+ the redo pass of its rare-path points for stencils <= 8), update, exact residue
+        assert s.info()["launches_per_iter"] == (7 if np.diff(c.off).max() <= 8 else 6)
     assert pc.fields_equal(whole)
 
 
