@@ -118,6 +118,43 @@ class DBuf {
   cudaStream_t st_ = nullptr;
 };
 
+// Grow-only device scratch per device and slot for the large transient buffers
+// of a run (the copy-back's packed store, the screening's keys and sort
+// space), shared by the process's domains and allocated with plain cudaMalloc:
+// measured at 40M points, taking a 6.7 GB buffer from the stream-ordered pool
+// on a fresh domain's stream stalled a cold lskum_run by 5-550 ms (pool
+// growth), while the pool-backed per-domain buffers of the same sizes did not.
+// A lease holds the slot until the holder's stream work on it is synchronised.
+enum : int { kScratchPack = 0, kScratchScreen = 1, kScratchSlots = 2 };
+class ScratchLease {
+ public:
+  ScratchLease(int device, int slot, std::size_t bytes) : e_(entry(device, slot)), lk_(e_.m) {
+    if (e_.bytes < bytes) {
+      if (e_.p) ck(cudaFree(e_.p), "cudaFree(scratch)");
+      e_.p = nullptr;
+      e_.bytes = 0;
+      ck(cudaMalloc(&e_.p, bytes), "cudaMalloc(scratch)");
+      e_.bytes = bytes;
+    }
+  }
+  ScratchLease(const ScratchLease&) = delete;
+  ScratchLease& operator=(const ScratchLease&) = delete;
+  char* get() const { return static_cast<char*>(e_.p); }
+
+ private:
+  struct Entry {
+    std::mutex m;
+    void* p = nullptr;
+    std::size_t bytes = 0;
+  };
+  static Entry& entry(int device, int slot) {
+    static Entry tab[64][kScratchSlots];
+    return tab[device & 63][slot];
+  }
+  Entry& e_;
+  std::unique_lock<std::mutex> lk_;
+};
+
 // Small pinned host blocks (control words, poll slots) are recycled through a
 // process-wide free list: cudaHostAlloc costs about a millisecond per call,
 // which a fresh domain would otherwise pay several times.
@@ -1371,14 +1408,24 @@ class Domain {
     DBuf<ScreenOut> so(1, st_);
     ScreenOut init{0, 0, 0, 0x7FFFFFFF, 0};
     ck(cudaMemcpyAsync(so.get(), &init, sizeof init, cudaMemcpyHostToDevice, st_), "H2D screen");
-    DBuf<unsigned long long> keys(static_cast<std::size_t>(n), st_), sorted(static_cast<std::size_t>(n), st_);
-    trace_sync(st_, "screen: buffers");
-    k_screen_keys<<<(n + 255) / 256, 256, 0, st_>>>(n, mind_.get(), keys.get(), so.get());
+    // keys, sorted keys, the sort's temporary space and the defect list in one scratch lease
     std::size_t tmp_bytes = 0;
-    ck(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort size");
-    DBuf<char> tmp(std::max<std::size_t>(1, tmp_bytes), st_);
+    ck(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, static_cast<unsigned long long*>(nullptr),
+                                      static_cast<unsigned long long*>(nullptr), n, 0, 64, st_),
+       "sort size");
+    auto up = [](std::size_t b) { return (b + 255) & ~static_cast<std::size_t>(255); };
+    const std::size_t kb = up(static_cast<std::size_t>(n) * sizeof(unsigned long long));
+    const std::size_t tb = up(std::max<std::size_t>(1, tmp_bytes));
+    const std::size_t bb = up(static_cast<std::size_t>(n) * sizeof(int));
+    ScratchLease scr(device_, kScratchScreen, 2 * kb + tb + bb);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(scr.get());
+    unsigned long long* sorted = reinterpret_cast<unsigned long long*>(scr.get() + kb);
+    char* tmp = scr.get() + 2 * kb;
+    int* bad = reinterpret_cast<int*>(scr.get() + 2 * kb + tb);
+    trace_sync(st_, "screen: buffers");
+    k_screen_keys<<<(n + 255) / 256, 256, 0, st_>>>(n, mind_.get(), keys, so.get());
     trace_sync(st_, "screen: keys");
-    ck(cub::DeviceRadixSort::SortKeys(tmp.get(), tmp_bytes, keys.get(), sorted.get(), n, 0, 64, st_), "sort");
+    ck(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, n, 0, 64, st_), "sort");
     trace_sync(st_, "screen: sorted");
     ScreenOut head{};
     ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
@@ -1397,13 +1444,12 @@ class Domain {
     ck(cudaStreamSynchronize(st_), "screen keys");
     if (head.n_finite > 0) {
       unsigned long long bits = 0;
-      ck(cudaMemcpy(&bits, sorted.get() + (head.n_finite - 1) / 2, sizeof bits, cudaMemcpyDeviceToHost), "D2H h_ref");
+      ck(cudaMemcpy(&bits, sorted + (head.n_finite - 1) / 2, sizeof bits, cudaMemcpyDeviceToHost), "D2H h_ref");
       std::memcpy(&out.h_ref, &bits, sizeof bits);
     }
     out.det_tol = 1e-12 * out.h_ref * out.h_ref * out.h_ref * out.h_ref;  // cloud.cpp:274
     const int cap = n;
-    DBuf<int> bad(static_cast<std::size_t>(cap), st_);
-    k_screen<<<(n + 255) / 256, 256, 0, st_>>>(geo(), out.det_tol, so.get(), bad.get(), cap);
+    k_screen<<<(n + 255) / 256, 256, 0, st_>>>(geo(), out.det_tol, so.get(), bad, cap);
     ck(cudaGetLastError(), "k_screen");
     ck(cudaMemcpyAsync(&head, so.get(), sizeof head, cudaMemcpyDeviceToHost, st_), "D2H screen");
     ck(cudaStreamSynchronize(st_), "screen");
@@ -1412,7 +1458,7 @@ class Domain {
     out.min_stencil = head.min_size;
     out.defective.resize(static_cast<std::size_t>(head.n_defective));
     if (head.n_defective > 0) {
-      ck(cudaMemcpy(out.defective.data(), bad.get(), sizeof(int) * head.n_defective, cudaMemcpyDeviceToHost),
+      ck(cudaMemcpy(out.defective.data(), bad, sizeof(int) * head.n_defective, cudaMemcpyDeviceToHost),
          "D2H defective");
       for (auto& p : out.defective) p = global_of(p);  // point ids of the cloud
       std::sort(out.defective.begin(), out.defective.end());
@@ -1509,11 +1555,12 @@ class Domain {
         return;
       }
       cudaGetLastError();
-      DBuf<double> packed(21 * n, st_);
+      ScratchLease packed_lease(device_, kScratchPack, 21 * n * sizeof(double));
+      double* const packed = reinterpret_cast<double*>(packed_lease.get());
       auto pack = [&](int lo, int hi) {
         k_pack_fields<<<std::max(1, std::min<int>((hi - lo + 255) / 256, 4096)), 256, 0, st_>>>(
             n_, lo, hi, soa ? 1 : 0, prim_.get(), qsrc, dqsrc, static_cast<long long>(n_loc_), res_.get(), dt_.get(),
-            static_cast<const int*>(gid_.get()), packed.get());
+            static_cast<const int*>(gid_.get()), packed);
         ck(cudaGetLastError(), "k_pack_fields");
       };
       if (f.pinned()) {  // the store is pinned: DMA straight into it
@@ -1535,10 +1582,10 @@ class Domain {
             if (err == cudaSuccess) err = cudaStreamWaitEvent(cs, packed_ev[c], 0);
             if (err != cudaSuccess) break;
             if (soa)
-              err = cudaMemcpy2DAsync(f.raw() + lo, n * sizeof(double), packed.get() + lo, n * sizeof(double),
+              err = cudaMemcpy2DAsync(f.raw() + lo, n * sizeof(double), packed + lo, n * sizeof(double),
                                       (hi - lo) * sizeof(double), 21, cudaMemcpyDeviceToHost, cs);
             else
-              err = cudaMemcpyAsync(f.raw() + 21ll * lo, packed.get() + 21ll * lo, 21ll * (hi - lo) * sizeof(double),
+              err = cudaMemcpyAsync(f.raw() + 21ll * lo, packed + 21ll * lo, 21ll * (hi - lo) * sizeof(double),
                                     cudaMemcpyDeviceToHost, cs);
           }
           trace("download: chunks queued");
@@ -1549,7 +1596,7 @@ class Domain {
           ck(serr, "download (copy stream)");
         } else {
           pack(0, n_);
-          ck(cudaMemcpyAsync(f.raw(), packed.get(), 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
+          ck(cudaMemcpyAsync(f.raw(), packed, 21 * n * sizeof(double), cudaMemcpyDeviceToHost, st_),
              "D2H fields");
         }
         ck(cudaStreamSynchronize(st_), "download");
@@ -1569,7 +1616,7 @@ class Domain {
       for (int c = 0; c < chunks; ++c) {
         const std::size_t lo = lo_of(c), hi = lo_of(c + 1);
         ck(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaMemcpyAsync(h + lo, packed.get() + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, st_),
+        ck(cudaMemcpyAsync(h + lo, packed + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, st_),
            "D2H fields");
         ck(cudaEventRecord(done[c], st_), "cudaEventRecord");
       }
