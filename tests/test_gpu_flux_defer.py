@@ -96,3 +96,53 @@ def test_deferred_rare_paths_are_bitwise_the_inline_fallbacks(maker, mach, iters
     assert np.array_equal(res, np.load(out + "_res.npy"))
     assert np.array_equal(f, np.load(out + "_f.npy"))
     assert np.any(f[:, 16:20] != 0.0) and np.all(np.isfinite(f))
+
+
+def _supersonic_naca_arrays(nw, nr, mach):
+    c = L.Cloud.generate_naca0012(nw, nr, 20.0, 0.0, 7, 8, frozen_wall=True)
+    g = c.geometry()
+    c.close()
+    a = np.radians(1.0)
+    prim = np.tile([1.0, mach * np.cos(a), mach * np.sin(a), 1.0 / 1.4], (len(g["x"]), 1))
+    w = 0.05 * np.exp(-((g["x"] + 0.5) ** 2 + (g["y"] - 0.3) ** 2) / 0.02)
+    prim[:, 0] *= 1.0 + w
+    prim[:, 3] *= 1.0 + w
+    return (g["x"], g["y"], g["kind"], g["nx"], g["ny"], g["off"], g["nbr"]), prim
+
+
+def _single(arrays, prim, iters, **cfg):
+    pc = L.Cloud.from_arrays(*arrays)
+    pc.reset_store(0)
+    pc.set_primitives(prim)
+    res = L.run_fixed_point(pc, L.Config(iters=iters, **cfg))
+    return pc, res.residues()
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_redo_pass_in_multi_domain_runs_is_bitwise_single_domain(gpus):
+    """Several domains on the device (MultiRun): each domain's flux pass lists
+    and redoes its own supersonic points; the run equals the one-domain run."""
+    arrays, prim = _supersonic_naca_arrays(400, 200, 2.0)
+    cfg = dict(mach=2.0, aoa=1.0, order=2, inner=3, cfl=0.5)
+    one, r1 = _single(arrays, prim, 6, **cfg)
+    many, rn = _single(arrays, prim, 6, gpus=gpus, **cfg)
+    assert np.array_equal(rn, r1)
+    assert many.fields_equal(one)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_redo_pass_in_rank_runs_is_bitwise_single_domain(world):
+    """One process per rank, interior and boundary flux passes (each followed
+    by its redo pass) on supersonic flow: bitwise the one-domain run."""
+    import rank_worker as W
+
+    arrays, prim = _supersonic_naca_arrays(400, 200, 2.0)
+    cfg = dict(mach=2.0, aoa=1.0, order=2, inner=3, cfl=0.5)
+    one, r1 = _single(arrays, prim, 6, **cfg)
+    want_f = one.fields()
+    out = W.launch(W.run_rank, world, arrays, prim, cfg, [2, 4], 0)
+    assert all(v[0] == "ok" for v in out), out
+    assert np.array_equal(out[0][1], r1)
+    owned, _ = L.partition(L.Cloud.from_arrays(*arrays), world)
+    for r, v in enumerate(out):
+        assert np.array_equal(v[2][owned[r]], want_f[owned[r]]), r
