@@ -783,11 +783,14 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   constexpr unsigned kFull = 0xFFFFFFFFu;
   const Geo& g = a.g;
   const double dx = X::sub(pn.x, pi.x), dy = X::sub(pn.y, pi.y);
+  // q~ = q - (dx/2) qx - (dy/2) qy as two FMAs per component (the reference's
+  // q - 0.5 (dx qx + dy qy) regrouped; a uniform field stays exact)
+  const double hdx = -0.5 * dx, hdy = -0.5 * dy;
   double ti[4], tn[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    ti[c] = corrected<false>(comp(qi, c), comp(qxi, c), comp(qyi, c), dx, dy);
-    tn[c] = corrected<false>(comp(qn, c), comp(qxn, c), comp(qyn, c), dx, dy);
+    ti[c] = fma(hdx, comp(qxi, c), fma(hdy, comp(qyi, c), comp(qi, c)));
+    tn[c] = fma(hdx, comp(qxn, c), fma(hdy, comp(qyn, c), comp(qn, c)));
   }
   bool ok = ti[3] < 0.0 && tn[3] < 0.0;
   if (!ok) {  // q3 >= 0 has no state: evaluate a dummy one, add nothing
