@@ -1073,6 +1073,7 @@ Gas make_gas(double gamma, double cfl, double det_tol) {
   g.gamma = gamma;
   g.gm1 = gamma - 1.0;
   g.inv_gm1 = 1.0 / (gamma - 1.0);
+  g.ep_fac = g.inv_gm1 + 1.0;
   g.cfl = cfl;
   g.det_tol = det_tol;
   const double m = 2.0 / (gamma - 1.0);

@@ -799,7 +799,7 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   }
   FluxState fi, fn;
   bool rd = false;
-  ok = reconstruct2<false, HP, DEFER>(ti, tn, a.gas, fi, fn, rd) && ok;
+  ok = reconstruct2<false, HP, DEFER, true>(ti, tn, a.gas, fi, fn, rd) && ok;
   if constexpr (DEFER) rd |= act && !ok;
   else if (act && !ok) raise_err(a.ctl, flux_key(a.ctl, g.part[i], gidx(g, i), dx <= 0.0 ? 0u : 1u, j), sub_flux(a.ctl));
   AxisTerms at[4];
@@ -811,8 +811,8 @@ __device__ __forceinline__ void flux_pair_fast(const FluxArgs& a, int i, int j, 
   // fma(rho_n, x_n, -gi) would leave ~1 ulp where the states are equal
   // (the free stream must stay an exact fixed point).
   double gi[4], gn[4];
-  const double epi = fi.e + fi.p, kki = -0.5 * fi.p;  // kk: -p/2 of split_flux_fast
-  const double epn = fn.e + fn.p, kkn = -0.5 * fn.p;
+  const double epi = fi.e, kki = -0.5 * fi.p;  // fi.e = rhoE + p here; kk: -p/2 of split_flux_fast
+  const double epn = fn.e, kkn = -0.5 * fn.p;
   split_flux_fast<0>(fi, at[0], !(dx <= 0.0), epi, kki, gi);
   split_flux_fast<0>(fn, at[1], !(dx <= 0.0), epn, kkn, gn);
 #pragma unroll
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(256) k_point_flux(int n_loc, const D4* __restr
   ok = reconstruct1_fast(t, gas, f) && ok;
   AxisTerms at[2];
   axis_terms2_fast(f, at);
-  const double ep = f.e + f.p, kk = -0.5 * f.p;  // -p/2 of split_flux_fast
+  const double ep = f.e, kk = -0.5 * f.p;  // f.e = rhoE + p; kk: -p/2 of split_flux_fast
   double gv[4];
   split_flux_fast<0>(f, at[0], false, ep, kk, gv);
   st4(&pf[i].g[0], D4{gv[0], gv[1], gv[2], gv[3]});
