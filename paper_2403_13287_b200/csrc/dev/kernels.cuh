@@ -1413,16 +1413,20 @@ __device__ __forceinline__ double acc_to_double(unsigned long long* d) {
 // (0 for outer points and for a failing point, whose error is recorded).
 __device__ __forceinline__ double update_point(const UpdateArgs& a, int ip, bool diag) {
   const Geo& g = a.g;
-  if (g.kind[ip] == KIND_OUTER) {
+  // every input in one round trip (the kind no longer gates the other loads;
+  // outer points, a thin ring, read res/prim/mind for nothing)
+  const unsigned kind = g.kind[ip];
+  const D4 r = ld4(a.res + ip);
+  const D4 s = ld4_rw(a.prim + ip);
+  const double mind = g.mind[ip];
+  if (kind == KIND_OUTER) {
     st4(a.q_next + ip, ld4(a.q + ip));
     if (diag) a.dt[ip] = 0.0;
     return 0.0;
   }
-  const D4 r = ld4(a.res + ip);
-  const D4 s = ld4_rw(a.prim + ip);
   const double speed = sqrt(X::add(X::mul(s.b, s.b), X::mul(s.c, s.c)));
   const double sound = sqrt(X::mul(a.gas.gamma, s.d) / s.a);
-  const double dt = X::mul(a.gas.cfl, g.mind[ip]) / X::add(speed, sound);
+  const double dt = X::mul(a.gas.cfl, mind) / X::add(speed, sound);
   double m = s.a, mx = X::mul(s.a, s.b), my_ = X::mul(s.a, s.c);
   double en = X::add(s.d / a.gas.gm1,
                      X::mul(X::mul(0.5, s.a), X::add(X::mul(s.b, s.b), X::mul(s.c, s.c))));
@@ -1445,7 +1449,7 @@ __device__ __forceinline__ double update_point(const UpdateArgs& a, int ip, bool
     raise_err(a.ctl, err_key(PH_UPDATE, g.part[ip], gidx(g, ip), 0, 0), sub_update(a.ctl));
     return 0.0;
   }
-  if (g.kind[ip] == KIND_WALL) {
+  if (kind == KIND_WALL) {
     const double2 nv = g.nrm[ip];
     const double un = X::add(X::mul(u1, nv.x), X::mul(u2, nv.y));
     u1 = X::sub(u1, X::mul(un, nv.x));
