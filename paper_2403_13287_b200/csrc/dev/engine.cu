@@ -130,11 +130,15 @@ class ScratchLease {
  public:
   ScratchLease(int device, int slot, std::size_t bytes) : e_(entry(device, slot)), lk_(e_.m) {
     if (e_.bytes < bytes) {
+      int prev = 0;
+      ck(cudaGetDevice(&prev), "cudaGetDevice");
+      ck(cudaSetDevice(device), "cudaSetDevice");  // the slot's device, whatever is current
       if (e_.p) ck(cudaFree(e_.p), "cudaFree(scratch)");
       e_.p = nullptr;
       e_.bytes = 0;
       ck(cudaMalloc(&e_.p, bytes), "cudaMalloc(scratch)");
       e_.bytes = bytes;
+      ck(cudaSetDevice(prev), "cudaSetDevice");
     }
   }
   ScratchLease(const ScratchLease&) = delete;
