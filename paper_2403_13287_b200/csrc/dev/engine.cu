@@ -649,15 +649,18 @@ bool flux_u8() {
 }
 
 // Rare-path deferral of the staged flux kernel (k_flux_ws<.., DEFER>, then
-// k_flux_redo over the points it listed); LSKUM_FLUX_DEFER=0 keeps the
-// fallback branches inside the staged kernel.
-bool flux_defer() {
+// k_flux_redo over the points it flagged).  LSKUM_FLUX_DEFER: 1 (default)
+// per run from the initial state (Domain::probe_defer), 0 never (fallback
+// branches inside the staged kernel), 2 always (tests of the redo path).
+int flux_defer_mode() {
   static int v = [] {
     const char* e = std::getenv("LSKUM_FLUX_DEFER");
-    return (e && std::atoi(e) == 0) ? 0 : 1;
+    const int m = e ? std::atoi(e) : 1;
+    return m < 0 || m > 2 ? 1 : m;
   }();
-  return v != 0;
+  return v;
 }
+bool flux_defer() { return flux_defer_mode() != 0; }
 
 template <int MB, int NW, int HP, bool U8, bool DEFER>
 void flux_ws_launch_k(const FluxArgs& a, const double2* w1, const double2* w2, const std::uint8_t* sing,
@@ -1723,6 +1726,29 @@ class Domain {
     g.n = n_loc_;
     k_qvar<<<(n_loc_ + 255) / 256, 256, 0, st_>>>(g, prim_.get(), q_[0].get(), gas_, ctl_.get());
     ck(cudaGetLastError(), "k_qvar");
+    probe_defer();
+  }
+  // Whether this run defers the flux's rare paths: only while few points take
+  // them (measured at 10M points: deferral 3.65 vs 3.78 ms per iteration up to
+  // M 1.6, but 10.7 vs 4.65 ms at M 2, where every point goes through the
+  // redo).  Decided from the run's initial state; both choices give the same
+  // bits.  Captured graphs bake the choice in.
+  void probe_defer() {
+    bool defer = false;
+    if (!strict_ && weights_ && flux_defer_mode() == 2 && !any_sing_) {
+      defer = true;
+    } else if (!strict_ && weights_ && flux_defer() && !any_sing_ && n_ > 0) {
+      DBuf<unsigned> cnt(1, st_);
+      ck(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned), st_), "zero probe");
+      k_defer_probe<<<std::min((n_ + 255) / 256, 4096), 256, 0, st_>>>(geo(), prim_.get(), cnt.get());
+      ck(cudaGetLastError(), "k_defer_probe");
+      unsigned h = 0;
+      ck(cudaMemcpyAsync(&h, cnt.get(), sizeof h, cudaMemcpyDeviceToHost, st_), "D2H probe");
+      ck(cudaStreamSynchronize(st_), "probe");
+      defer = static_cast<long long>(h) * 100 <= static_cast<long long>(n_);  // <= 1% of the points
+    }
+    if (defer != defer_run_) clear_graphs();
+    defer_run_ = defer;
   }
   void begin_run(int order, int inner, int fp_mode, int chunk) {
     reset_run(order, inner, fp_mode, chunk, true);
@@ -1737,7 +1763,7 @@ class Domain {
   int flux_launches() const {
     const bool pf = !strict_ && weights_ && order_ == 1 && point_flux_enabled() && pf_.get() && kmax_ <= 8;
     if (pf) return 2;
-    const bool redo = !strict_ && weights_ && kmax_ <= 8 && flux_staged() && flux_defer() && !any_sing_;
+    const bool redo = !strict_ && weights_ && kmax_ <= 8 && flux_staged() && defer_run_;
     return redo ? 2 : 1;
   }
   int launches_per_iter() const { return (order_ == 2 ? inner_ : 0) + flux_launches() + 1 + (strict_ ? 2 : 1); }
@@ -1911,7 +1937,7 @@ class Domain {
                  static_cast<const std::uint8_t*>(psign_.get()));
     } else if (!strict_ && weights_) {
       const FluxRedo rd{redo_bits_.get()};
-      flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), any_sing_ ? nullptr : &rd, st_);
+      flux_w_launch(fa, kmax_, w1_.get(), w2_.get(), sing_.get(), defer_run_ ? &rd : nullptr, st_);
     } else {
       flux_launch(W_, strict_, fa, smem_, st_);
     }
@@ -2382,6 +2408,7 @@ class Domain {
   DBuf<std::uint8_t> sing_;     // first singular split direction per point
   DBuf<unsigned> redo_bits_;       // flux points whose evaluation took a rare path (k_flux_redo)
   bool any_sing_ = false;          // a live point has a singular split stencil: no deferral
+  bool defer_run_ = false;         // this run defers the flux's rare paths (probe_defer)
   bool weights_ = false;
   DBuf<Ctl> ctl_;
   DBuf<Shared> sh_;

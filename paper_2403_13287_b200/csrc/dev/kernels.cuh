@@ -1204,6 +1204,25 @@ __global__ void k_flux_any_sing(Geo g, const std::uint8_t* __restrict__ sing, un
   if (i < g.n && g.kind[i] != KIND_OUTER && sing[i] != 0xFFu) atomicOr(any, 1u);
 }
 
+// Points whose state has a velocity component at or above 1.35 sqrt(2 p / rho)
+// (|s| >= 1.35 where the erf fast path ends at 1.5; invalid states count too):
+// k_flux_redo's share of a flux pass is about this fraction of the points, so
+// the engine keeps the deferral only while it is small (Domain::probe_defer).
+__global__ void k_defer_probe(Geo g, const D4* __restrict__ prim, unsigned* __restrict__ count) {
+  constexpr unsigned kFull = 0xFFFFFFFFu;
+  for (int base = blockIdx.x * blockDim.x; base < g.n; base += gridDim.x * blockDim.x) {
+    const int i = base + static_cast<int>(threadIdx.x);
+    bool hit = false;
+    if (i < g.n && g.kind[i] != KIND_OUTER) {
+      const D4 s = ld4(prim + i);
+      const double um = fmax(fabs(s.b), fabs(s.c));
+      hit = !(um * um * (0.5 * s.a / s.d) < 1.35 * 1.35);
+    }
+    const unsigned m = __ballot_sync(kFull, hit);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, static_cast<unsigned>(__popc(m)));
+  }
+}
+
 // The flagged points of a DEFER flux pass, evaluated as k_flux_w does (global
 // loads, fallbacks and failure checks in place: the bits k_flux_ws without
 // DEFER stores).  A warp step scans 4096 flags (a uint4 of bits per lane);
