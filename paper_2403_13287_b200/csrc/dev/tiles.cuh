@@ -27,7 +27,7 @@
 
 namespace lskd {
 
-constexpr int kTileIv = 8;     // intervals per tile (more: the tile is gathered from global memory)
+constexpr int kTileIv = 8;  // intervals per tile (more: the tile is gathered from global memory)
 constexpr int kTileGap = 16;   // id gaps up to this are staged instead of starting a new interval
 constexpr int kTileRec = 112;  // staged bytes per point: xy 16 + q 32 + qx 32 + qy 32
 
@@ -43,7 +43,9 @@ struct TilePlan {
   int pad;
   TileIv iv[kTileIv];
 };
-static_assert(sizeof(TilePlan) == 80, "TilePlan is bulk-copied as 80 bytes");
+constexpr unsigned kPlanBytes = sizeof(TilePlan);            // bulk-copied with the stage before
+constexpr int kPlanSlot = (static_cast<int>(sizeof(TilePlan)) + 127) / 128 * 128;  // its room in a stage
+static_assert(sizeof(TilePlan) % 16 == 0, "TilePlan is bulk-copied");
 
 // One block per tile of TP points (uniform 8-point stencils): sort the tile's
 // 9 TP ids (own + neighbours), cut them into intervals at gaps > kTileGap,
@@ -189,7 +191,7 @@ struct SmemSrc {  // a staged tile
 // [128, 128 + 16 TP) the tile's neighbour slots, then xy [smax] x 16 B,
 // q [smax] x 32 B, qx [smax] x 32 B, qy [smax] x 32 B.
 __host__ __device__ constexpr std::size_t tile_stage_bytes(int tp, int smax) {
-  return 128 + 16 * static_cast<std::size_t>(tp) + static_cast<std::size_t>(smax) * kTileRec;
+  return kPlanSlot + 16 * static_cast<std::size_t>(tp) + static_cast<std::size_t>(smax) * kTileRec;
 }
 
 // The tiled sweep: 2 TP threads per block (two lanes per point), persistent
@@ -229,8 +231,8 @@ __global__ void __launch_bounds__(2 * TP, MB)
   const bool run = !s_skip;
   const std::size_t sb = tile_stage_bytes(TP, smax);
   auto stage = [&](int s) { return tsm + s * sb; };
-  auto slots_of = [&](int s) { return stage(s) + 128; };
-  auto xy_of = [&](int s) { return stage(s) + 128 + 16 * TP; };
+  auto slots_of = [&](int s) { return stage(s) + kPlanSlot; };
+  auto xy_of = [&](int s) { return stage(s) + kPlanSlot + 16 * TP; };
   auto q_of = [&](int s) { return xy_of(s) + static_cast<std::size_t>(smax) * 16; };
   auto qx_of = [&](int s) { return xy_of(s) + static_cast<std::size_t>(smax) * 48; };
   auto qy_of = [&](int s) { return xy_of(s) + static_cast<std::size_t>(smax) * 80; };
@@ -257,11 +259,11 @@ __global__ void __launch_bounds__(2 * TP, MB)
     __syncwarp();  // every lane has read the plan (it may live in the stage being refilled)
     if (lane == 0) {
       cur[s] = make_int2(nint, own);
-      const unsigned bytes = (next < ntiles ? 80u : 0u) + 16u * npts + static_cast<unsigned>(staged) * kTileRec;
+      const unsigned bytes = (next < ntiles ? kPlanBytes : 0u) + 16u * npts + static_cast<unsigned>(staged) * kTileRec;
       mbar_arrive_tx(&full[s], bytes);
     }
     __syncwarp();
-    if (lane == 0 && next < ntiles) bulk_g2s(stage(s), plan + tile_at(next), 80u, &full[s]);
+    if (lane == 0 && next < ntiles) bulk_g2s(stage(s), plan + tile_at(next), kPlanBytes, &full[s]);
     if (lane == 1) bulk_g2s(slots_of(s), slot + 8ll * tile * TP, 16u * npts, &full[s]);
     if (len > 0) {
       bulk_g2s(xy_of(s) + off * 16, g.xy + start, len * 16u, &full[s]);
