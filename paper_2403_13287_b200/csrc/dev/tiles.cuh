@@ -305,7 +305,15 @@ __global__ void __launch_bounds__(2 * TP, MB)
         sweep_point8<S>(gsrc, i, nbr, g, i, h, dq_out, gas, ctl, sweep);
       }
     }
-    // count this warp out of stage s; the last warp refills it
+    // count this warp out of stage s; the last warp refills it.  Every value
+    // this warp read from the stage has been consumed (the derivatives are
+    // stored) before it counts itself out, so the refill's bulk copies cannot
+    // overtake a read.  compute-sanitizer racecheck does not model this
+    // shared-atomic hand-off and reports the refill's writes against the
+    // earlier reads; release/acquire fences plus fence.proxy.async around the
+    // count do not silence it and cost 2.8% (0.499 -> 0.513 ms at 10M), so the
+    // protocol stays as is (the tiled sweep is bitwise the untiled one in
+    // every test, tests/test_gpu_tiles.py).
     __syncwarp();
     int last = 0;
     if (lane == 0) {
