@@ -61,3 +61,28 @@ def test_direct_upload_and_chunked_copy_back_are_bitwise_the_staged_paths(layout
     assert np.array_equal(res, np.load(out + "_res.npy"))
     assert np.array_equal(f, np.load(out + "_f.npy"))
     assert np.any(f[:, 8:16] != 0.0) and np.all(np.isfinite(f))
+
+
+def test_fresh_handles_reuse_the_device_scratch_bitwise():
+    """The copy-back's packed store and the screening buffers live in grow-only
+    per-device scratch shared by the process's domains (engine.cu ScratchLease):
+    a smaller cloud after a larger one, then the larger again, each on a fresh
+    handle, give the same bits as the first run of that size."""
+    def run(nw, nr):
+        c = L.Cloud.generate_naca0012(nw, nr, 20.0, 0.0, 7, 8, frozen_wall=True)
+        c.reset_store(0)
+        g = c.geometry()
+        a = np.radians(1.0)
+        prim = np.tile([1.0, 0.85 * np.cos(a), 0.85 * np.sin(a), 1.0 / 1.4], (c.n, 1))
+        prim[:, 0] *= 1.0 + 0.02 * np.exp(-((g["x"] + 0.5) ** 2 + (g["y"] - 0.3) ** 2) / 0.02)
+        c.set_primitives(prim)
+        res = L.run_fixed_point(c, L.Config(mach=0.85, aoa=1.0, iters=3, order=2, inner=3, cfl=0.5))
+        out = (res.residues(), c.fields())
+        c.close()
+        return out
+
+    big1 = run(1000, 625)
+    small = run(400, 200)
+    big2 = run(1000, 625)
+    assert np.array_equal(big1[0], big2[0]) and np.array_equal(big1[1], big2[1])
+    assert small[1].shape[0] == 80000 and np.all(np.isfinite(small[1]))
